@@ -1,0 +1,123 @@
+/*
+ * fasted.h -- C ABI of libfasted.so, the B200 (sm_100a) FaSTED epsilon
+ * self-join engine.
+ *
+ * Plain pointers and sizes only.  Every data pointer is DEVICE memory owned
+ * by the caller (torch tensors in the Python drop-in); every call is
+ * asynchronous on `stream` (a cudaStream_t passed as void*, NULL = legacy
+ * default stream) unless stated otherwise.  Thread-safe: one host thread per
+ * device may call concurrently (all state is per call).
+ *
+ * Status codes mirror the reference's exception classes
+ * (/root/reference/pkg/src/mpjoin/errors.py:4-29 and the CLI exit-code map,
+ * cli.py:56-59,588-607):
+ *   0 FASTED_OK
+ *   2 FASTED_ERR_ARGUMENT   -> ArgumentError / ConfigError
+ *   3 FASTED_ERR_RANGE      -> RangeError (FP16 overflow in quantisation)
+ *   4 FASTED_ERR_CAPACITY   -> result buffer too small (count still exact)
+ *   5 FASTED_ERR_CUDA       -> CUDA runtime / launch failure
+ *   6 FASTED_ERR_UNSUPPORTED-> device is not sm_100 (no silent fallback)
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/mpjoin):
+ *   fasted_quantize  : dataset.to_half            dataset.py:164-193
+ *                      + _kernel.squared_norms_rz _kernel.py:79-93
+ *   fasted_norms     : dataset.compute_squared_norms dataset.py:159-161
+ *   fasted_join      : tiling.self_join's sweep   tiling.py:307-344
+ *                      (work queue + compute_block_tile tiling.py:199-285
+ *                       + _kernel.accumulate_panel _kernel.py:57-76
+ *                       + combine_distance mma.py:143-157); a 128x128 range
+ *                      is compute_block_tile itself
+ *   fasted_sort_pairs: tiling.make_result_set     tiling.py:116-122
+ *                      (and the merge, tiling.py:346-351)
+ */
+#ifndef FASTED_H_
+#define FASTED_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FASTED_ABI_VERSION 1
+
+enum {
+    FASTED_OK = 0,
+    FASTED_ERR_ARGUMENT = 2,
+    FASTED_ERR_RANGE = 3,
+    FASTED_ERR_CAPACITY = 4,
+    FASTED_ERR_CUDA = 5,
+    FASTED_ERR_UNSUPPORTED = 6
+};
+
+/* fasted_join flags */
+enum {
+    FASTED_JOIN_TC = 0,     /* tcgen05/TMEM fused kernel (the product path)          */
+    FASTED_JOIN_EXACT = 1,  /* CUDA-core FFMA.RZ kernel, bit-exact with the reference */
+    FASTED_JOIN_COUNT = 2   /* OR-able: count only, write no records                 */
+};
+
+int fasted_abi_version(void);
+const char* fasted_strerror(int status);
+/* Message of the last failing call on this host thread ("" if none). */
+const char* fasted_last_error(void);
+/* 0 if `device` is an sm_100 part this library can drive, else 6. */
+int fasted_device_check(int device);
+
+/*
+ * FP32 [n, d] row-major -> FP16 [n_pad, d_pad] row-major (RNE, zero padded)
+ * plus per-row FP32 squared norms accumulated round-toward-zero in
+ * ascending k over all d_pad columns (bit-exact with to_half).
+ * n_pad >= n, d_pad >= d, d_pad % 8 == 0.
+ * On FP16 overflow returns FASTED_ERR_RANGE after the stream syncs, with
+ * *first_overflow_host = row-major flat index (i*d + k) of the first value
+ * whose cast is +-inf (the point/dimension RangeError names).  This call
+ * synchronises `stream` to read the overflow flag.
+ */
+int fasted_quantize(const float* x, int64_t n, int64_t d, uint16_t* values16,
+                    int64_t n_pad, int64_t d_pad, float* norms,
+                    int64_t* first_overflow_host, void* stream);
+
+/* RZ squared norms of an existing FP16 [n_pad, d_pad] matrix. */
+int fasted_norms(const uint16_t* values16, int64_t n_pad, int64_t d_pad, float* norms,
+                 void* stream);
+
+/*
+ * Epsilon join over point rows [row_begin, row_end) x columns
+ * [col_begin, col_end) of the FP16 matrix; all four bounds multiples of 128
+ * (or the end == n_pad), n_pad % 128 == 0, d_pad % 16 == 0.
+ * A pair (i, j) qualifies iff i, j < n_logical and
+ *   max(((-2 a_ij) + s_i) + s_j, 0) <= eps_sq           (tiling.py:273-279)
+ * with i == j forced to distance 0 (the reference's self-distance is
+ * exactly 0, tiling.py:13-14).  Records (1-based uint32 i, j and FP32
+ * dist_sq) go to out_i/out_j/out_d in UNSPECIFIED order, only while the
+ * running index < capacity; *count (device, zeroed by this call) receives
+ * the exact total, so a caller whose buffer was too small can resize and
+ * rerun.  With FASTED_JOIN_COUNT the out_* pointers may be NULL.
+ */
+int fasted_join(const uint16_t* values16, const float* norms, int64_t n_logical,
+                int64_t n_pad, int64_t d_pad, int64_t row_begin, int64_t row_end,
+                int64_t col_begin, int64_t col_end, float eps_sq, int flags,
+                uint32_t* out_i, uint32_t* out_j, float* out_d, uint64_t capacity,
+                unsigned long long* count, void* stream);
+
+/*
+ * Canonical (i, j) order for `count` records whose i lie in
+ * [row_begin+1, row_end] and j in [1, n_cols]: i/j/d are sorted in place
+ * (tmp_* are scratch of the same length).  workspace must hold
+ * fasted_sort_workspace_bytes(row_end - row_begin, n_cols) bytes.
+ */
+size_t fasted_sort_workspace_bytes(int64_t n_rows, int64_t n_cols);
+int fasted_sort_pairs(uint32_t* i, uint32_t* j, float* d, uint64_t count, int64_t row_begin,
+                      int64_t row_end, int64_t n_cols, uint32_t* tmp_i, uint32_t* tmp_j,
+                      float* tmp_d, void* workspace, size_t workspace_bytes, void* stream);
+
+/* Number of SMs and device name of the current device (for reports). */
+int fasted_device_info(int* sm_count, char* name, int name_len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FASTED_H_ */

@@ -1,0 +1,319 @@
+// Canonical (i, j) ordering of the join's pair records -- the GPU
+// make_result_set (reference tiling.py:116-122, np.lexsort((j, i))) and the
+// merge at tiling.py:346-351.
+//
+// The join emits records in arbitrary order.  Ordering is a counting sort
+// on the row (i) followed by a per-row sort on the column (j):
+//   1. row histogram (atomics, one per record)
+//   2. exclusive scan of the counts -> 64-bit row offsets
+//   3. scatter into row segments
+//   4. per-row ordering by j.  j values of a row are distinct, so a record's
+//      final slot is its rank among the row's j values:
+//        - rows <= SHORT_MAX records: one warp per row, rank by comparison
+//          against the row staged in shared memory;
+//        - longer rows: a bitmap of the row's j range is set, prefix
+//          popcounts give every record's rank in O(n_cols/32 + len).
+// All passes are bandwidth-trivial next to the join (|R| * 12 bytes).
+#include "common.cuh"
+
+namespace fasted {
+
+constexpr int SCAN_THREADS = 1024;
+constexpr int SCAN_ITEMS = 4;
+constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
+constexpr int SHORT_MAX = 1024;
+constexpr int SHORT_WARPS = 4;
+constexpr int LONG_BLOCKS = 32;
+constexpr int LONG_THREADS = 512;
+
+struct SortWs {
+    uint32_t* counts;            // n_rows
+    uint32_t* cursor;            // n_rows
+    unsigned long long* offsets; // n_rows + 1
+    unsigned long long* bsum;    // n_scan_blocks + 1
+    uint32_t* long_rows;         // n_rows
+    uint32_t* long_count;        // 1
+    uint32_t* bitmap;            // LONG_BLOCKS * 2 * words
+};
+
+static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t carve(void* base, int64_t n_rows, int64_t n_cols, SortWs* ws) {
+    const int64_t nsb = (n_rows + SCAN_TILE - 1) / SCAN_TILE;
+    const int64_t words = (n_cols + 31) / 32 + 1;
+    size_t off = 0;
+    char* b = static_cast<char*>(base);
+    auto take = [&](size_t bytes) {
+        char* p = b ? b + off : nullptr;
+        off += align256(bytes);
+        return p;
+    };
+    SortWs w;
+    w.counts = reinterpret_cast<uint32_t*>(take(n_rows * 4));
+    w.cursor = reinterpret_cast<uint32_t*>(take(n_rows * 4));
+    w.offsets = reinterpret_cast<unsigned long long*>(take((n_rows + 1) * 8));
+    w.bsum = reinterpret_cast<unsigned long long*>(take((nsb + 1) * 8));
+    w.long_rows = reinterpret_cast<uint32_t*>(take(n_rows * 4));
+    w.long_count = reinterpret_cast<uint32_t*>(take(4));
+    w.bitmap = reinterpret_cast<uint32_t*>(take((size_t)LONG_BLOCKS * 2 * words * 4));
+    if (ws) *ws = w;
+    return off;
+}
+
+__global__ void hist_kernel(const uint32_t* __restrict__ pi, uint64_t count, int64_t row_begin,
+                            uint32_t* __restrict__ counts) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < count;
+         p += (uint64_t)gridDim.x * blockDim.x)
+        atomicAdd(&counts[pi[p] - 1 - row_begin], 1u);
+}
+
+// Block-level exclusive scan of SCAN_TILE counts; writes local offsets and
+// the block total.
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_local_kernel(const uint32_t* __restrict__ counts, int64_t n, unsigned long long* __restrict__ offsets,
+                  unsigned long long* __restrict__ bsum) {
+    __shared__ unsigned long long warp_tot[SCAN_THREADS / 32];
+    const int64_t base = (int64_t)blockIdx.x * SCAN_TILE + (int64_t)threadIdx.x * SCAN_ITEMS;
+    unsigned long long v[SCAN_ITEMS];
+    unsigned long long s = 0;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k++) {
+        v[k] = (base + k < n) ? counts[base + k] : 0ull;
+        s += v[k];
+    }
+    // warp inclusive scan of s
+    unsigned long long incl = s;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+        if ((threadIdx.x & 31) >= (unsigned)o) incl += t;
+    }
+    if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = incl;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        unsigned long long w = warp_tot[threadIdx.x];
+        unsigned long long wi = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+            if (threadIdx.x >= (unsigned)o) wi += t;
+        }
+        warp_tot[threadIdx.x] = wi - w;   // exclusive warp offsets
+        if (threadIdx.x == 31) bsum[blockIdx.x] = wi;
+    }
+    __syncthreads();
+    unsigned long long run = warp_tot[threadIdx.x >> 5] + incl - s;
+#pragma unroll
+    for (int k = 0; k < SCAN_ITEMS; k++) {
+        if (base + k < n) offsets[base + k] = run;
+        run += v[k];
+    }
+}
+
+// Exclusive scan of the block totals in place (single block, serial chunks).
+__global__ void __launch_bounds__(SCAN_THREADS)
+scan_blocks_kernel(unsigned long long* __restrict__ bsum, int64_t nb) {
+    __shared__ unsigned long long warp_tot[SCAN_THREADS / 32];
+    __shared__ unsigned long long carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t c0 = 0; c0 < nb; c0 += SCAN_THREADS) {
+        const int64_t idx = c0 + threadIdx.x;
+        const unsigned long long v = idx < nb ? bsum[idx] : 0ull;
+        unsigned long long incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            unsigned long long t = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((threadIdx.x & 31) >= (unsigned)o) incl += t;
+        }
+        if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = incl;
+        __syncthreads();
+        if (threadIdx.x < 32) {
+            unsigned long long w = warp_tot[threadIdx.x];
+            unsigned long long wi = w;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                unsigned long long t = __shfl_up_sync(0xffffffffu, wi, o);
+                if (threadIdx.x >= (unsigned)o) wi += t;
+            }
+            warp_tot[threadIdx.x] = wi - w;
+        }
+        __syncthreads();
+        const unsigned long long excl = carry + warp_tot[threadIdx.x >> 5] + incl - v;
+        __syncthreads();
+        if (idx < nb) bsum[idx] = excl;
+        if (threadIdx.x == SCAN_THREADS - 1) carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) bsum[nb] = carry;
+}
+
+__global__ void scan_add_kernel(unsigned long long* __restrict__ offsets, int64_t n,
+                                const unsigned long long* __restrict__ bsum) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (idx < n) offsets[idx] += bsum[idx / SCAN_TILE];
+    if (idx == 0) offsets[n] = bsum[(n + SCAN_TILE - 1) / SCAN_TILE];
+}
+
+__global__ void scatter_kernel(const uint32_t* __restrict__ pi, const uint32_t* __restrict__ pj,
+                               const float* __restrict__ pd, uint64_t count, int64_t row_begin,
+                               const unsigned long long* __restrict__ offsets,
+                               uint32_t* __restrict__ cursor, uint32_t* __restrict__ tj,
+                               float* __restrict__ td) {
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < count;
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t r = (int64_t)pi[p] - 1 - row_begin;
+        const unsigned long long pos = offsets[r] + atomicAdd(&cursor[r], 1u);
+        tj[pos] = pj[p];
+        td[pos] = pd[p];
+    }
+}
+
+// One warp per row: rank-by-comparison inside shared memory.
+__global__ void __launch_bounds__(SHORT_WARPS * 32)
+short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
+                  const unsigned long long* __restrict__ offsets, int64_t n_rows,
+                  int64_t row_begin, uint32_t* __restrict__ oi, uint32_t* __restrict__ oj,
+                  float* __restrict__ od, uint32_t* __restrict__ long_rows,
+                  uint32_t* __restrict__ long_count) {
+    __shared__ uint32_t keys[SHORT_WARPS][SHORT_MAX];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t r = (int64_t)blockIdx.x * SHORT_WARPS + w; r < n_rows;
+         r += (int64_t)gridDim.x * SHORT_WARPS) {
+        const unsigned long long s0 = offsets[r], s1 = offsets[r + 1];
+        const uint32_t len = (uint32_t)(s1 - s0);
+        if (len == 0) continue;
+        if (len > SHORT_MAX) {
+            if (lane == 0) long_rows[atomicAdd(long_count, 1u)] = (uint32_t)r;
+            continue;
+        }
+        for (uint32_t e = lane; e < len; e += 32) keys[w][e] = tj[s0 + e];
+        __syncwarp();
+        for (uint32_t e = lane; e < len; e += 32) {
+            const uint32_t k = keys[w][e];
+            uint32_t rank = 0;
+            for (uint32_t q = 0; q < len; q++) rank += keys[w][q] < k;
+            oi[s0 + rank] = (uint32_t)(row_begin + r + 1);
+            oj[s0 + rank] = k;
+            od[s0 + rank] = td[s0 + e];
+        }
+        __syncwarp();
+    }
+}
+
+// One block per long row: bitmap ranks over the column range.
+__global__ void __launch_bounds__(LONG_THREADS)
+long_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
+                 const unsigned long long* __restrict__ offsets, int64_t row_begin,
+                 int64_t n_cols, const uint32_t* __restrict__ long_rows,
+                 const uint32_t* __restrict__ long_count, uint32_t* __restrict__ bitmap_all,
+                 uint32_t* __restrict__ oi, uint32_t* __restrict__ oj, float* __restrict__ od) {
+    __shared__ uint32_t warp_tot[LONG_THREADS / 32];
+    __shared__ uint32_t carry;
+    const int64_t words = (n_cols + 31) / 32 + 1;
+    uint32_t* bits = bitmap_all + (int64_t)blockIdx.x * 2 * words;
+    uint32_t* pref = bits + words;
+    const uint32_t nl = *long_count;
+    for (uint32_t li = blockIdx.x; li < nl; li += gridDim.x) {
+        const int64_t r = long_rows[li];
+        const unsigned long long s0 = offsets[r], s1 = offsets[r + 1];
+        for (int64_t w = threadIdx.x; w < words; w += blockDim.x) bits[w] = 0;
+        __syncthreads();
+        for (unsigned long long e = s0 + threadIdx.x; e < s1; e += blockDim.x) {
+            const uint32_t j0 = tj[e] - 1;
+            atomicOr(&bits[j0 >> 5], 1u << (j0 & 31));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry = 0;
+        __syncthreads();
+        for (int64_t c0 = 0; c0 < words; c0 += blockDim.x) {
+            const int64_t w = c0 + threadIdx.x;
+            const uint32_t v = w < words ? (uint32_t)__popc(bits[w]) : 0u;
+            const uint32_t incl = warp_inclusive_scan(v);
+            if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = incl;
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                const uint32_t t = warp_tot[threadIdx.x];
+                const uint32_t ti = warp_inclusive_scan(t);
+                warp_tot[threadIdx.x] = ti - t;
+            }
+            __syncthreads();
+            const uint32_t excl = carry + warp_tot[threadIdx.x >> 5] + incl - v;
+            __syncthreads();
+            if (w < words) pref[w] = excl;
+            if (threadIdx.x == blockDim.x - 1) carry = excl + v;
+            __syncthreads();
+        }
+        for (unsigned long long e = s0 + threadIdx.x; e < s1; e += blockDim.x) {
+            const uint32_t j = tj[e];
+            const uint32_t j0 = j - 1;
+            const uint32_t rank =
+                pref[j0 >> 5] + (uint32_t)__popc(bits[j0 >> 5] & ((1u << (j0 & 31)) - 1u));
+            oi[s0 + rank] = (uint32_t)(row_begin + r + 1);
+            oj[s0 + rank] = j;
+            od[s0 + rank] = td[e];
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace fasted
+
+using namespace fasted;
+
+extern "C" size_t fasted_sort_workspace_bytes(int64_t n_rows, int64_t n_cols) {
+    if (n_rows < 1 || n_cols < 1) return 0;
+    return carve(nullptr, n_rows, n_cols, nullptr);
+}
+
+extern "C" int fasted_sort_pairs(uint32_t* pi, uint32_t* pj, float* pd, uint64_t count,
+                                 int64_t row_begin, int64_t row_end, int64_t n_cols,
+                                 uint32_t* tmp_i, uint32_t* tmp_j, float* tmp_d,
+                                 void* workspace, size_t workspace_bytes, void* stream) {
+    (void)tmp_i;
+    const int64_t n_rows = row_end - row_begin;
+    if (count == 0) return FASTED_OK;
+    if (!pi || !pj || !pd || !tmp_j || !tmp_d || !workspace || n_rows < 1 || n_cols < 1 ||
+        n_cols > 0xffffffffLL) {
+        set_error("fasted_sort_pairs: bad arguments");
+        return FASTED_ERR_ARGUMENT;
+    }
+    const size_t need = carve(nullptr, n_rows, n_cols, nullptr);
+    if (workspace_bytes < need) {
+        set_error("fasted_sort_pairs: workspace %zu < %zu bytes", workspace_bytes, need);
+        return FASTED_ERR_ARGUMENT;
+    }
+    SortWs ws;
+    carve(workspace, n_rows, n_cols, &ws);
+    cudaStream_t s = as_stream(stream);
+    cudaMemsetAsync(ws.counts, 0, n_rows * 4, s);
+    cudaMemsetAsync(ws.cursor, 0, n_rows * 4, s);
+    cudaMemsetAsync(ws.long_count, 0, 4, s);
+    const int sms = sm_count_current();
+    const unsigned rec_grid = (unsigned)((count + 255) / 256 < (uint64_t)sms * 16
+                                             ? (count + 255) / 256
+                                             : (uint64_t)sms * 16);
+    hist_kernel<<<rec_grid, 256, 0, s>>>(pi, count, row_begin, ws.counts);
+    FASTED_CHECK_LAUNCH("hist_kernel");
+    const int64_t nsb = (n_rows + SCAN_TILE - 1) / SCAN_TILE;
+    scan_local_kernel<<<(unsigned)nsb, SCAN_THREADS, 0, s>>>(ws.counts, n_rows, ws.offsets,
+                                                              ws.bsum);
+    FASTED_CHECK_LAUNCH("scan_local_kernel");
+    scan_blocks_kernel<<<1, SCAN_THREADS, 0, s>>>(ws.bsum, nsb);
+    FASTED_CHECK_LAUNCH("scan_blocks_kernel");
+    scan_add_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(ws.offsets, n_rows, ws.bsum);
+    FASTED_CHECK_LAUNCH("scan_add_kernel");
+    scatter_kernel<<<rec_grid, 256, 0, s>>>(pi, pj, pd, count, row_begin, ws.offsets, ws.cursor,
+                                            tmp_j, tmp_d);
+    FASTED_CHECK_LAUNCH("scatter_kernel");
+    const int64_t sgrid = (n_rows + SHORT_WARPS - 1) / SHORT_WARPS;
+    short_rows_kernel<<<(unsigned)(sgrid < (int64_t)sms * 64 ? sgrid : (int64_t)sms * 64),
+                        SHORT_WARPS * 32, 0, s>>>(tmp_j, tmp_d, ws.offsets, n_rows, row_begin,
+                                                  pi, pj, pd, ws.long_rows, ws.long_count);
+    FASTED_CHECK_LAUNCH("short_rows_kernel");
+    long_rows_kernel<<<LONG_BLOCKS, LONG_THREADS, 0, s>>>(tmp_j, tmp_d, ws.offsets, row_begin,
+                                                          n_cols, ws.long_rows, ws.long_count,
+                                                          ws.bitmap, pi, pj, pd);
+    FASTED_CHECK_LAUNCH("long_rows_kernel");
+    return FASTED_OK;
+}
