@@ -204,13 +204,17 @@ class JoinReport:
     per_device: list
 
 
-def self_join_devices(hd, eps_sq: float, devices, exact: bool = False):
-    """Row-block partition across `devices`; returns (i, j, d, JoinReport)."""
+def self_join_devices(hd, eps_sq: float, devices, exact: bool = False, row_range=None):
+    """Row-block partition of `row_range` (default: all rows) across
+    `devices`; returns (i, j, d, JoinReport)."""
     import torch
 
+    for dev in set(devices):
+        _lib.require_device(dev)
     t_start = time.perf_counter()
     n_dev = -(-hd.n_padded // BLOCK) * BLOCK
-    parts = partition_rows(n_dev, len(devices))
+    r0, r1 = row_range if row_range is not None else (0, n_dev)
+    parts = [(r0 + a, r0 + b) for a, b in partition_rows(r1 - r0, len(devices))]
 
     def run(g):
         dev = devices[g]

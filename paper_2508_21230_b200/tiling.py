@@ -215,13 +215,16 @@ def compute_block_tile(hd: HalfDataset, coord: TileCoord, eps_sq, cfg: TileConfi
 
 def self_join(hd: HalfDataset, epsilon: float, cfg: TileConfig | None = None,
               stats_out: EngineStats | None = None, *, mode: str = "tc",
-              devices=None) -> ResultSet:
+              devices=None, shard=None) -> ResultSet:
     """Full epsilon self-join: every ordered pair with distance <= epsilon
     (tiling.py:288-359), on one or more B200s.
 
     mode "tc" is the tcgen05 product path; "exact" reproduces the reference
     bit for bit.  devices: list of CUDA device indices (row-block sharded,
-    no collectives); default the current device.
+    no collectives); default the current device.  shard=(rank, world): one
+    process per GPU -- this call returns only the pairs whose i lies in the
+    rank's contiguous row-block range; concatenating ranks in order gives
+    the full, sorted ResultSet.
     """
     if cfg is None:
         cfg = TileConfig()
@@ -233,9 +236,16 @@ def self_join(hd: HalfDataset, epsilon: float, cfg: TileConfig | None = None,
     eps_sq = _eps_sq(epsilon)
     if devices is None:
         devices = _default_devices()
+    row_range = None
+    if shard is not None:
+        rank, world = shard
+        if not (0 <= rank < world):
+            raise ArgumentError(f"shard {shard} invalid")
+        n_dev = -(-hd.n_padded // 128) * 128
+        row_range = engine.partition_rows(n_dev, world)[rank]
     t0 = time.perf_counter()
     i, j, d, rep = engine.self_join_devices(hd, float(eps_sq), list(devices),
-                                            exact=(mode == "exact"))
+                                            exact=(mode == "exact"), row_range=row_range)
     rs = ResultSet(i, j, d, n=int(hd.n_logical), epsilon=float(epsilon))
     if stats_out is not None:
         n_dev = -(-hd.n_padded // 128) * 128

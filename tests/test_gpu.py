@@ -1,0 +1,280 @@
+"""GPU parity tests: the CUDA path through the C ABI against the reference's
+golden vectors and the CPU oracle.  Run on a B200 with ``-m gpu``.
+
+Bars (north star): quantise and the exact kernel are bit-exact; the tcgen05
+kernel matches the reference pair set exactly for every pair whose reference
+dist_sq lies outside the relative band |d2 - eps^2| <= 1e-3 * eps^2.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import paper_2508_21230_b200 as F  # noqa: E402
+from paper_2508_21230_b200 import _lib, engine  # noqa: E402
+
+SYNTH = ["uniform_700x45", "spec_512x128", "ragged_130x17", "wide_300x64", "c1_slice_1024x128"]
+BAND = 1e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def device():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (no CPU fallback exists)")
+    _lib.require_device(0)
+    return 0
+
+
+def _band_ok(oracle, hd, rs, ref_i, ref_j, ref_d, eps, band=BAND):
+    es = float(oracle.eps_sq_of(eps))
+    rep = F.band_compare(rs.i, rs.j, rs.dist_sq, ref_i, ref_j, ref_d, es,
+                         lambda i, j: oracle.pair_d2(hd.values, hd.norms, i, j), band=band)
+    return rep
+
+
+def test_loaded_library_is_in_tree():
+    F.self_join(F.to_half(F.Dataset(np.eye(3, dtype=np.float32))), 0.5)
+    maps = open("/proc/self/maps").read()
+    assert os.path.realpath(_lib.LIB_PATH) in maps
+
+
+@pytest.mark.parametrize("name", SYNTH)
+def test_to_half_bit_exact(golden, name):
+    hd = F.to_half(F.Dataset(golden[f"{name}_x"]))
+    assert np.array_equal(hd.values.view(np.uint16), golden[f"{name}_values"])
+    assert np.array_equal(hd.norms, golden[f"{name}_norms"])
+    assert np.array_equal(F.compute_squared_norms(hd), hd.norms)
+
+
+def test_to_half_known_answers(golden):
+    hd = F.to_half(F.Dataset(golden["tohalf_in"]))
+    assert np.array_equal(hd.values.view(np.uint16), golden["tohalf_values"])
+    assert np.array_equal(hd.norms, golden["tohalf_norms"])
+    hd = F.to_half(F.Dataset(np.full((1, 16), 0.1, np.float32)))
+    assert hd.norms[0] == np.float32(0.15992188)
+
+
+def test_range_error_message(golden_meta):
+    with pytest.raises(F.RangeError) as e:
+        F.to_half(F.Dataset(np.array([[1.0, 2.0], [3.0, 70000.0]], np.float32)))
+    assert str(e.value) == golden_meta["range_error_message"]
+    with pytest.raises(F.RangeError) as e:
+        F.to_half(F.Dataset(np.array([[65520.0]], np.float32)))
+    assert str(e.value) == golden_meta["range_error_message_65520"]
+
+
+def test_to_half_large_matches_oracle(oracle):
+    x = F.synthetic_rows(1000000, 960, 12345, 0, 3000)
+    x[7, 5] = -60000.0
+    x[11, 3] = 2.0 ** -20
+    hd = F.to_half(F.Dataset(x))
+    v16, norms, _ = oracle.to_half(x)
+    assert np.array_equal(hd.values.view(np.uint16), v16.view(np.uint16))
+    assert np.array_equal(hd.norms, norms)
+
+
+# ── exact kernel: bit parity ─────────────────────────────────────────────
+
+
+@pytest.mark.parametrize("name", SYNTH)
+def test_exact_join_bit_exact(golden, golden_meta, oracle, name):
+    meta = golden_meta["cases"][name]
+    hd = F.to_half(F.Dataset(golden[f"{name}_x"]))
+    rs = F.self_join(hd, meta["epsilon"], mode="exact")
+    assert np.array_equal(rs.i, golden[f"{name}_i"])
+    assert np.array_equal(rs.j, golden[f"{name}_j"])
+    assert np.array_equal(rs.dist_sq.view(np.uint32), golden[f"{name}_d"].view(np.uint32))
+    assert hashlib.sha256(oracle.pairs_payload(rs.i, rs.j, rs.dist_sq)).hexdigest() == \
+        meta["result_sha256"]
+
+
+def test_exact_c1_reference_digest(golden_meta, oracle):
+    c1 = golden_meta["C1"]
+    hd = F.to_half(F.generate_synthetic(c1["n"], c1["d"], seed=c1["seed"]))
+    rs = F.self_join(hd, c1["epsilon"], mode="exact")
+    assert len(rs) == c1["pairs"]
+    assert hashlib.sha256(oracle.pairs_payload(rs.i, rs.j, rs.dist_sq)).hexdigest() == \
+        c1["result_sha256"]
+
+
+def test_compute_block_tile_exact(golden):
+    hd = F.to_half(F.Dataset(golden["tile_x"]))
+    es = np.float32(np.float32(3.3) * np.float32(3.3))
+    i, j, d = F.compute_block_tile(hd, F.TileCoord(2, 1), es, F.TileConfig())
+    assert np.array_equal(i, golden["tile_i"]) and np.array_equal(j, golden["tile_j"])
+    assert np.array_equal(d.view(np.uint32), golden["tile_d"].view(np.uint32))
+
+
+def _panel_join(n, d, seed, eps, rb, cb, exact):
+    """Join of tile (rb, cb) of a big synthetic shape from its two panels."""
+    a = F.synthetic_rows(n, d, seed, rb * 128, min(rb * 128 + 128, n))
+    b = F.synthetic_rows(n, d, seed, cb * 128, min(cb * 128 + 128, n))
+    pa = np.zeros((128, d), np.float32)
+    pb = np.zeros((128, d), np.float32)
+    pa[:len(a)], pb[:len(b)] = a, b
+    hd = F.to_half(F.Dataset(np.concatenate([pa, pb])))
+    dd = engine.upload(hd, 0)
+    es = float(np.float32(np.float32(eps) * np.float32(eps)))
+    res = engine.join_device(dd, es, rows=(0, 128), cols=(128, 256), exact=exact)
+    i, j, dist = engine.to_host(res)
+    gi = i.astype(np.int64) - 1 + rb * 128
+    gj = j.astype(np.int64) - 1 - 128 + cb * 128
+    keep = (i <= len(a)) & (j - 128 <= len(b))
+    return (gi[keep] + 1).astype(np.uint32), (gj[keep] + 1).astype(np.uint32), dist[keep], hd
+
+
+def test_sampled_tiles_exact_and_tc(golden, golden_meta, oracle):
+    """C2-C5 shapes, reference compute_block_tile outputs."""
+    for name, rec in golden_meta["sampled_tiles"].items():
+        for t in rec["tiles"]:
+            rb, cb = t["row_block"], t["col_block"]
+            key = f"{name}_{rb}_{cb}"
+            i, j, d, _ = _panel_join(rec["n"], rec["d"], rec["seed"], rec["epsilon"], rb, cb, True)
+            assert np.array_equal(i, golden[key + "_i"]), key
+            assert np.array_equal(j, golden[key + "_j"]), key
+            assert np.array_equal(d.view(np.uint32), golden[key + "_d"].view(np.uint32)), key
+            ti, tj, td, hd = _panel_join(rec["n"], rec["d"], rec["seed"], rec["epsilon"], rb, cb,
+                                         False)
+            es = float(oracle.eps_sq_of(rec["epsilon"]))
+            rep = F.band_compare(ti, tj, td, golden[key + "_i"], golden[key + "_j"],
+                                 golden[key + "_d"], es, lambda a, b: np.full(len(a), np.inf))
+            assert rep.missing_out_of_band == 0, (key, rep)
+
+
+# ── tcgen05 kernel: band parity ──────────────────────────────────────────
+
+
+@pytest.mark.parametrize("name", SYNTH)
+def test_tc_join_band_parity(golden, golden_meta, oracle, name):
+    meta = golden_meta["cases"][name]
+    hd = F.to_half(F.Dataset(golden[f"{name}_x"]))
+    rs = F.self_join(hd, meta["epsilon"])
+    rep = _band_ok(oracle, hd, rs, golden[f"{name}_i"], golden[f"{name}_j"],
+                   golden[f"{name}_d"], meta["epsilon"])
+    assert rep.ok, rep
+    assert rep.max_rel_dd2_matched < BAND, rep
+    # canonical order
+    key = rs.i.astype(np.uint64) << np.uint64(32) | rs.j.astype(np.uint64)
+    assert np.all(np.diff(key.astype(np.int64)) > 0)
+
+
+def test_tc_integer_regime_exact(golden):
+    """Small-integer coordinates: every product and partial sum is exact, so
+    the tensor core must agree bit for bit (SPEC.md:526 criterion 4)."""
+    hd = F.to_half(F.Dataset(golden["integer_x"]))
+    rs = F.self_join(hd, 6.0)
+    assert np.array_equal(rs.i, golden["integer_i"]) and np.array_equal(rs.j, golden["integer_j"])
+    assert np.array_equal(rs.dist_sq, golden["integer_d"])
+
+
+def test_tc_hand_fixtures(golden):
+    tri = F.to_half(F.Dataset(np.array([[0.0, 0.0], [3.0, 4.0]], np.float32)))
+    rs = F.self_join(tri, 5.0)
+    assert rs.as_tuples() == [(1, 1, 0.0), (1, 2, 25.0), (2, 1, 25.0), (2, 2, 0.0)]
+    same = F.to_half(F.Dataset(np.ones((3, 4), np.float32) * 0.7))
+    assert F.selectivity(F.self_join(same, 0.5)) == 2.0
+
+
+@pytest.mark.parametrize("mode", ["tc", "exact"])
+def test_eps_zero_gives_self_pairs(mode):
+    hd = F.to_half(F.generate_synthetic(3000, 96, seed=5))
+    rs = F.self_join(hd, 0.0, mode=mode)
+    assert len(rs) == 3000
+    assert np.array_equal(rs.i, np.arange(1, 3001, dtype=np.uint32))
+    assert np.array_equal(rs.i, rs.j) and not rs.dist_sq.any()
+
+
+def test_duplicates_eps_zero(golden):
+    hd = F.to_half(F.Dataset(golden["dup_x"]))
+    rs = F.self_join(hd, 0.0, mode="exact")
+    assert np.array_equal(rs.i, golden["dup_i"]) and np.array_equal(rs.j, golden["dup_j"])
+    tc = F.self_join(hd, 0.0)
+    # diagonal always present; exact-duplicate pairs at eps = 0 are the
+    # documented zero-width-band exception
+    assert tc.index_pairs() <= rs.index_pairs()
+    assert {(k, k) for k in range(1, hd.n_logical + 1)} <= tc.index_pairs()
+
+
+def test_c1_tc_vs_reference(golden_meta, oracle):
+    c1 = golden_meta["C1"]
+    hd = F.to_half(F.generate_synthetic(c1["n"], c1["d"], seed=c1["seed"]))
+    ref = F.self_join(hd, c1["epsilon"], mode="exact")   # == reference (digest test)
+    st = F.EngineStats()
+    rs = F.self_join(hd, c1["epsilon"], stats_out=st)
+    rep = _band_ok(oracle, hd, rs, ref.i, ref.j, ref.dist_sq, c1["epsilon"])
+    print("C1 band report:", rep, "kernel s:", st.kernel_wall_seconds)
+    assert rep.ok, rep
+
+
+def test_row_sharding_matches_single_device(golden_meta):
+    c1 = golden_meta["C1"]
+    hd = F.to_half(F.generate_synthetic(5000, 128, seed=3))
+    one = F.self_join(hd, 3.9)
+    three = F.self_join(hd, 3.9, devices=[0, 0, 0])
+    assert one.same_pairs(three)
+    assert np.array_equal(one.dist_sq.view(np.uint32), three.dist_sq.view(np.uint32))
+
+
+def test_capacity_rerun_and_count_only():
+    hd = F.to_half(F.generate_synthetic(4000, 64, seed=9))
+    dd = engine.upload(hd, 0)
+    es = float(np.float32(np.float32(2.6) ** 2))
+    full = engine.join_device(dd, es)
+    small = engine.join_device(dd, es, capacity=17)
+    assert small.reruns >= 1 and small.count == full.count
+    a, b = engine.to_host(full), engine.to_host(small)
+    assert all(np.array_equal(x, y) for x, y in zip(a, b))
+    cnt = torch.zeros(1, dtype=torch.int64, device="cuda:0")
+    L = _lib.load()
+    _lib.check(L.fasted_join(dd.values.data_ptr(), dd.norms.data_ptr(), dd.n_logical, dd.n_dev,
+                             dd.d_pad, 0, dd.n_dev, 0, dd.n_dev, es, _lib.JOIN_COUNT, None,
+                             None, None, 0, cnt.data_ptr(),
+                             torch.cuda.current_stream().cuda_stream), "count")
+    assert int(cnt.item()) == full.count
+
+
+def test_long_rows_sort_path():
+    """eps above the diameter: every row holds all n pairs (> 1024 -> bitmap path)."""
+    n = 2500
+    hd = F.to_half(F.generate_synthetic(n, 32, seed=1))
+    rs = F.self_join(hd, 100.0)
+    assert len(rs) == n * n
+    assert np.array_equal(rs.i, np.repeat(np.arange(1, n + 1, dtype=np.uint32), n))
+    assert np.array_equal(rs.j, np.tile(np.arange(1, n + 1, dtype=np.uint32), n))
+
+
+def test_invalid_arguments_raise():
+    hd = F.to_half(F.generate_synthetic(10, 8, seed=1))
+    with pytest.raises(F.ArgumentError):
+        F.self_join(hd, -1.0)
+    with pytest.raises(F.ConfigError):
+        F.self_join(hd, 1.0, F.TileConfig(warp_kslice=8))
+    with pytest.raises(F.ArgumentError):
+        F.compute_block_tile(hd, F.TileCoord(5, 0), 1.0, F.TileConfig())
+
+
+@pytest.mark.slow
+def test_c3_full_size_tc_vs_exact(oracle):
+    """1M x 128 (C3): full tcgen05 join against the bit-exact kernel (itself
+    pinned to the reference), plus oracle cross-check of sampled row blocks."""
+    n, d, eps = 1000000, 128, 3.685431479161428
+    hd = F.to_half(F.generate_synthetic(n, d, seed=12345))
+    es = float(oracle.eps_sq_of(eps))
+    ref = F.self_join(hd, eps, mode="exact")
+    rs = F.self_join(hd, eps)
+    rep = _band_ok(oracle, hd, rs, ref.i, ref.j, ref.dist_sq, eps)
+    print("C3 band report:", rep)
+    assert rep.ok, rep
+    # exact kernel == oracle on two row blocks at full column range
+    for rb in (0, 5000):
+        oi, oj, od = oracle.join(hd.values, hd.norms, n, eps, rows=(rb * 128, rb * 128 + 128))
+        sel = (ref.i > rb * 128) & (ref.i <= rb * 128 + 128)
+        assert np.array_equal(oi, ref.i[sel]) and np.array_equal(oj, ref.j[sel])
+        assert np.array_equal(od.view(np.uint32), ref.dist_sq[sel].view(np.uint32))
+    assert es > 0

@@ -1,0 +1,232 @@
+"""CPU tests: host-side API mirror, validation, the C-ABI library surface.
+No GPU compute is called here (the product path has no CPU fallback)."""
+
+import ctypes
+import os
+import re
+import struct
+
+import numpy as np
+import pytest
+
+import paper_2508_21230_b200 as F
+from paper_2508_21230_b200 import _lib, engine
+from paper_2508_21230_b200.tiling import _check_engine_inputs
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+# ── C ABI surface ────────────────────────────────────────────────────────
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "fasted.h")).read()
+    return sorted(set(re.findall(r"\b(fasted_[a-z_]+)\s*\(", src)))
+
+
+def test_library_exports_every_header_symbol():
+    L = _lib.load()
+    syms = _header_symbols()
+    assert len(syms) >= 10
+    for s in syms:
+        assert hasattr(L, s), s
+    assert set(syms) == set(_lib.EXPORTS)
+
+
+def test_library_host_calls_without_gpu():
+    L = _lib.load()
+    assert L.fasted_abi_version() == 1
+    assert L.fasted_strerror(3) == b"value out of FP16 range"
+    assert L.fasted_sort_workspace_bytes(1000, 1000) > 0
+    # argument validation happens before any device work
+    assert L.fasted_join(None, None, 1, 128, 16, 0, 128, 0, 128, 1.0, 0, None, None, None, 0,
+                         None, None) == _lib.ERR_ARGUMENT
+    assert L.fasted_quantize(None, 1, 1, None, 1, 8, None, None, None) == _lib.ERR_ARGUMENT
+
+
+def test_library_is_sm100a_only():
+    out = os.popen(f"cuobjdump -lelf {_lib.LIB_PATH} 2>/dev/null").read()
+    if not out:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out
+    assert not re.search(r"sm_(?!100a)\d+", out.replace("sm_100a", ""))
+
+
+def test_kernels_use_tcgen05_and_tma():
+    sass = os.popen(f"cuobjdump -sass {_lib.LIB_PATH} 2>/dev/null").read()
+    if not sass:
+        pytest.skip("cuobjdump unavailable")
+    for mnemonic in ("UTCHMMA", "UTMALDG", "LDTM", "FFMA.RZ"):
+        assert mnemonic in sass, mnemonic
+
+
+def test_product_path_fails_loudly_without_gpu():
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    hd = F.HalfDataset(3, 4, np.zeros((128, 16), np.float16), np.zeros(128, np.float32))
+    with pytest.raises(F.DeviceError):
+        F.self_join(hd, 1.0)
+    with pytest.raises(F.DeviceError):
+        F.to_half(F.Dataset(np.ones((2, 2), np.float32)))
+
+
+def test_product_package_never_imports_oracle():
+    pkg = os.path.join(ROOT, "paper_2508_21230_b200")
+    for fn in os.listdir(pkg):
+        if fn.endswith(".py"):
+            src = open(os.path.join(pkg, fn)).read()
+            assert not re.search(r"^\s*(from|import)\s+oracle", src, re.M), fn
+
+
+# ── API mirror ───────────────────────────────────────────────────────────
+
+
+def test_tileconfig_validation_matches_reference():
+    F.TileConfig().validate()
+    for kw in [dict(warp_kslice=8), dict(warp_side=24), dict(block_side=96),
+               dict(block_kslice=24), dict(dispatch_square=0), dict(prefetch_depth=3),
+               dict(workers=0)]:
+        with pytest.raises(F.ConfigError):
+            F.TileConfig(**kw).validate()
+
+
+def test_engine_input_checks():
+    hd = F.HalfDataset(5, 5, np.zeros((64, 16), np.float16), np.zeros(64, np.float32))
+    with pytest.raises(F.ConfigError):
+        _check_engine_inputs(hd, F.TileConfig())
+    hd = F.HalfDataset(5, 5, np.zeros((128, 8), np.float16), np.zeros(128, np.float32))
+    with pytest.raises(F.ConfigError):
+        _check_engine_inputs(hd, F.TileConfig())
+
+
+def test_rasterize_examples():   # SPEC.md rasterize_tiles examples
+    assert [(c.row_block, c.col_block) for c in F.rasterize_tiles(2, 2, 8)] == \
+        [(0, 0), (0, 1), (1, 0), (1, 1)]
+    order = F.rasterize_tiles(16, 16, 8)
+    assert {(c.row_block, c.col_block) for c in order[:64]} == {(r, c) for r in range(8) for c in range(8)}
+    o9 = F.rasterize_tiles(9, 9, 8)
+    assert len(o9) == 81 and len(set(o9)) == 81
+
+
+def test_make_result_set_sorts():
+    rs = F.make_result_set([2, 1, 1], [1, 3, 2], np.array([0.5, 0.25, 0.125], np.float32), 3, 1.0)
+    assert rs.as_tuples() == [(1, 2, 0.125), (1, 3, 0.25), (2, 1, 0.5)]
+    assert rs.i.dtype == np.uint32
+
+
+def test_selectivity_and_flops():
+    rs = F.make_result_set([1, 1, 2, 2, 3, 3, 1, 2, 3], [1, 2, 1, 2, 3, 1, 3, 3, 2],
+                           np.zeros(9, np.float32), 3, 1.0)
+    assert F.selectivity(rs) == 2.0
+    assert F.derived_flops(128, 16, 1.0) == 2 * 128 * 128 * 16 / 1e12
+    assert F.distance_tflops(1000, 10, 2.0) == 2 * 1000 * 1000 * 10 / 2.0 / 1e12
+    with pytest.raises(F.ArgumentError):
+        F.derived_flops(1, 1, 0.0)
+
+
+def test_overlap_examples():   # SPEC.md overlap_accuracy examples
+    a = F.make_result_set([1], [1], np.zeros(1, np.float32), 1, 1.0)
+    b = F.make_result_set([1, 1], [1, 2], np.zeros(2, np.float32), 1, 1.0)
+    assert F.overlap_accuracy(a, a) == 1.0
+    assert F.overlap_accuracy(a, b) == 0.5
+
+
+def test_distance_error_stats_example():
+    t = F.make_result_set([1, 2], [2, 1], np.array([1.1 ** 2, 0.9 ** 2], np.float32), 2, 2.0)
+    r = F.make_result_set([1, 2], [2, 1], np.array([1.0, 1.0]), 2, 2.0)
+    st = F.distance_error_stats(t, r)
+    assert abs(st.err_mean) < 1e-6 and abs(st.err_std - 0.1) < 1e-6
+
+
+def test_band_compare_classification():
+    es = 100.0
+    ref = (np.array([1, 1, 2], np.uint32), np.array([1, 2, 2], np.uint32),
+           np.array([0.0, 99.95, 10.0], np.float32))
+    test = (np.array([1, 2, 2], np.uint32), np.array([1, 1, 2], np.uint32),
+            np.array([0.0, 99.99, 10.0], np.float32))
+    rep = F.band_compare(*test, *ref, es, lambda i, j: np.array([100.05]))
+    assert rep.missing_in_band == 1 and rep.extra_in_band == 1 and rep.ok
+    rep = F.band_compare(*test, *ref, es, lambda i, j: np.array([150.0]))
+    assert rep.extra_out_of_band == 1 and not rep.ok
+
+
+def test_calibrate_epsilon_matches_reference_procedure():
+    ds = F.generate_synthetic(3, 4, seed=0)
+    same = np.repeat(ds.values[:1], 3, axis=0)
+    cal = F.calibrate_epsilon(same, 2.0)
+    assert cal.iterations == 0 and cal.estimated_selectivity == 2.0
+    with pytest.raises(F.CalibrationError):
+        F.calibrate_epsilon(F.generate_synthetic(10, 4, seed=1), 20.0)
+
+
+# ── data ─────────────────────────────────────────────────────────────────
+
+
+def test_generate_synthetic_matches_numpy_stream():
+    ds = F.generate_synthetic(7, 5, seed=12345, lo=-1.0, hi=3.0)
+    u = np.random.default_rng(12345).random((7, 5), dtype=np.float32)
+    assert np.array_equal(ds.values, u * np.float32(4.0) + np.float32(-1.0))
+
+
+@pytest.mark.parametrize("n,d,r0,r1", [(50, 7, 3, 20), (50, 8, 0, 50), (50, 9, 11, 12), (9, 3, 9, 9)])
+def test_synthetic_rows_equals_full(n, d, r0, r1):
+    full = F.generate_synthetic(n, d, seed=99).values
+    assert np.array_equal(F.synthetic_rows(n, d, 99, r0, r1), full[r0:r1])
+
+
+def _write_fvecs(path, rows):
+    with open(path, "wb") as f:
+        for row in rows:
+            f.write(struct.pack("<i", len(row)))
+            f.write(struct.pack(f"<{len(row)}f", *row))
+
+
+def test_load_fvecs_roundtrip_and_errors(tmp_path):   # test_dataset.py:34-82
+    p = tmp_path / "a.fvecs"
+    _write_fvecs(p, [(1.0, 2.0), (3.0, 4.0)])
+    assert np.array_equal(F.load_fvecs(p).values, np.array([[1, 2], [3, 4]], np.float32))
+    e = tmp_path / "e.fvecs"
+    e.write_bytes(b"")
+    with pytest.raises(F.FormatError, match="empty"):
+        F.load_fvecs(e)
+    b = tmp_path / "b.fvecs"
+    with open(b, "wb") as f:
+        f.write(struct.pack("<i2f", 2, 1.0, 2.0))
+        f.write(struct.pack("<i3f", 3, 1.0, 2.0, 3.0))
+        f.write(b"\x00" * 4)
+    with pytest.raises(F.FormatError, match="inconsistent dimension 3.*offset 12"):
+        F.load_fvecs(b)
+    t = tmp_path / "t.fvecs"
+    with open(t, "wb") as f:
+        f.write(struct.pack("<i2f", 2, 1.0, 2.0))
+        f.write(struct.pack("<if", 2, 1.0))
+    with pytest.raises(F.FormatError, match="truncated record at byte offset 12"):
+        F.load_fvecs(t)
+    z = tmp_path / "z.fvecs"
+    z.write_bytes(struct.pack("<i", 0))
+    with pytest.raises(F.FormatError, match="must be >= 1"):
+        F.load_fvecs(z)
+
+
+def test_dataset_invariants():
+    for bad in (np.zeros((0, 3), np.float32), np.zeros((3, 0), np.float32)):
+        with pytest.raises(F.ArgumentError):
+            F.Dataset(bad)
+    x = np.ones((2, 2), np.float32)
+    x[1, 1] = np.nan
+    with pytest.raises(F.ArgumentError):
+        F.Dataset(x)
+
+
+def test_partition_rows():
+    assert engine.partition_rows(1024, 3) == [(0, 256), (256, 640), (640, 1024)]
+    with pytest.raises(F.ArgumentError):
+        engine.partition_rows(1024, 0)
+
+
+def test_error_hierarchy():
+    assert issubclass(F.RangeError, ValueError) and issubclass(F.RangeError, F.MPJoinError)
+    assert issubclass(F.AccumulatorOverflow, ArithmeticError)
+    assert issubclass(F.DeviceError, RuntimeError)
