@@ -216,23 +216,17 @@ def main():
     rows = engine.partition_rows(n_dev, world)[rank]
     dd = engine.upload(hd, device)
     eps_sq = float(np.float32(np.float32(eps) * np.float32(eps)))
-    L = _lib.load()
     stream = torch.cuda.current_stream()
-    # size the pair buffer once (exact count)
+    # size the record buffer once (exact count + per-warp chunk slack)
     first = engine.join_device(dd, eps_sq, rows=rows, sort=False)
-    cap = first.count
-    oi = torch.empty(max(cap, 1), dtype=torch.int32, device=f"cuda:{device}")
-    oj = torch.empty_like(oi)
-    od = torch.empty(max(cap, 1), dtype=torch.float32, device=f"cuda:{device}")
-    cnt = torch.zeros(1, dtype=torch.int64, device=f"cuda:{device}")
+    cap = first.count + engine.hole_slack(device)
     del first
+    rec = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=f"cuda:{device}")
+    cnt = torch.zeros(2, dtype=torch.int64, device=f"cuda:{device}")
 
     def step():
-        st = L.fasted_join(dd.values.data_ptr(), dd.norms.data_ptr(), dd.n_logical, dd.n_dev,
-                           dd.d_pad, rows[0], rows[1], 0, dd.n_dev, eps_sq, _lib.JOIN_TC,
-                           oi.data_ptr(), oj.data_ptr(), od.data_ptr(), cap, cnt.data_ptr(),
-                           stream.cuda_stream)
-        _lib.check(st, "fasted_join")
+        engine.join_raw(dd, eps_sq, _lib.JOIN_TC, rows, (0, dd.n_dev), rec, cap, cnt,
+                        stream.cuda_stream)
 
     def barrier():
         if world > 1:
@@ -253,7 +247,7 @@ def main():
         barrier()
     per_step = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
     ms_local = ev[0].elapsed_time(ev[-1]) / args.steps
-    pairs_local = int(cnt.item())
+    pairs_local = int(cnt[0].item())
     ms = ms_local
     pairs = pairs_local
     if world > 1:
@@ -278,7 +272,7 @@ def main():
         traffic = prof.get(args.workload, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
-    del oi, oj, od
+    del rec
     torch.cuda.empty_cache()
 
     # ---- e2e through the public API with host buffers (H2D + D2H inside)

@@ -55,7 +55,12 @@ enum {
 enum {
     FASTED_JOIN_TC = 0,     /* tcgen05/TMEM fused kernel (the product path)          */
     FASTED_JOIN_EXACT = 1,  /* CUDA-core FFMA.RZ kernel, bit-exact with the reference */
-    FASTED_JOIN_COUNT = 2   /* OR-able: count only, write no records                 */
+    FASTED_JOIN_COUNT = 2,  /* OR-able: count only, write no records                 */
+    /* Diagnostics for power/throughput attribution (results are NOT valid): */
+    FASTED_JOIN_DIAG_NOEPI = 256,    /* tcgen05 kernel: skip the epilogue entirely     */
+    FASTED_JOIN_DIAG_NOMMA = 512,    /* tcgen05 kernel: skip the MMAs (TMA + epilogue) */
+    FASTED_JOIN_DIAG_LOADONLY = 1024, /* epilogue: TMEM loads only, no math           */
+    FASTED_JOIN_DIAG_NOSLOW = 2048   /* epilogue: sign test only, never write         */
 };
 
 int fasted_abi_version(void);
@@ -90,28 +95,39 @@ int fasted_norms(const uint16_t* values16, int64_t n_pad, int64_t d_pad, float* 
  * A pair (i, j) qualifies iff i, j < n_logical and
  *   max(((-2 a_ij) + s_i) + s_j, 0) <= eps_sq           (tiling.py:273-279)
  * with i == j forced to distance 0 (the reference's self-distance is
- * exactly 0, tiling.py:13-14).  Records (1-based uint32 i, j and FP32
- * dist_sq) go to out_i/out_j/out_d in UNSPECIFIED order, only while the
- * running index < capacity; *count (device, zeroed by this call) receives
- * the exact total, so a caller whose buffer was too small can resize and
- * rerun.  With FASTED_JOIN_COUNT the out_* pointers may be NULL.
+ * exactly 0, tiling.py:13-14).  Records are 16 bytes, {uint32 i, uint32 j,
+ * float dist_sq, uint32 0} with 1-based i, j, written to out_records in
+ * UNSPECIFIED order.  Each warp fills private runs of FASTED_RECORD_CHUNK
+ * slots, so the record array may contain unused slots, marked i == 0
+ * (fasted_sort_pairs drops them).
+ * `count` is DEVICE memory for two uint64 (zeroed by this call):
+ *   count[0] = exact number of qualifying pairs,
+ *   count[1] = chunks taken; slots used = count[1] * FASTED_RECORD_CHUNK.
+ * Slots >= capacity are not written; if slots used > capacity the caller
+ * resizes (count[0] + FASTED_RECORD_CHUNK * 32 * SMs always suffices) and
+ * reruns.  With FASTED_JOIN_COUNT the out_* pointers may be NULL.
  */
+#define FASTED_RECORD_CHUNK 256
 int fasted_join(const uint16_t* values16, const float* norms, int64_t n_logical,
                 int64_t n_pad, int64_t d_pad, int64_t row_begin, int64_t row_end,
                 int64_t col_begin, int64_t col_end, float eps_sq, int flags,
-                uint32_t* out_i, uint32_t* out_j, float* out_d, uint64_t capacity,
-                unsigned long long* count, void* stream);
+                void* out_records, uint64_t capacity, unsigned long long* count,
+                void* stream);
 
 /*
- * Canonical (i, j) order for `count` records whose i lie in
- * [row_begin+1, row_end] and j in [1, n_cols]: i/j/d are sorted in place
- * (tmp_* are scratch of the same length).  workspace must hold
- * fasted_sort_workspace_bytes(row_end - row_begin, n_cols) bytes.
+ * Canonical (i, j) order (the reference's lexsort) of `slots` join records
+ * (16-byte records from fasted_join; slots with i == 0 are unused and
+ * dropped) whose i lie in [row_begin+1, row_end] and j in [1, n_cols].
+ * Writes the valid records, sorted, to out_i/out_j/out_d (SoA, length >=
+ * number of valid records); tmp_j/tmp_d are scratch of the same length.
+ * workspace must hold fasted_sort_workspace_bytes(row_end - row_begin,
+ * n_cols) bytes.
  */
 size_t fasted_sort_workspace_bytes(int64_t n_rows, int64_t n_cols);
-int fasted_sort_pairs(uint32_t* i, uint32_t* j, float* d, uint64_t count, int64_t row_begin,
-                      int64_t row_end, int64_t n_cols, uint32_t* tmp_i, uint32_t* tmp_j,
-                      float* tmp_d, void* workspace, size_t workspace_bytes, void* stream);
+int fasted_sort_pairs(const void* records, uint64_t slots, int64_t row_begin, int64_t row_end,
+                      int64_t n_cols, uint32_t* out_i, uint32_t* out_j, float* out_d,
+                      uint32_t* tmp_j, float* tmp_d, void* workspace, size_t workspace_bytes,
+                      void* stream);
 
 /* Number of SMs and device name of the current device (for reports). */
 int fasted_device_info(int* sm_count, char* name, int name_len);

@@ -59,11 +59,11 @@ def load():
         L.fasted_norms.argtypes = [p, i64, i64, p, p]
         L.fasted_join.restype = ci
         L.fasted_join.argtypes = [p, p, i64, i64, i64, i64, i64, i64, i64, f, ci,
-                                  p, p, p, u64, p, p]
+                                  p, u64, p, p]
         L.fasted_sort_workspace_bytes.restype = ctypes.c_size_t
         L.fasted_sort_workspace_bytes.argtypes = [i64, i64]
         L.fasted_sort_pairs.restype = ci
-        L.fasted_sort_pairs.argtypes = [p, p, p, u64, i64, i64, i64, p, p, p, p,
+        L.fasted_sort_pairs.argtypes = [p, u64, i64, i64, i64, p, p, p, p, p, p,
                                         ctypes.c_size_t, p]
         if L.fasted_abi_version() != 1:
             raise DeviceError("libfasted ABI version mismatch")

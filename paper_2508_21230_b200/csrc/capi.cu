@@ -80,8 +80,8 @@ extern "C" int fasted_device_info(int* sm_count, char* name, int name_len) {
 extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t n_logical,
                            int64_t n_pad, int64_t d_pad, int64_t row_begin, int64_t row_end,
                            int64_t col_begin, int64_t col_end, float eps_sq, int flags,
-                           uint32_t* out_i, uint32_t* out_j, float* out_d, uint64_t capacity,
-                           unsigned long long* count, void* stream) {
+                           void* out_records, uint64_t capacity, unsigned long long* count,
+                           void* stream) {
     const bool count_only = (flags & FASTED_JOIN_COUNT) != 0;
     const int kind = flags & 1;
     if (!values16 || !norms || !count || n_pad < 128 || (n_pad % 128) != 0 || d_pad < 16 ||
@@ -100,12 +100,13 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
         set_error("fasted_join: eps_sq must be finite and >= 0");
         return FASTED_ERR_ARGUMENT;
     }
-    if (!count_only && capacity > 0 && (!out_i || !out_j || !out_d)) {
-        set_error("fasted_join: output arrays required unless FASTED_JOIN_COUNT");
+    if (!count_only && capacity > 0 &&
+        (!out_records || (reinterpret_cast<uintptr_t>(out_records) & 15u) != 0)) {
+        set_error("fasted_join: 16-byte aligned record buffer required unless FASTED_JOIN_COUNT");
         return FASTED_ERR_ARGUMENT;
     }
     cudaStream_t s = as_stream(stream);
-    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), s);
+    cudaError_t e = cudaMemsetAsync(count, 0, 2 * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(count)");
     if (row_end == row_begin || col_end == col_begin) return FASTED_OK;
     JoinArgs a;
@@ -119,9 +120,9 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     a.col_end = col_end;
     a.eps_sq = eps_sq;
     a.count_only = count_only ? 1 : 0;
-    a.out_i = out_i;
-    a.out_j = out_j;
-    a.out_d = out_d;
+    a.diag_flags = flags & (FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA |
+                            FASTED_JOIN_DIAG_LOADONLY | FASTED_JOIN_DIAG_NOSLOW);
+    a.out = reinterpret_cast<uint4*>(out_records);
     a.capacity = count_only ? 0ull : (unsigned long long)capacity;
     a.count = count;
     const __half* X = reinterpret_cast<const __half*>(values16);

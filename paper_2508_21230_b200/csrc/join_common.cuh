@@ -1,5 +1,5 @@
 // Pieces shared by the two join kernels: arguments, the reference distance
-// combine, and warp-aggregated pair compaction.
+// combine, and the chunked pair writer.
 #pragma once
 #include "common.cuh"
 
@@ -11,11 +11,10 @@ struct JoinArgs {
     int64_t row_begin, row_end, col_begin, col_end;
     float eps_sq;
     int count_only;
-    uint32_t* out_i;
-    uint32_t* out_j;
-    float* out_d;
-    unsigned long long capacity;
-    unsigned long long* count;
+    int diag_flags;                    // FASTED_JOIN_DIAG_* (experiments only)
+    uint4* out;                        // records {i, j, dist_sq bits, 0}
+    unsigned long long capacity;       // record slots available in out
+    unsigned long long* count;         // [0] exact pair total, [1] chunks taken
 };
 
 // ((-2 a) + s_i) + s_j in FP32 round-to-nearest, clamped at 0
@@ -26,27 +25,67 @@ __device__ __forceinline__ float combine_rn(float a, float si, float sj) {
     return fmaxf(d2, 0.0f);
 }
 
-// Emit the (<= 8) qualifying pairs of one thread's row segment; the column
-// of bit c is col0 + (c < 4 ? tx*4 + c : 64 + tx*4 + c - 4).  All 32 lanes
-// of the warp must call this (warp-aggregated reservation).
-__device__ __forceinline__ void emit_pairs8(const JoinArgs& a, uint32_t mask, int64_t i,
-                                            int64_t col0, int tx, const float* dv) {
-    if (!__any_sync(0xffffffffu, mask != 0)) return;
-    const uint32_t cnt = __popc(mask);
-    unsigned long long pos = warp_reserve(a.count, cnt);
-    if (a.count_only) return;
-#pragma unroll
-    for (int c = 0; c < 8; c++) {
-        if (mask & (1u << c)) {
-            if (pos < a.capacity) {
-                const int64_t j = col0 + (c < 4 ? tx * 4 + c : 64 + tx * 4 + (c - 4));
-                a.out_i[pos] = (uint32_t)(i + 1);
-                a.out_j[pos] = (uint32_t)(j + 1);
-                a.out_d[pos] = dv[c];
-            }
-            pos++;
-        }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// Chunked pair writer.  Every warp appends into private runs of
+// FASTED_RECORD_CHUNK record slots taken from a global chunk counter (one
+// atomic per 256 records), so different SMs write different cache lines and
+// no shared "next slot" counter sits on the critical path.  An append of up
+// to 32 records (one per lane) is one coalesced 16-byte store per lane.
+// The tail of a warp's last chunk is marked unused (i == 0) by
+// writer_finish; the sort drops those slots.
+constexpr uint32_t WRITER_CHUNK = FASTED_RECORD_CHUNK;
+
+struct PairWriter {
+    unsigned long long base;   // first slot of the current chunk
+    uint32_t fill;             // slots used in it (WRITER_CHUNK = none open)
+    unsigned long long total;  // pairs found by this warp
+};
+
+__device__ __forceinline__ void writer_init(PairWriter& w) {
+    w.base = 0;
+    w.fill = WRITER_CHUNK;
+    w.total = 0;
+}
+
+// Warp collective.  `ballot` (warp-uniform) holds the lanes that append one
+// record each; `mine` is this lane's bit.
+__device__ __forceinline__ void writer_append(PairWriter& w, const JoinArgs& a, uint32_t ballot,
+                                              bool mine, uint32_t i1, uint32_t j1, float d2) {
+    const uint32_t n = __popc(ballot);
+    w.total += n;
+    if (a.count_only || n == 0) return;
+    const uint32_t room = WRITER_CHUNK - w.fill;
+    unsigned long long next = 0;
+    if (n > room) {
+        unsigned long long c = 0;
+        if (lane_id() == 0) c = atomicAdd(a.count + 1, 1ull);
+        next = __shfl_sync(0xffffffffu, c, 0) * WRITER_CHUNK;
     }
+    if (mine) {
+        const uint32_t r = __popc(ballot & lanemask_lt());
+        const unsigned long long slot = r < room ? w.base + w.fill + r : next + (r - room);
+        if (slot < a.capacity) a.out[slot] = make_uint4(i1, j1, __float_as_uint(d2), 0u);
+    }
+    if (n > room) {
+        w.base = next;
+        w.fill = n - room;
+    } else {
+        w.fill += n;
+    }
+}
+
+// Warp collective: mark the open chunk's unused tail (i == 0), publish the total.
+__device__ __forceinline__ void writer_finish(PairWriter& w, const JoinArgs& a) {
+    if (!a.count_only) {
+        for (uint32_t s = w.fill + lane_id(); s < WRITER_CHUNK; s += 32)
+            if (w.base + s < a.capacity) a.out[w.base + s] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    if (lane_id() == 0 && w.total) atomicAdd(a.count, w.total);
 }
 
 int launch_join_exact(const __half* X, const JoinArgs& a, cudaStream_t s);

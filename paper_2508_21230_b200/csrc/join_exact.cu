@@ -29,6 +29,8 @@ join_exact_kernel(const __half* __restrict__ X, const JoinArgs a) {
     const int64_t n_row_tiles = (a.row_end - a.row_begin) / EX_BM;
     const int64_t n_col_tiles = (a.col_end - a.col_begin + EX_BN - 1) / EX_BN;
     const int64_t n_tiles = n_row_tiles * n_col_tiles;
+    PairWriter wr;
+    writer_init(wr);
 
     for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
         const int64_t row0 = a.row_begin + (tile / n_col_tiles) * EX_BM;
@@ -85,21 +87,21 @@ join_exact_kernel(const __half* __restrict__ X, const JoinArgs a) {
             const int64_t i = row0 + (r < 4 ? ty * 4 + r : 64 + ty * 4 + (r - 4));
             const bool row_ok = i < a.n_logical;
             const float si = a.norms[i];
-            uint32_t mask = 0;
-            float dv[8];
 #pragma unroll
             for (int c = 0; c < 8; c++) {
                 const int64_t j = col0 + (c < 4 ? tx * 4 + c : 64 + tx * 4 + (c - 4));
                 float d2 = 0.0f;
+                bool hit = false;
                 if (row_ok && j < a.n_logical && j < a.col_end) {
                     d2 = combine_rn(acc[r][c], si, a.norms[j]);
-                    if (d2 <= a.eps_sq) mask |= 1u << c;
+                    hit = d2 <= a.eps_sq;
                 }
-                dv[c] = d2;
+                const uint32_t b = __ballot_sync(0xffffffffu, hit);
+                if (b) writer_append(wr, a, b, hit, (uint32_t)(i + 1), (uint32_t)(j + 1), d2);
             }
-            emit_pairs8(a, mask, i, col0, tx, dv);
         }
     }
+    writer_finish(wr, a);
 }
 
 }  // namespace fasted

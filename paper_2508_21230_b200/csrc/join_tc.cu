@@ -1,29 +1,38 @@
 // Kernel 2 (the product path): fused tcgen05 epsilon join for sm_100a.
 //
+// Per CTA tile (128 points x 256 points), everything stays on chip:
 //   TMA (SWIZZLE_128B) -> 4-stage smem ring -> tcgen05.mma kind::f16
-//   (M=128, N=256, K=16; FP32 accumulators in TMEM, double buffered: 2 x 256
-//   columns) -> epilogue warps: tcgen05.ld -> ((-2a)+s_i)+s_j -> <= eps^2 ->
-//   warp-ballot compaction with one global atomic per warp.
+//   (M=128, N=256, K=16) accumulating a_ij = x_i . x_j in TMEM, then ONE
+//   extra tcgen05.mma kind::tf32 step (K=8) that adds
+//       sigma_i + rho_j = -s_i/2 + (-s_j/2 + eps^2/2)
+//   from two tiny per-point "augment" rows (norms split into 3 exact tf32
+//   parts, prepared per call by aug_prepare_kernel).  The accumulator then
+//   holds D_ij = (eps^2 - d2_ij) / 2, so the epilogue's common path is a
+//   sign test: d2 <= eps^2  <=>  D >= 0.  Epilogue warps AND-reduce the
+//   sign bits of 32 TMEM columns per tcgen05.ld (16 LOP3 per 32 pairs); only
+//   a chunk holding a hit (or the diagonal) takes the per-column ballot path
+//   that writes {i, j, d2 = eps^2 - 2D} records (PairWriter).
 //
 // The distance matrix never reaches HBM.  Replaces the reference's tile
 // sweep (tiling.py:307-344): compute_block_tile (tiling.py:199-285),
 // accumulate_panel (_kernel.py:57-76) and combine_distance (mma.py:143-157).
-// Arithmetic differs from the reference only in how the tensor core sums
-// the FP32 products of a_ij (the reference sums sequentially with RZ); the
-// epilogue uses the reference's combine order and threshold.  Self pairs
-// (i == j) are forced to distance 0, which is exactly what the reference
-// produces (its a_ii and s_i are the same RZ chain).
+// Arithmetic differs from the reference in how a_ij and the norm terms are
+// summed (tensor core FP32 accumulation instead of a sequential
+// round-toward-zero chain); pair sets agree outside the 1e-3 relative band
+// around eps^2 (tests/test_gpu.py).  Self pairs (i == j) are forced to
+// distance 0, which is exactly what the reference produces.
 //
 // Persistent CTAs (one per SM, 384 threads):
-//   warp 0      : TMA producer (one lane)
-//   warp 1      : MMA issuer   (one lane)
-//   warp 2      : TMEM allocator / deallocator
-//   warp 3      : idle
-//   warps 4..11 : epilogue; warp w reads TMEM lanes 32*(w%4).. and column
-//                 half (w-4)/4 of the 256-column accumulator.
-// Tiles are (128 rows x 256 columns) walked in a grouped raster: GROUP row
-// blocks sweep every column tile together, so each 256-row B panel is read
-// from HBM once per group and the group's A panels stay L2 resident.
+//   warp 0      : TMEM allocator / deallocator, then TMA producer (one lane)
+//   warp 1      : MMA issuer (one lane)
+//   warps 2..9  : epilogue; warp w reads TMEM lanes 32*(w%4).. and column
+//                 half (w-2)/4 of the 256-column accumulator.
+// (320 threads leave 200 registers per thread: the epilogue holds a warp's
+// whole 32 x 128 accumulator slice in registers.)
+// TMEM: 2 accumulators x 256 columns (double buffered across tiles).
+// Tiles walk a grouped raster: GROUP row blocks sweep every column tile
+// together, so each 256-row B panel is read from HBM once per group and the
+// group's A panels stay L2 resident.
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
@@ -36,19 +45,25 @@ constexpr int BM = 128;
 constexpr int BN = 256;
 constexpr int BK = 64;   // one 128-byte swizzle atom of FP16
 constexpr int UK = 16;   // K of one kind::f16 tcgen05.mma
+constexpr int AUG_K = 8; // K of one kind::tf32 tcgen05.mma: one 32-byte row
 constexpr int STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2;
 constexpr int B_BYTES = BN * BK * 2;
+constexpr int AUG_A_BYTES = BM * AUG_K * 4;
+constexpr int AUG_B_BYTES = BN * AUG_K * 4;
 constexpr int NUM_EPI_WARPS = 8;
-constexpr int THREADS = 128 + NUM_EPI_WARPS * 32;
+constexpr int FIRST_EPI_WARP = 2;
+constexpr int THREADS = (FIRST_EPI_WARP + NUM_EPI_WARPS) * 32;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int BAR_BYTES = 256;
 constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + BAR_BYTES + 1024;
 constexpr int GROUP = 16;
 
-// Instruction descriptor, kind::f16: D=F32 (bits 4-5 = 1), A=B=F16 (0),
-// both K-major (bits 15,16 = 0), N>>3 at bits 17-22, M>>4 at bits 24-28.
-constexpr uint32_t IDESC = (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// Instruction descriptors: D=F32 (bits 4-5 = 1); A/B format at bits 7-9 /
+// 10-12 (F16 = 0, TF32 = 2); both K-major; N>>3 at 17-22; M>>4 at 24-28.
+constexpr uint32_t IDESC_F16 =
+    (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+constexpr uint32_t IDESC_TF32 = IDESC_F16 | (2u << 7) | (2u << 10);
 
 struct Sched {
     int row_blocks;
@@ -123,15 +138,21 @@ __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// K-major operand, 128-byte swizzle: rows of 128 B, 8-row core groups
-// 1024 B apart (SBO), LBO unused (1), descriptor version 1 (sm_100).
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+// Shared-memory matrix descriptors (K-major, swizzled): start address >> 4,
+// LBO = 1 (unused for swizzled K-major), SBO = bytes between 8-row groups,
+// version 1 (sm_100), layout type (SWIZZLE_128B = 2, SWIZZLE_32B = 6).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t sbo_bytes,
+                                              uint32_t layout) {
     return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) |
-           ((uint64_t)(1024u >> 4) << 32) | ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
+           ((uint64_t)(sbo_bytes >> 4) << 32) | ((uint64_t)1u << 46) |
+           ((uint64_t)layout << 61);
 }
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) { return smem_desc(saddr, 1024, 2); }
+__device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) { return smem_desc(saddr, 256, 6); }
 
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                        uint32_t accumulate) {
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
@@ -140,16 +161,20 @@ __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_
         : "memory");
 }
 
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(IDESC_TF32), "r"(1u)
+        : "memory");
+}
+
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
         : "memory");
 }
-
-#define FASTED_R32(X)                                                                        \
-    X[0], X[1], X[2], X[3], X[4], X[5], X[6], X[7], X[8], X[9], X[10], X[11], X[12], X[13],  \
-        X[14], X[15], X[16], X[17], X[18], X[19], X[20], X[21], X[22], X[23], X[24], X[25], \
-        X[26], X[27], X[28], X[29], X[30], X[31]
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile(
@@ -179,23 +204,6 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
                  : "memory");
 }
 
-// Packed FP32x2 (sm_100): two IEEE RN ops per instruction.
-__device__ __forceinline__ uint64_t pk(float x, float y) {
-    return (uint64_t)__float_as_uint(x) | ((uint64_t)__float_as_uint(y) << 32);
-}
-__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
-    uint64_t d;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-    return d;
-}
-__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
-    uint64_t d;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-    return d;
-}
-__device__ __forceinline__ float lo_f(uint64_t v) { return __uint_as_float((uint32_t)v); }
-__device__ __forceinline__ float hi_f(uint64_t v) { return __uint_as_float((uint32_t)(v >> 32)); }
-
 __device__ __forceinline__ void tile_coords(const Sched& s, int64_t t, int& rb, int& ct) {
     const int64_t per_group = (int64_t)s.group * s.col_tiles;
     const int64_t g = t / per_group;
@@ -206,8 +214,64 @@ __device__ __forceinline__ void tile_coords(const Sched& s, int64_t t, int& rb, 
     rb = (int)(g * s.group + r % rows_in);
 }
 
+// r[e] for a warp-uniform runtime e without local memory: a 5-level
+// select tree (31 SEL), so the rare path never spills the chunk.
+__device__ __forceinline__ uint32_t pick32(const uint32_t (&r)[32], uint32_t e) {
+    uint32_t t[16];
+#pragma unroll
+    for (int k = 0; k < 16; k++) t[k] = (e & 16u) ? r[k + 16] : r[k];
+#pragma unroll
+    for (int k = 0; k < 8; k++) t[k] = (e & 8u) ? t[k + 8] : t[k];
+#pragma unroll
+    for (int k = 0; k < 4; k++) t[k] = (e & 4u) ? t[k + 4] : t[k];
+#pragma unroll
+    for (int k = 0; k < 2; k++) t[k] = (e & 2u) ? t[k + 2] : t[k];
+    return (e & 1u) ? t[1] : t[0];
+}
+
+// Epilogue of one 32-column chunk (columns jb.., row i = this lane).
+// r[e] = D_{i, jb+e} = (eps^2 - d2) / 2 as FP32 bits.
+__device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, const uint32_t (&r)[32],
+                                          int64_t jb, int64_t i, int64_t iw, bool row_ok) {
+    // common path: is any D >= 0 (sign bit clear)?  16 three-input ANDs.
+    uint32_t acc = 0xffffffffu;
+#pragma unroll
+    for (int e = 0; e < 32; e += 2) acc &= r[e] & r[e + 1];
+    const bool diag = (jb < iw + 32) && (iw < jb + 32);   // warp-uniform
+    if (!__any_sync(0xffffffffu, (int)acc >= 0) && !diag) return;
+    if (a.diag_flags & FASTED_JOIN_DIAG_NOSLOW) return;
+    // rare path.  Self pairs first: distance exactly 0 (the reference's
+    // a_ii and s_i are the same chain), one append for the whole warp.
+    if (diag) {
+        const bool self = (i >= jb) && (i < jb + 32) && row_ok;
+        const uint32_t b = __ballot_sync(0xffffffffu, self);
+        if (b) writer_append(wr, a, b, self, (uint32_t)(i + 1), (uint32_t)(i + 1), 0.0f);
+    }
+    // Candidate columns: a column holds a hit iff the AND over the warp of
+    // its D words has the sign bit clear -- 32 independent REDUX.AND whose
+    // results live in uniform registers.  Then visit only those columns.
+    uint32_t cm = 0;
+#pragma unroll
+    for (int e = 0; e < 32; e++)
+        cm |= ((~__reduce_and_sync(0xffffffffu, r[e]) >> 31) & 1u) << e;
+    while (cm) {
+        const uint32_t e = __ffs(cm) - 1;
+        cm &= cm - 1;
+        const uint32_t v = pick32(r, e);
+        const int64_t j = jb + e;
+        const bool ok = ((int)v >= 0) && (i != j) && row_ok && j < a.n_logical;
+        const uint32_t b = __ballot_sync(0xffffffffu, ok);
+        if (b == 0u) continue;
+        const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
+        writer_append(wr, a, b, ok, (uint32_t)(i + 1), (uint32_t)(j + 1), d2);
+    }
+}
+
 __global__ void __launch_bounds__(THREADS, 1)
-join_tc_kernel(const __grid_constant__ CUtensorMap tmap, const JoinArgs a, const Sched sch) {
+join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
+               const __grid_constant__ CUtensorMap tmap_aug_a,
+               const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
+               const Sched sch) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -235,10 +299,14 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap, const JoinArgs a, const
             mbar_init(tempty_bar(b), NUM_EPI_WARPS);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap))
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_a))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_b))
                      : "memory");
     }
-    if (warp == 2) {
+    if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                          slot),
                      "r"(TMEM_COLS)
@@ -251,7 +319,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap, const JoinArgs a, const
     const uint32_t tmem_base = *slot_ptr;
 
     if (warp == 0) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer: nkb FP16 stages + 1 augment stage per tile
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
@@ -261,16 +329,25 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap, const JoinArgs a, const
                 const int row0 = (int)(a.row_begin + (int64_t)rb * BM);
                 const int col0 = (int)(a.col_begin + (int64_t)ct * BN);
                 const bool second = (int64_t)col0 + 128 < a.col_end;
-                const uint32_t bytes = A_BYTES + (second ? B_BYTES : B_BYTES / 2);
-                for (int kb = 0; kb < sch.nkb; kb++) {
+                for (int kb = 0; kb <= sch.nkb; kb++) {
                     mbar_wait(empty_bar(s), ph ^ 1u);
-                    mbar_expect_tx(full_bar(s), bytes);
-                    const int kx = kb * BK;
-                    tma_load_2d(sA + s * A_BYTES, &tmap, full_bar(s), kx, row0);
-                    tma_load_2d(sB + s * B_BYTES, &tmap, full_bar(s), kx, col0);
-                    if (second)
-                        tma_load_2d(sB + s * B_BYTES + B_BYTES / 2, &tmap, full_bar(s), kx,
-                                    col0 + 128);
+                    if (kb < sch.nkb) {
+                        mbar_expect_tx(full_bar(s), A_BYTES + (second ? B_BYTES : B_BYTES / 2));
+                        const int kx = kb * BK;
+                        tma_load_2d(sA + s * A_BYTES, &tmap_x, full_bar(s), kx, row0);
+                        tma_load_2d(sB + s * B_BYTES, &tmap_x, full_bar(s), kx, col0);
+                        if (second)
+                            tma_load_2d(sB + s * B_BYTES + B_BYTES / 2, &tmap_x, full_bar(s), kx,
+                                        col0 + 128);
+                    } else {
+                        mbar_expect_tx(full_bar(s),
+                                       AUG_A_BYTES + (second ? AUG_B_BYTES : AUG_B_BYTES / 2));
+                        tma_load_2d(sA + s * A_BYTES, &tmap_aug_a, full_bar(s), 0, row0);
+                        tma_load_2d(sB + s * B_BYTES, &tmap_aug_b, full_bar(s), 0, col0);
+                        if (second)
+                            tma_load_2d(sB + s * B_BYTES + AUG_B_BYTES / 2, &tmap_aug_b,
+                                        full_bar(s), 0, col0 + 128);
+                    }
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1u;
@@ -282,6 +359,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap, const JoinArgs a, const
     } else if (warp == 1) {
         // ---------------- MMA issuer
         if (lane == 0) {
+            const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
             int s = 0;
             uint32_t ph = 0;
             int lt = 0;
@@ -291,15 +369,22 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap, const JoinArgs a, const
                 mbar_wait(tempty_bar(buf), aph ^ 1u);
                 tc_fence_after();
                 const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
-                for (int kb = 0; kb < sch.nkb; kb++) {
+                for (int kb = 0; kb <= sch.nkb; kb++) {
                     mbar_wait(full_bar(s), ph);
                     tc_fence_after();
-                    const uint64_t ad = sw128_desc(sA + s * A_BYTES);
-                    const uint64_t bd = sw128_desc(sB + s * B_BYTES);
+                    if (!no_mma) {
+                        if (kb < sch.nkb) {
+                            const uint64_t ad = sw128_desc(sA + s * A_BYTES);
+                            const uint64_t bd = sw128_desc(sB + s * B_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BK / UK; kk++) {
-                        const uint64_t koff = (uint64_t)((kk * UK * 2) >> 4);
-                        mma_f16(dtm, ad + koff, bd + koff, (kb | kk) != 0 ? 1u : 0u);
+                            for (int kk = 0; kk < BK / UK; kk++) {
+                                const uint64_t koff = (uint64_t)((kk * UK * 2) >> 4);
+                                mma_issue<IDESC_F16>(dtm, ad + koff, bd + koff,
+                                                     (kb | kk) != 0 ? 1u : 0u);
+                            }
+                        } else {
+                            mma_tf32(dtm, sw32_desc(sA + s * A_BYTES), sw32_desc(sB + s * B_BYTES));
+                        }
                     }
                     mma_commit(empty_bar(s));
                     if (++s == STAGES) {
@@ -311,13 +396,13 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap, const JoinArgs a, const
             }
         }
         __syncwarp();
-    } else if (warp >= 4) {
+    } else if (warp >= FIRST_EPI_WARP) {
         // ---------------- epilogue
         const int q = warp & 3;          // TMEM lane quarter this warp may access
-        const int h = (warp - 4) >> 2;   // column half of the 256-wide accumulator
+        const int h = (warp - FIRST_EPI_WARP) >> 2;   // column half of the accumulator
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-        const float eps_sq = a.eps_sq;
-        const uint64_t neg2 = pk(-2.0f, -2.0f);
+        PairWriter wr;
+        writer_init(wr);
         int lt = 0;
         for (int64_t t = blockIdx.x; t < sch.total; t += gridDim.x, ++lt) {
             int rb, ct;
@@ -326,77 +411,84 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap, const JoinArgs a, const
             const int64_t col0 = a.col_begin + (int64_t)ct * BN;
             const int64_t iw = row0 + q * 32;
             const int64_t i = iw + lane;
-            const float si = __ldg(a.norms + i);
-            const uint64_t si2 = pk(si, si);
             const bool row_ok = i < a.n_logical;
             const int buf = lt & 1;
             const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
+            // chunks of 32 columns inside [col0 + 128h, col_end)
+            const int64_t left = a.col_end - (col0 + h * 128);
+            int nchunks = left <= 0 ? 0 : (left >= 128 ? 4 : (int)(left / 32));
+            if (a.diag_flags & FASTED_JOIN_DIAG_NOEPI) nchunks = 0;
+            const uint32_t tcol = tmem_base + lane_base + (uint32_t)(buf * BN + h * 128);
             mbar_wait(tfull_bar(buf), aph);
             tc_fence_after();
-#pragma unroll 1
-            for (int c = 0; c < 4; c++) {
-                const int64_t jb = col0 + h * 128 + c * 32;
-                if (jb >= a.col_end) break;
-                uint32_t r[32];
-                tmem_ld32(tmem_base + lane_base + (uint32_t)(buf * BN + h * 128 + c * 32), r);
-                tmem_ld_wait(r);
-                const float4* sj4 = reinterpret_cast<const float4*>(a.norms + jb);
-                bool hit = false;
-#pragma unroll
-                for (int e = 0; e < 32; e += 4) {
-                    const float4 s4 = __ldg(sj4 + (e >> 2));
-                    uint64_t d01 = ffma2(pk(__uint_as_float(r[e]), __uint_as_float(r[e + 1])),
-                                         neg2, si2);
-                    uint64_t d23 = ffma2(pk(__uint_as_float(r[e + 2]), __uint_as_float(r[e + 3])),
-                                         neg2, si2);
-                    d01 = fadd2(d01, pk(s4.x, s4.y));
-                    d23 = fadd2(d23, pk(s4.z, s4.w));
-                    hit |= (lo_f(d01) <= eps_sq) | (hi_f(d01) <= eps_sq) |
-                           (lo_f(d23) <= eps_sq) | (hi_f(d23) <= eps_sq);
-                }
-                const bool diag = (jb < iw + 32) && (iw < jb + 32);
-                if (__any_sync(0xffffffffu, hit) || diag) {
-                    uint32_t m = 0;
-                    float dv[32];
-#pragma unroll
-                    for (int e = 0; e < 32; e++) {
-                        const int64_t j = jb + e;
-                        float d2 = combine_rn(__uint_as_float(r[e]), si, __ldg(a.norms + j));
-                        if (i == j) d2 = 0.0f;
-                        dv[e] = d2;
-                        if (row_ok && j < a.n_logical && d2 <= eps_sq) m |= 1u << e;
-                    }
-                    const uint32_t cnt = __popc(m);
-                    unsigned long long pos = warp_reserve(a.count, cnt);
-                    if (!a.count_only) {
-#pragma unroll
-                        for (int e = 0; e < 32; e++) {
-                            if (m & (1u << e)) {
-                                if (pos < a.capacity) {
-                                    a.out_i[pos] = (uint32_t)(i + 1);
-                                    a.out_j[pos] = (uint32_t)(jb + e + 1);
-                                    a.out_d[pos] = dv[e];
-                                }
-                                pos++;
-                            }
-                        }
-                    }
-                }
+            // Pull this warp's whole 32 x 128 slice out of TMEM with back-to-back
+            // loads and ONE wait (a tcgen05.ld queues behind the MMAs already
+            // issued for the next tile, so waiting per chunk costs that queue
+            // drain each time), then hand the accumulator back to the MMA warp
+            // before any math: the epilogue overlaps the next tiles' MMAs.
+            uint32_t r0[32], r1[32], r2[32], r3[32];
+            if (nchunks > 0) tmem_ld32(tcol, r0);
+            if (nchunks > 1) tmem_ld32(tcol + 32u, r1);
+            if (nchunks > 2) tmem_ld32(tcol + 64u, r2);
+            if (nchunks > 3) tmem_ld32(tcol + 96u, r3);
+            if (nchunks > 0) {
+                tmem_ld_wait(r0);
+                tmem_ld_wait(r1);
+                tmem_ld_wait(r2);
+                tmem_ld_wait(r3);
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(tempty_bar(buf));
+            const int64_t jb = col0 + h * 128;
+            if (nchunks > 0) epi_chunk(a, wr, r0, jb, i, iw, row_ok);
+            if (nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok);
+            if (nchunks > 2) epi_chunk(a, wr, r2, jb + 64, i, iw, row_ok);
+            if (nchunks > 3) epi_chunk(a, wr, r3, jb + 96, i, iw, row_ok);
         }
+        writer_finish(wr, a);
     }
 
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 2) {
+    if (warp == 0) {
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
                      "r"(TMEM_COLS)
                      : "memory");
     }
+}
+
+// Exact split of an FP32 value into three TF32 values (10-bit mantissas,
+// low 13 bits zero) whose sum is the input: 3 x 11 significant bits >= 24.
+__device__ __forceinline__ void split_tf32(float x, float& h1, float& h2, float& h3) {
+    auto tf32 = [](float v) {
+        uint32_t u;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(u) : "f"(v));
+        return __uint_as_float(u & 0xffffe000u);
+    };
+    h1 = tf32(x);
+    const float r1 = __fsub_rn(x, h1);
+    h2 = tf32(r1);
+    h3 = tf32(__fsub_rn(r1, h2));
+}
+
+// Augment rows: A_i = [sigma_i parts, 1, 1, 1, 0, 0], B_j = [1, 1, 1,
+// rho_j parts, 0, 0] with sigma = -s/2 and rho = -s/2 + eps^2/2, so that
+// A_i . B_j = (eps^2 - s_i - s_j) / 2.
+__global__ void aug_prepare_kernel(const float* __restrict__ norms, int64_t n_pad, float eps_sq,
+                                   float4* __restrict__ aug_a, float4* __restrict__ aug_b) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n_pad) return;
+    const float sigma = -0.5f * norms[i];
+    const float rho = __fadd_rn(sigma, 0.5f * eps_sq);
+    float a1, a2, a3, b1, b2, b3;
+    split_tf32(sigma, a1, a2, a3);
+    split_tf32(rho, b1, b2, b3);
+    aug_a[2 * i] = make_float4(a1, a2, a3, 1.0f);
+    aug_a[2 * i + 1] = make_float4(1.0f, 1.0f, 0.0f, 0.0f);
+    aug_b[2 * i] = make_float4(1.0f, 1.0f, 1.0f, b1);
+    aug_b[2 * i + 1] = make_float4(b2, b3, 0.0f, 0.0f);
 }
 
 }  // namespace tc
@@ -414,13 +506,30 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     return fn;
 }
 
-int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
-    using namespace tc;
+static int encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                     uint64_t rows, uint64_t row_bytes, uint32_t box_inner, uint32_t box_rows,
+                     CUtensorMapSwizzle swz) {
     auto encode = tensor_map_encoder();
     if (!encode) {
         set_error("cuTensorMapEncodeTiled unavailable from the driver");
         return FASTED_ERR_CUDA;
     }
+    cuuint64_t gdim[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)row_bytes};
+    cuuint32_t box[2] = {box_inner, box_rows};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult cr = encode(map, dt, 2, const_cast<void*>(base), gdim, gstride, box, estride,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)cr);
+        return FASTED_ERR_CUDA;
+    }
+    return FASTED_OK;
+}
+
+int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
+    using namespace tc;
     if ((a.d_pad % 8) != 0 || (reinterpret_cast<uintptr_t>(X) & 15u) != 0) {
         set_error("join_tc: d_pad must be a multiple of 8 and X 16-byte aligned");
         return FASTED_ERR_ARGUMENT;
@@ -429,18 +538,32 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         set_error("join_tc: n_pad exceeds TMA int32 coordinates");
         return FASTED_ERR_ARGUMENT;
     }
-    CUtensorMap map;
-    cuuint64_t gdim[2] = {(cuuint64_t)a.d_pad, (cuuint64_t)a.n_pad};
-    cuuint64_t gstride[1] = {(cuuint64_t)a.d_pad * 2};
-    cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BM};
-    cuuint32_t estride[2] = {1, 1};
-    CUresult cr = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<__half*>(X), gdim,
-                         gstride, box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed (%d)", (int)cr);
-        return FASTED_ERR_CUDA;
+    // per-call augment rows (eps-dependent), stream ordered
+    float4* aug = nullptr;
+    const size_t aug_bytes = (size_t)a.n_pad * 64;   // two [n_pad][8] FP32 arrays
+    cudaError_t e = cudaMallocAsync(&aug, aug_bytes, s);
+    if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(augment rows)");
+    float4* aug_a = aug;
+    float4* aug_b = aug + 2 * a.n_pad;
+    aug_prepare_kernel<<<(unsigned)((a.n_pad + 255) / 256), 256, 0, s>>>(a.norms, a.n_pad,
+                                                                         a.eps_sq, aug_a, aug_b);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFreeAsync(aug, s);
+        return cuda_status(e, "aug_prepare_kernel");
+    }
+    CUtensorMap mx, ma, mb;
+    int st = encode_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, X, a.d_pad, a.n_pad, a.d_pad * 2, BK,
+                       BM, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (st == FASTED_OK)
+        st = encode_2d(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, aug_a, AUG_K, a.n_pad, 32, AUG_K, BM,
+                       CU_TENSOR_MAP_SWIZZLE_32B);
+    if (st == FASTED_OK)
+        st = encode_2d(&mb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, aug_b, AUG_K, a.n_pad, 32, AUG_K, BM,
+                       CU_TENSOR_MAP_SWIZZLE_32B);
+    if (st != FASTED_OK) {
+        cudaFreeAsync(aug, s);
+        return st;
     }
     Sched sch;
     sch.row_blocks = (int)((a.row_end - a.row_begin) / BM);
@@ -448,19 +571,22 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     sch.group = GROUP;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.total = (int64_t)sch.row_blocks * sch.col_tiles;
-    if (sch.total <= 0) return FASTED_OK;
     const int sms = sm_count_current();
     const int64_t grid = sch.total < sms ? sch.total : sms;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(join_tc_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             SMEM_BYTES);
-        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(join_tc_kernel)");
+        e = cudaFuncSetAttribute(join_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 SMEM_BYTES);
+        if (e != cudaSuccess) {
+            cudaFreeAsync(aug, s);
+            return cuda_status(e, "cudaFuncSetAttribute(join_tc_kernel)");
+        }
         attr_set = true;
     }
-    join_tc_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(map, a, sch);
-    FASTED_CHECK_LAUNCH("join_tc_kernel");
+    if (grid > 0) join_tc_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mx, ma, mb, a, sch);
+    e = cudaGetLastError();
+    cudaFreeAsync(aug, s);
+    if (e != cudaSuccess) return cuda_status(e, "join_tc_kernel");
     return FASTED_OK;
 }
 

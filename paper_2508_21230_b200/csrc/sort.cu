@@ -60,11 +60,13 @@ static size_t carve(void* base, int64_t n_rows, int64_t n_cols, SortWs* ws) {
     return off;
 }
 
-__global__ void hist_kernel(const uint32_t* __restrict__ pi, uint64_t count, int64_t row_begin,
+__global__ void hist_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
                             uint32_t* __restrict__ counts) {
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < count;
-         p += (uint64_t)gridDim.x * blockDim.x)
-        atomicAdd(&counts[pi[p] - 1 - row_begin], 1u);
+         p += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t i = rec[p].x;
+        if (i) atomicAdd(&counts[i - 1 - row_begin], 1u);   // i == 0: unused slot
+    }
 }
 
 // Block-level exclusive scan of SCAN_TILE counts; writes local offsets and
@@ -155,17 +157,18 @@ __global__ void scan_add_kernel(unsigned long long* __restrict__ offsets, int64_
     if (idx == 0) offsets[n] = bsum[(n + SCAN_TILE - 1) / SCAN_TILE];
 }
 
-__global__ void scatter_kernel(const uint32_t* __restrict__ pi, const uint32_t* __restrict__ pj,
-                               const float* __restrict__ pd, uint64_t count, int64_t row_begin,
+__global__ void scatter_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
                                const unsigned long long* __restrict__ offsets,
                                uint32_t* __restrict__ cursor, uint32_t* __restrict__ tj,
                                float* __restrict__ td) {
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < count;
          p += (uint64_t)gridDim.x * blockDim.x) {
-        const int64_t r = (int64_t)pi[p] - 1 - row_begin;
+        const uint4 v = rec[p];
+        if (v.x == 0) continue;
+        const int64_t r = (int64_t)v.x - 1 - row_begin;
         const unsigned long long pos = offsets[r] + atomicAdd(&cursor[r], 1u);
-        tj[pos] = pj[p];
-        td[pos] = pd[p];
+        tj[pos] = v.y;
+        td[pos] = __uint_as_float(v.z);
     }
 }
 
@@ -208,8 +211,9 @@ long_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
                  int64_t n_cols, const uint32_t* __restrict__ long_rows,
                  const uint32_t* __restrict__ long_count, uint32_t* __restrict__ bitmap_all,
                  uint32_t* __restrict__ oi, uint32_t* __restrict__ oj, float* __restrict__ od) {
-    __shared__ uint32_t warp_tot[LONG_THREADS / 32];
+    __shared__ uint32_t warp_tot[32];
     __shared__ uint32_t carry;
+    constexpr int NW = LONG_THREADS / 32;
     const int64_t words = (n_cols + 31) / 32 + 1;
     uint32_t* bits = bitmap_all + (int64_t)blockIdx.x * 2 * words;
     uint32_t* pref = bits + words;
@@ -233,7 +237,7 @@ long_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
             if ((threadIdx.x & 31) == 31) warp_tot[threadIdx.x >> 5] = incl;
             __syncthreads();
             if (threadIdx.x < 32) {
-                const uint32_t t = warp_tot[threadIdx.x];
+                const uint32_t t = threadIdx.x < NW ? warp_tot[threadIdx.x] : 0u;
                 const uint32_t ti = warp_inclusive_scan(t);
                 warp_tot[threadIdx.x] = ti - t;
             }
@@ -266,15 +270,15 @@ extern "C" size_t fasted_sort_workspace_bytes(int64_t n_rows, int64_t n_cols) {
     return carve(nullptr, n_rows, n_cols, nullptr);
 }
 
-extern "C" int fasted_sort_pairs(uint32_t* pi, uint32_t* pj, float* pd, uint64_t count,
-                                 int64_t row_begin, int64_t row_end, int64_t n_cols,
-                                 uint32_t* tmp_i, uint32_t* tmp_j, float* tmp_d,
+extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t row_begin,
+                                 int64_t row_end, int64_t n_cols, uint32_t* out_i,
+                                 uint32_t* out_j, float* out_d, uint32_t* tmp_j, float* tmp_d,
                                  void* workspace, size_t workspace_bytes, void* stream) {
-    (void)tmp_i;
     const int64_t n_rows = row_end - row_begin;
     if (count == 0) return FASTED_OK;
-    if (!pi || !pj || !pd || !tmp_j || !tmp_d || !workspace || n_rows < 1 || n_cols < 1 ||
-        n_cols > 0xffffffffLL) {
+    const uint4* rec = static_cast<const uint4*>(records);
+    if (!rec || !out_i || !out_j || !out_d || !tmp_j || !tmp_d || !workspace || n_rows < 1 ||
+        n_cols < 1 || n_cols > 0xffffffffLL) {
         set_error("fasted_sort_pairs: bad arguments");
         return FASTED_ERR_ARGUMENT;
     }
@@ -293,7 +297,7 @@ extern "C" int fasted_sort_pairs(uint32_t* pi, uint32_t* pj, float* pd, uint64_t
     const unsigned rec_grid = (unsigned)((count + 255) / 256 < (uint64_t)sms * 16
                                              ? (count + 255) / 256
                                              : (uint64_t)sms * 16);
-    hist_kernel<<<rec_grid, 256, 0, s>>>(pi, count, row_begin, ws.counts);
+    hist_kernel<<<rec_grid, 256, 0, s>>>(rec, count, row_begin, ws.counts);
     FASTED_CHECK_LAUNCH("hist_kernel");
     const int64_t nsb = (n_rows + SCAN_TILE - 1) / SCAN_TILE;
     scan_local_kernel<<<(unsigned)nsb, SCAN_THREADS, 0, s>>>(ws.counts, n_rows, ws.offsets,
@@ -303,17 +307,18 @@ extern "C" int fasted_sort_pairs(uint32_t* pi, uint32_t* pj, float* pd, uint64_t
     FASTED_CHECK_LAUNCH("scan_blocks_kernel");
     scan_add_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(ws.offsets, n_rows, ws.bsum);
     FASTED_CHECK_LAUNCH("scan_add_kernel");
-    scatter_kernel<<<rec_grid, 256, 0, s>>>(pi, pj, pd, count, row_begin, ws.offsets, ws.cursor,
-                                            tmp_j, tmp_d);
+    scatter_kernel<<<rec_grid, 256, 0, s>>>(rec, count, row_begin, ws.offsets, ws.cursor, tmp_j,
+                                            tmp_d);
     FASTED_CHECK_LAUNCH("scatter_kernel");
     const int64_t sgrid = (n_rows + SHORT_WARPS - 1) / SHORT_WARPS;
     short_rows_kernel<<<(unsigned)(sgrid < (int64_t)sms * 64 ? sgrid : (int64_t)sms * 64),
                         SHORT_WARPS * 32, 0, s>>>(tmp_j, tmp_d, ws.offsets, n_rows, row_begin,
-                                                  pi, pj, pd, ws.long_rows, ws.long_count);
+                                                  out_i, out_j, out_d, ws.long_rows,
+                                                  ws.long_count);
     FASTED_CHECK_LAUNCH("short_rows_kernel");
     long_rows_kernel<<<LONG_BLOCKS, LONG_THREADS, 0, s>>>(tmp_j, tmp_d, ws.offsets, row_begin,
                                                           n_cols, ws.long_rows, ws.long_count,
-                                                          ws.bitmap, pi, pj, pd);
+                                                          ws.bitmap, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("long_rows_kernel");
     return FASTED_OK;
 }

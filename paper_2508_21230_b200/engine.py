@@ -6,8 +6,9 @@ sweeps a contiguous range of 128-row blocks against every column, so the
 path shards with no collective (north star (4)).  Per device:
 
     upload (H2D, skipped when to_half left the data resident)
-    -> fasted_join      (tcgen05 kernel, or the bit-exact CUDA-core kernel)
-    -> fasted_sort_pairs (canonical (i, j) order on the device)
+    -> fasted_join       (tcgen05 kernel, or the bit-exact CUDA-core kernel)
+                          16-byte pair records, unordered
+    -> fasted_sort_pairs (canonical (i, j) order, SoA, on the device)
     -> D2H of (i, j, dist_sq)
 
 Concatenating the devices' results in device order is globally sorted.
@@ -15,7 +16,6 @@ Concatenating the devices' results in device order is globally sorted.
 
 from __future__ import annotations
 
-import ctypes
 import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
@@ -26,7 +26,9 @@ import numpy as np
 from . import _lib
 from .errors import ArgumentError
 
-BLOCK = 128  # row-block granularity of the kernels and of the partitioner
+BLOCK = 128          # row-block granularity of the kernels and of the partitioner
+RECORD_CHUNK = 256   # FASTED_RECORD_CHUNK in include/fasted.h
+RECORD_BYTES = 16    # {i, j, dist_sq, 0}
 
 
 @dataclass
@@ -41,13 +43,15 @@ class DeviceData:
 
 @dataclass
 class DeviceResult:
-    i: "object"          # torch.uint32-as-int32 [count] (sorted)
+    i: "object"          # torch.int32 [count], canonical order (None if unsorted)
     j: "object"
     d: "object"
     count: int
     kernel_ms: float     # CUDA-event time of the join launch(es)
     sort_ms: float
     reruns: int
+    slots: int           # record slots the kernel used (>= count; unused have i == 0)
+    records: "object" = None   # torch.int32 [slots, 4] raw records (kept when unsorted)
 
 
 def partition_rows(n_dev: int, parts: int) -> list:
@@ -56,6 +60,15 @@ def partition_rows(n_dev: int, parts: int) -> list:
         raise ArgumentError("need at least one device")
     R = n_dev // BLOCK
     return [((R * g // parts) * BLOCK, (R * (g + 1) // parts) * BLOCK) for g in range(parts)]
+
+
+def hole_slack(device: int) -> int:
+    """Upper bound on unused record slots: every warp may leave one partly
+    filled chunk (64 warps per SM is the hardware maximum)."""
+    import torch
+
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    return sms * 64 * RECORD_CHUNK
 
 
 def upload(hd, device: int) -> DeviceData:
@@ -90,32 +103,39 @@ _count_memo: dict = {}
 _memo_lock = threading.Lock()
 
 
+def join_raw(dd: DeviceData, eps_sq: float, flags: int, rows, cols, records, capacity: int,
+             count, stream) -> None:
+    """One fasted_join launch (results stay on the device)."""
+    st = _lib.load().fasted_join(dd.values.data_ptr(), dd.norms.data_ptr(), dd.n_logical,
+                                 dd.n_dev, dd.d_pad, rows[0], rows[1], cols[0], cols[1],
+                                 float(eps_sq), flags,
+                                 records.data_ptr() if records is not None else None,
+                                 capacity, count.data_ptr(), stream)
+    _lib.check(st, "fasted_join")
+
+
 def _estimate_capacity(dd: DeviceData, eps_sq: float, rows, cols, flags: int, stream) -> int:
     """Count-only join on a few evenly spaced row blocks -> capacity guess."""
     import torch
 
-    L = _lib.load()
     r0, r1 = rows
     nblk = (r1 - r0) // BLOCK
     samples = min(nblk, 8)
     if samples == 0:
         return 0
-    cnt = torch.zeros(1, dtype=torch.int64, device=f"cuda:{dd.device}")
+    cnt = torch.zeros(2, dtype=torch.int64, device=f"cuda:{dd.device}")
     tot = 0
     for s in range(samples):
         b = r0 + (nblk * s // samples) * BLOCK
-        _lib.check(L.fasted_join(dd.values.data_ptr(), dd.norms.data_ptr(), dd.n_logical,
-                                 dd.n_dev, dd.d_pad, b, b + BLOCK, cols[0], cols[1],
-                                 float(eps_sq), flags | _lib.JOIN_COUNT, None, None, None, 0,
-                                 cnt.data_ptr(), stream), "fasted_join(count sample)")
-        tot += int(cnt.item())
-    est = tot * nblk / samples
-    return int(est * 1.25) + 65536
+        join_raw(dd, eps_sq, flags | _lib.JOIN_COUNT, (b, b + BLOCK), cols, None, 0, cnt, stream)
+        tot += int(cnt[0].item())
+    return int(tot * nblk / samples * 1.25) + 65536
 
 
 def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool = False,
                 capacity: int | None = None, sort: bool = True) -> DeviceResult:
-    """Run the join for rows x cols on dd.device; results stay on the device."""
+    """Run the join for rows x cols on dd.device; results stay on the device.
+    With sort=False the raw 16-byte records are returned (res.records)."""
     import torch
 
     L = _lib.load()
@@ -128,39 +148,41 @@ def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool
         sp = stream.cuda_stream
         key = (dd.n_dev, dd.d_pad, dd.n_logical, float(eps_sq), rows, cols, flags,
                dd.values.data_ptr())
+        slack = hole_slack(dd.device)
         if capacity is None:
             with _memo_lock:
                 capacity = _count_memo.get(key)
             if capacity is None:
                 capacity = _estimate_capacity(dd, eps_sq, rows, cols, flags, sp)
-        cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+            capacity += slack
+        cnt = torch.zeros(2, dtype=torch.int64, device=dev)
         reruns = 0
         kernel_ms = 0.0
         while True:
             cap = max(int(capacity), 1)
-            oi = torch.empty(cap, dtype=torch.int32, device=dev)
-            oj = torch.empty(cap, dtype=torch.int32, device=dev)
-            od = torch.empty(cap, dtype=torch.float32, device=dev)
+            rec = torch.empty((cap, 4), dtype=torch.int32, device=dev)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            st = L.fasted_join(dd.values.data_ptr(), dd.norms.data_ptr(), dd.n_logical, dd.n_dev,
-                               dd.d_pad, rows[0], rows[1], cols[0], cols[1], float(eps_sq), flags,
-                               oi.data_ptr(), oj.data_ptr(), od.data_ptr(), cap, cnt.data_ptr(),
-                               sp)
+            join_raw(dd, eps_sq, flags, rows, cols, rec, cap, cnt, sp)
             e1.record(stream)
-            _lib.check(st, "fasted_join")
-            count = int(cnt.item())
+            count, chunks = (int(v) for v in cnt.tolist())
+            slots = chunks * RECORD_CHUNK
             kernel_ms += e0.elapsed_time(e1)
-            if count <= cap:
+            if slots <= cap:
                 break
-            capacity = count
+            capacity = count + slack
             reruns += 1
         with _memo_lock:
             _count_memo[key] = count
-        oi, oj, od = oi[:count], oj[:count], od[:count]
+        rec = rec[:slots]
+        if not sort:
+            return DeviceResult(None, None, None, count, kernel_ms, 0.0, reruns, slots, rec)
+        oi = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
+        oj = torch.empty_like(oi)
+        od = torch.empty(max(count, 1), dtype=torch.float32, device=dev)
         sort_ms = 0.0
-        if sort and count:
+        if count:
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             ws_bytes = L.fasted_sort_workspace_bytes(rows[1] - rows[0], dd.n_dev)
@@ -168,21 +190,29 @@ def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool
             tj = torch.empty(count, dtype=torch.int32, device=dev)
             td = torch.empty(count, dtype=torch.float32, device=dev)
             s0.record(stream)
-            _lib.check(L.fasted_sort_pairs(oi.data_ptr(), oj.data_ptr(), od.data_ptr(), count,
-                                           rows[0], rows[1], dd.n_dev, None, tj.data_ptr(),
-                                           td.data_ptr(), ws.data_ptr(), ws_bytes, sp),
+            _lib.check(L.fasted_sort_pairs(rec.data_ptr(), slots, rows[0], rows[1], dd.n_dev,
+                                           oi.data_ptr(), oj.data_ptr(), od.data_ptr(),
+                                           tj.data_ptr(), td.data_ptr(), ws.data_ptr(), ws_bytes,
+                                           sp),
                        "fasted_sort_pairs")
             s1.record(stream)
             s1.synchronize()
             sort_ms = s0.elapsed_time(s1)
             del ws, tj, td
-    return DeviceResult(oi, oj, od, count, kernel_ms, sort_ms, reruns)
+        del rec
+    return DeviceResult(oi[:count], oj[:count], od[:count], count, kernel_ms, sort_ms, reruns,
+                        slots)
 
 
 def to_host(res: DeviceResult):
     """D2H into pinned buffers; returns numpy (i uint32, j uint32, d float32)."""
     import torch
 
+    if res.records is not None:          # unsorted raw records: drop unused slots
+        raw = res.records.cpu().numpy()
+        keep = raw[:, 0] != 0
+        return (raw[keep, 0].view(np.uint32).copy(), raw[keep, 1].view(np.uint32).copy(),
+                raw[keep, 2].view(np.float32).copy())
     n = res.count
     hi = torch.empty(n, dtype=torch.int32, pin_memory=True)
     hj = torch.empty(n, dtype=torch.int32, pin_memory=True)

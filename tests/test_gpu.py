@@ -230,13 +230,26 @@ def test_capacity_rerun_and_count_only():
     assert small.reruns >= 1 and small.count == full.count
     a, b = engine.to_host(full), engine.to_host(small)
     assert all(np.array_equal(x, y) for x, y in zip(a, b))
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda:0")
-    L = _lib.load()
-    _lib.check(L.fasted_join(dd.values.data_ptr(), dd.norms.data_ptr(), dd.n_logical, dd.n_dev,
-                             dd.d_pad, 0, dd.n_dev, 0, dd.n_dev, es, _lib.JOIN_COUNT, None,
-                             None, None, 0, cnt.data_ptr(),
-                             torch.cuda.current_stream().cuda_stream), "count")
-    assert int(cnt.item()) == full.count
+    cnt = torch.zeros(2, dtype=torch.int64, device="cuda:0")
+    engine.join_raw(dd, es, _lib.JOIN_COUNT, (0, dd.n_dev), (0, dd.n_dev), None, 0, cnt,
+                    torch.cuda.current_stream().cuda_stream)
+    assert int(cnt[0].item()) == full.count
+    # raw (unsorted) records hold exactly the sorted set, unused slots marked i == 0
+    raw = engine.join_device(dd, es, sort=False)
+    ri, rj, rd = engine.to_host(raw)
+    order = np.lexsort((rj, ri))
+    assert np.array_equal(ri[order], a[0]) and np.array_equal(rj[order], a[1])
+    assert raw.slots % 256 == 0 and raw.slots >= raw.count
+
+
+def test_exact_kernel_matches_oracle_at_size(oracle):
+    """Bit parity of the exact kernel over a ragged multi-tile problem."""
+    x = F.synthetic_rows(10000, 77, 5, 0, 3001)
+    hd = F.to_half(F.Dataset(x))
+    rs = F.self_join(hd, 2.9, mode="exact")
+    oi, oj, od = oracle.join(hd.values, hd.norms, 3001, 2.9)
+    assert np.array_equal(rs.i, oi) and np.array_equal(rs.j, oj)
+    assert np.array_equal(rs.dist_sq.view(np.uint32), od.view(np.uint32))
 
 
 def test_long_rows_sort_path():
@@ -278,3 +291,33 @@ def test_c3_full_size_tc_vs_exact(oracle):
         assert np.array_equal(oi, ref.i[sel]) and np.array_equal(oj, ref.j[sel])
         assert np.array_equal(od.view(np.uint32), ref.dist_sq[sel].view(np.uint32))
     assert es > 0
+
+
+@pytest.mark.parametrize("n_rows,maxc", [(5000, 150), (20000, 100), (3000, 2000)])
+def test_sort_pairs_random_records(n_rows, maxc):
+    """fasted_sort_pairs on shuffled records with unused slots (i == 0),
+    short rows (warp rank path) and long rows (> 1024: bitmap path)."""
+    rng = np.random.default_rng(n_rows)
+    counts = rng.integers(0, maxc, n_rows)
+    i = np.repeat(np.arange(1, n_rows + 1), counts).astype(np.int32)
+    n_cols = n_rows * 2
+    j = np.concatenate([rng.choice(n_cols, c, replace=False) + 1 for c in counts]).astype(np.int32)
+    d = rng.random(len(i)).astype(np.float32)
+    rec = np.zeros((len(i) + 777, 4), np.int32)
+    slots = rng.permutation(len(rec))[:len(i)]
+    rec[slots, 0], rec[slots, 1], rec[slots, 2] = i, j, d.view(np.int32)
+    L = _lib.load()
+    trec = torch.from_numpy(rec).cuda()
+    oi, oj = torch.empty(len(i), dtype=torch.int32, device="cuda"), torch.empty(len(i), dtype=torch.int32, device="cuda")
+    od, tj = torch.empty(len(i), dtype=torch.float32, device="cuda"), torch.empty(len(i), dtype=torch.int32, device="cuda")
+    td = torch.empty(len(i), dtype=torch.float32, device="cuda")
+    wsb = L.fasted_sort_workspace_bytes(n_rows, n_cols)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(L.fasted_sort_pairs(trec.data_ptr(), len(rec), 0, n_rows, n_cols, oi.data_ptr(),
+                                   oj.data_ptr(), od.data_ptr(), tj.data_ptr(), td.data_ptr(),
+                                   ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream),
+               "sort")
+    order = np.lexsort((j, i))
+    assert np.array_equal(oi.cpu().numpy(), i[order])
+    assert np.array_equal(oj.cpu().numpy(), j[order])
+    assert np.array_equal(od.cpu().numpy(), d[order])

@@ -39,7 +39,7 @@ def test_library_host_calls_without_gpu():
     assert L.fasted_strerror(3) == b"value out of FP16 range"
     assert L.fasted_sort_workspace_bytes(1000, 1000) > 0
     # argument validation happens before any device work
-    assert L.fasted_join(None, None, 1, 128, 16, 0, 128, 0, 128, 1.0, 0, None, None, None, 0,
+    assert L.fasted_join(None, None, 1, 128, 16, 0, 128, 0, 128, 1.0, 0, None, 0,
                          None, None) == _lib.ERR_ARGUMENT
     assert L.fasted_quantize(None, 1, 1, None, 1, 8, None, None, None) == _lib.ERR_ARGUMENT
 
