@@ -60,7 +60,8 @@ enum {
     FASTED_JOIN_DIAG_NOEPI = 256,    /* tcgen05 kernel: skip the epilogue entirely     */
     FASTED_JOIN_DIAG_NOMMA = 512,    /* tcgen05 kernel: skip the MMAs (TMA + epilogue) */
     FASTED_JOIN_DIAG_LOADONLY = 1024, /* epilogue: TMEM loads only, no math           */
-    FASTED_JOIN_DIAG_NOSLOW = 2048   /* epilogue: sign test only, never write         */
+    FASTED_JOIN_DIAG_NOSLOW = 2048,  /* epilogue: sign test only, never write         */
+    FASTED_JOIN_DIAG_MASKOR = 4096   /* epilogue: lane masks + one REDUX.OR          */
 };
 
 int fasted_abi_version(void);

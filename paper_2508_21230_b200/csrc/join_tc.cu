@@ -1,17 +1,27 @@
 // Kernel 2 (the product path): fused tcgen05 epsilon join for sm_100a.
 //
-// Per CTA tile (128 points x 256 points), everything stays on chip:
-//   TMA (SWIZZLE_128B) -> 4-stage smem ring -> tcgen05.mma kind::f16
-//   (M=128, N=256, K=16) accumulating a_ij = x_i . x_j in TMEM, then ONE
-//   extra tcgen05.mma kind::tf32 step (K=8) that adds
+// Per tile, everything stays on chip:
+//   TMA (SWIZZLE_128B) -> smem ring -> tcgen05.mma kind::f16 (K=16)
+//   accumulating a_ij = x_i . x_j in TMEM, then ONE extra tcgen05.mma
+//   kind::tf32 step (K=8) that adds
 //       sigma_i + rho_j = -s_i/2 + (-s_j/2 + eps^2/2)
 //   from two tiny per-point "augment" rows (norms split into 3 exact tf32
 //   parts, prepared per call by aug_prepare_kernel).  The accumulator then
 //   holds D_ij = (eps^2 - d2_ij) / 2, so the epilogue's common path is a
-//   sign test: d2 <= eps^2  <=>  D >= 0.  Epilogue warps AND-reduce the
-//   sign bits of 32 TMEM columns per tcgen05.ld (16 LOP3 per 32 pairs); only
-//   a chunk holding a hit (or the diagonal) takes the per-column ballot path
-//   that writes {i, j, d2 = eps^2 - 2D} records (PairWriter).
+//   sign test: d2 <= eps^2  <=>  D >= 0.  Epilogue warps drain their whole
+//   TMEM slice with back-to-back tcgen05.ld and one wait, release the
+//   accumulator to the MMA warp, then AND-reduce the sign bits (16 LOP3 per
+//   32 pairs); only a chunk holding a hit (or the diagonal) finds its
+//   candidate columns with REDUX and writes {i, j, d2 = eps^2 - 2D} records
+//   (PairWriter, one atomic per 256 records per warp).
+//
+// Two variants of the same kernel (template CG):
+//   CG = 2 (default): CTA pair (cluster of 2, tcgen05 cta_group::2).  A
+//          256 x 256 tile per pair; each CTA stages its 128 rows of A and its
+//          128-row half of B, the leader CTA issues M=256 N=256 MMAs that read
+//          both CTAs' shared memory.  Per SM this halves the B-operand shared
+//          memory reads and the L2->SM traffic of the 1-CTA form.
+//   CG = 1: one CTA, 128 x 256 tile (kept for A/B measurements).
 //
 // The distance matrix never reaches HBM.  Replaces the reference's tile
 // sweep (tiling.py:307-344): compute_block_tile (tiling.py:199-285),
@@ -22,18 +32,18 @@
 // around eps^2 (tests/test_gpu.py).  Self pairs (i == j) are forced to
 // distance 0, which is exactly what the reference produces.
 //
-// Persistent CTAs (one per SM, 384 threads):
+// Warp roles (320 threads -> up to 200 registers per thread, enough for a
+// warp's 32 x 128 accumulator slice):
 //   warp 0      : TMEM allocator / deallocator, then TMA producer (one lane)
-//   warp 1      : MMA issuer (one lane)
+//   warp 1      : MMA issuer (one lane; leader CTA only for CG = 2)
 //   warps 2..9  : epilogue; warp w reads TMEM lanes 32*(w%4).. and column
 //                 half (w-2)/4 of the 256-column accumulator.
-// (320 threads leave 200 registers per thread: the epilogue holds a warp's
-// whole 32 x 128 accumulator slice in registers.)
 // TMEM: 2 accumulators x 256 columns (double buffered across tiles).
-// Tiles walk a grouped raster: GROUP row blocks sweep every column tile
+// Tiles walk a grouped raster: GROUP row tiles sweep every column tile
 // together, so each 256-row B panel is read from HBM once per group and the
 // group's A panels stay L2 resident.
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "join_common.cuh"
@@ -41,32 +51,36 @@
 namespace fasted {
 namespace tc {
 
-constexpr int BM = 128;
-constexpr int BN = 256;
-constexpr int BK = 64;   // one 128-byte swizzle atom of FP16
-constexpr int UK = 16;   // K of one kind::f16 tcgen05.mma
-constexpr int AUG_K = 8; // K of one kind::tf32 tcgen05.mma: one 32-byte row
-constexpr int STAGES = 4;
+constexpr int BM = 128;   // rows per CTA (TMEM lanes)
+constexpr int BN = 256;   // columns per tile (TMEM columns per accumulator)
+constexpr int BK = 64;    // one 128-byte swizzle atom of FP16
+constexpr int UK = 16;    // K of one kind::f16 tcgen05.mma
+constexpr int AUG_K = 8;  // K of one kind::tf32 tcgen05.mma: one 32-byte row
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int B_BYTES = BN * BK * 2;
-constexpr int AUG_A_BYTES = BM * AUG_K * 4;
-constexpr int AUG_B_BYTES = BN * AUG_K * 4;
+constexpr int B_HALF_BYTES = 128 * BK * 2;
+constexpr int AUG_ROW_BYTES = AUG_K * 4;
 constexpr int NUM_EPI_WARPS = 8;
 constexpr int FIRST_EPI_WARP = 2;
 constexpr int THREADS = (FIRST_EPI_WARP + NUM_EPI_WARPS) * 32;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int BAR_BYTES = 256;
-constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + BAR_BYTES + 1024;
-constexpr int GROUP = 16;
 
-// Instruction descriptors: D=F32 (bits 4-5 = 1); A/B format at bits 7-9 /
-// 10-12 (F16 = 0, TF32 = 2); both K-major; N>>3 at 17-22; M>>4 at 24-28.
-constexpr uint32_t IDESC_F16 =
-    (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
-constexpr uint32_t IDESC_TF32 = IDESC_F16 | (2u << 7) | (2u << 10);
+template <int CG>
+struct Cfg {
+    static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of B
+    static constexpr int STAGES = CG == 2 ? 6 : 4;
+    static constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + BAR_BYTES + 1024;
+    static constexpr int TILE_M = BM * CG;                // rows per tile
+    // Instruction descriptors: D=F32 (bits 4-5 = 1); A/B format at bits
+    // 7-9 / 10-12 (F16 = 0, TF32 = 2); both K-major; N>>3 at 17-22; M>>4 at
+    // 24-28 (M = 256 for the CTA pair).
+    static constexpr uint32_t IDESC_F16 =
+        (1u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(TILE_M >> 4) << 24);
+    static constexpr uint32_t IDESC_TF32 = IDESC_F16 | (2u << 7) | (2u << 10);
+};
 
 struct Sched {
-    int row_blocks;
+    int row_tiles;
     int col_tiles;
     int group;
     int nkb;
@@ -77,18 +91,31 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\t"
+                 "barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
 
+// try_wait with a suspend-time hint (ns): a waiting warp sleeps in hardware
+// until the phase completes or the hint expires, instead of re-polling.
 __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}"
         : "=r"(ok)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "r"(1000000u)
         : "memory");
     return ok != 0;
 }
@@ -106,7 +133,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     const uint64_t t0 = global_timer();
     uint32_t spins = 0;
     while (!mbar_try_wait(bar, parity)) {
-        if (++spins == 2048u) {
+        if (++spins == 16u) {
             spins = 0;
             if (global_timer() - t0 > 20000000000ull) __trap();
         }
@@ -117,18 +144,40 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// Arrive on the barrier at the same offset in CTA `rank` of the cluster.
+// Relaxed: the only ordering needed (TMEM reads before the MMA reuses the
+// accumulator) comes from tcgen05.fence::before_thread_sync; a release
+// arrive would also wait for this thread's outstanding global stores
+// (measured: an ERRBAR per tile on the critical path).
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+                 : "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
 }
 
+template <int CG>
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
                                             int c0, int c1) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
-        : "memory");
+    if constexpr (CG == 1) {
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1)
+            : "memory");
+    } else {
+        // both CTAs signal the leader's barrier: clear the peer bit
+        asm volatile(
+            "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
+            "bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+            "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+            : "memory");
+    }
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -150,30 +199,57 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t sbo_bytes
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) { return smem_desc(saddr, 1024, 2); }
 __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) { return smem_desc(saddr, 256, 6); }
 
-template <uint32_t IDESC>
-__device__ __forceinline__ void mma_issue(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                          uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accumulate)
-        : "memory");
+template <int CG>
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t accumulate) {
+    if constexpr (CG == 1)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(Cfg<CG>::IDESC_F16), "r"(accumulate)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(Cfg<CG>::IDESC_F16), "r"(accumulate)
+            : "memory");
 }
 
+template <int CG>
 __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(IDESC_TF32), "r"(1u)
-        : "memory");
+    if constexpr (CG == 1)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(Cfg<CG>::IDESC_TF32), "r"(1u)
+            : "memory");
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(adesc), "l"(bdesc), "r"(Cfg<CG>::IDESC_TF32), "r"(1u)
+            : "memory");
 }
 
+// Completion of all prior MMAs -> arrive on `bar` (in both CTAs for CG=2).
+template <int CG>
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-        : "memory");
+    if constexpr (CG == 1)
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                bar)
+            : "memory");
+    else
+        asm volatile(
+            "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster."
+            "b64 [%0], %1;" ::"r"(bar),
+            "h"((uint16_t)0x3)
+            : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -204,14 +280,14 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
                  : "memory");
 }
 
-__device__ __forceinline__ void tile_coords(const Sched& s, int64_t t, int& rb, int& ct) {
+__device__ __forceinline__ void tile_coords(const Sched& s, int64_t t, int& rt, int& ct) {
     const int64_t per_group = (int64_t)s.group * s.col_tiles;
     const int64_t g = t / per_group;
     const int64_t r = t - g * per_group;
-    const int64_t left = (int64_t)s.row_blocks - g * s.group;
+    const int64_t left = (int64_t)s.row_tiles - g * s.group;
     const int rows_in = (int)(left < s.group ? left : s.group);
     ct = (int)(r / rows_in);
-    rb = (int)(g * s.group + r % rows_in);
+    rt = (int)(g * s.group + r % rows_in);
 }
 
 // r[e] for a warp-uniform runtime e without local memory: a 5-level
@@ -247,13 +323,20 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
         const uint32_t b = __ballot_sync(0xffffffffu, self);
         if (b) writer_append(wr, a, b, self, (uint32_t)(i + 1), (uint32_t)(i + 1), 0.0f);
     }
-    // Candidate columns: a column holds a hit iff the AND over the warp of
-    // its D words has the sign bit clear -- 32 independent REDUX.AND whose
-    // results live in uniform registers.  Then visit only those columns.
+    // Candidate columns: a column holds a hit iff some lane's D word has the
+    // sign bit clear.  Either 32 independent REDUX.AND (uniform datapath) or
+    // a per-lane mask OR-reduced once (FASTED_JOIN_DIAG_MASKOR).
     uint32_t cm = 0;
+    if (a.diag_flags & FASTED_JOIN_DIAG_MASKOR) {
+        uint32_t lm = 0;
 #pragma unroll
-    for (int e = 0; e < 32; e++)
-        cm |= ((~__reduce_and_sync(0xffffffffu, r[e]) >> 31) & 1u) << e;
+        for (int e = 0; e < 32; e++) lm |= ((~r[e]) >> 31) << e;
+        cm = __reduce_or_sync(0xffffffffu, lm);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 32; e++)
+            cm |= ((~__reduce_and_sync(0xffffffffu, r[e]) >> 31) & 1u) << e;
+    }
     while (cm) {
         const uint32_t e = __ffs(cm) - 1;
         cm &= cm - 1;
@@ -267,17 +350,20 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
     }
 }
 
+template <int CG>
 __global__ void __launch_bounds__(THREADS, 1)
 join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                const __grid_constant__ CUtensorMap tmap_aug_a,
                const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
                const Sched sch) {
+    using C = Cfg<CG>;
+    constexpr int STAGES = C::STAGES;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     const uint32_t sA = base;
     const uint32_t sB = base + STAGES * A_BYTES;
-    const uint32_t bars = sB + STAGES * B_BYTES;
+    const uint32_t bars = sB + STAGES * C::B_BYTES;
     auto full_bar = [&](int s) { return bars + 8u * s; };
     auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
     auto tfull_bar = [&](int b) { return bars + 8u * (2 * STAGES + b); };
@@ -288,15 +374,23 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    const int64_t tile_id0 = CG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+    const int64_t tile_step = CG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
+            // CG = 2: only the leader's full barrier is used; the leader's
+            // expect_tx covers both CTAs' bytes and the peer's TMA completes
+            // its bytes there (it cannot run ahead a phase: it first waits
+            // for this stage's empty barrier, i.e. the previous phase done).
             mbar_init(full_bar(s), 1);
             mbar_init(empty_bar(s), 1);
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(tfull_bar(b), 1);
-            mbar_init(tempty_bar(b), NUM_EPI_WARPS);
+            mbar_init(tempty_bar(b), NUM_EPI_WARPS * CG);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x))
@@ -307,14 +401,22 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                      : "memory");
     }
     if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                         slot),
-                     "r"(TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        if constexpr (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             slot),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             slot),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        }
     }
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *slot_ptr;
 
@@ -323,30 +425,59 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         if (lane == 0) {
             int s = 0;
             uint32_t ph = 0;
-            for (int64_t t = blockIdx.x; t < sch.total; t += gridDim.x) {
-                int rb, ct;
-                tile_coords(sch, t, rb, ct);
-                const int row0 = (int)(a.row_begin + (int64_t)rb * BM);
-                const int col0 = (int)(a.col_begin + (int64_t)ct * BN);
-                const bool second = (int64_t)col0 + 128 < a.col_end;
+            for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
+                int rt, ct;
+                tile_coords(sch, t, rt, ct);
+                const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M;
+                const int64_t col0 = a.col_begin + (int64_t)ct * BN;
+                // which 128-row halves exist (a half past the range end is skipped:
+                // its rows/columns are masked in the epilogue)
+                const bool a_hi = row0 + 128 < a.row_end;
+                const bool b_hi = col0 + 128 < a.col_end;
+                const int my_a = (int)(row0 + 128 * rank);
+                const bool a_mine = rank == 0 || a_hi;
                 for (int kb = 0; kb <= sch.nkb; kb++) {
                     mbar_wait(empty_bar(s), ph ^ 1u);
+                    const uint32_t fb = full_bar(s);
                     if (kb < sch.nkb) {
-                        mbar_expect_tx(full_bar(s), A_BYTES + (second ? B_BYTES : B_BYTES / 2));
                         const int kx = kb * BK;
-                        tma_load_2d(sA + s * A_BYTES, &tmap_x, full_bar(s), kx, row0);
-                        tma_load_2d(sB + s * B_BYTES, &tmap_x, full_bar(s), kx, col0);
-                        if (second)
-                            tma_load_2d(sB + s * B_BYTES + B_BYTES / 2, &tmap_x, full_bar(s), kx,
-                                        col0 + 128);
+                        if constexpr (CG == 1) {
+                            mbar_expect_tx(fb, A_BYTES + (b_hi ? 2 : 1) * B_HALF_BYTES);
+                            tma_load_2d<1>(sA + s * A_BYTES, &tmap_x, fb, kx, (int)row0);
+                            tma_load_2d<1>(sB + s * C::B_BYTES, &tmap_x, fb, kx, (int)col0);
+                            if (b_hi)
+                                tma_load_2d<1>(sB + s * C::B_BYTES + B_HALF_BYTES, &tmap_x, fb, kx,
+                                               (int)col0 + 128);
+                        } else {
+                            if (leader)
+                                mbar_expect_tx(fb, (a_hi ? 2 : 1) * A_BYTES +
+                                                       (b_hi ? 2 : 1) * B_HALF_BYTES);
+                            if (a_mine)
+                                tma_load_2d<2>(sA + s * A_BYTES, &tmap_x, fb, kx, my_a);
+                            if (rank == 0 || b_hi)
+                                tma_load_2d<2>(sB + s * C::B_BYTES, &tmap_x, fb, kx,
+                                               (int)(col0 + 128 * rank));
+                        }
                     } else {
-                        mbar_expect_tx(full_bar(s),
-                                       AUG_A_BYTES + (second ? AUG_B_BYTES : AUG_B_BYTES / 2));
-                        tma_load_2d(sA + s * A_BYTES, &tmap_aug_a, full_bar(s), 0, row0);
-                        tma_load_2d(sB + s * B_BYTES, &tmap_aug_b, full_bar(s), 0, col0);
-                        if (second)
-                            tma_load_2d(sB + s * B_BYTES + AUG_B_BYTES / 2, &tmap_aug_b,
-                                        full_bar(s), 0, col0 + 128);
+                        constexpr int AUG_A = BM * AUG_ROW_BYTES;
+                        constexpr int AUG_B_HALF = 128 * AUG_ROW_BYTES;
+                        if constexpr (CG == 1) {
+                            mbar_expect_tx(fb, AUG_A + (b_hi ? 2 : 1) * AUG_B_HALF);
+                            tma_load_2d<1>(sA + s * A_BYTES, &tmap_aug_a, fb, 0, (int)row0);
+                            tma_load_2d<1>(sB + s * C::B_BYTES, &tmap_aug_b, fb, 0, (int)col0);
+                            if (b_hi)
+                                tma_load_2d<1>(sB + s * C::B_BYTES + AUG_B_HALF, &tmap_aug_b, fb,
+                                               0, (int)col0 + 128);
+                        } else {
+                            if (leader)
+                                mbar_expect_tx(fb, (a_hi ? 2 : 1) * AUG_A +
+                                                       (b_hi ? 2 : 1) * AUG_B_HALF);
+                            if (a_mine)
+                                tma_load_2d<2>(sA + s * A_BYTES, &tmap_aug_a, fb, 0, my_a);
+                            if (rank == 0 || b_hi)
+                                tma_load_2d<2>(sB + s * C::B_BYTES, &tmap_aug_b, fb, 0,
+                                               (int)(col0 + 128 * rank));
+                        }
                     }
                     if (++s == STAGES) {
                         s = 0;
@@ -357,13 +488,13 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         }
         __syncwarp();
     } else if (warp == 1) {
-        // ---------------- MMA issuer
-        if (lane == 0) {
+        // ---------------- MMA issuer (the leader CTA of a pair)
+        if (lane == 0 && leader) {
             const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
             int s = 0;
             uint32_t ph = 0;
             int lt = 0;
-            for (int64_t t = blockIdx.x; t < sch.total; t += gridDim.x, ++lt) {
+            for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
                 const int buf = lt & 1;
                 const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
                 mbar_wait(tempty_bar(buf), aph ^ 1u);
@@ -375,28 +506,28 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     if (!no_mma) {
                         if (kb < sch.nkb) {
                             const uint64_t ad = sw128_desc(sA + s * A_BYTES);
-                            const uint64_t bd = sw128_desc(sB + s * B_BYTES);
+                            const uint64_t bd = sw128_desc(sB + s * C::B_BYTES);
 #pragma unroll
                             for (int kk = 0; kk < BK / UK; kk++) {
                                 const uint64_t koff = (uint64_t)((kk * UK * 2) >> 4);
-                                mma_issue<IDESC_F16>(dtm, ad + koff, bd + koff,
-                                                     (kb | kk) != 0 ? 1u : 0u);
+                                mma_f16<CG>(dtm, ad + koff, bd + koff, (kb | kk) != 0 ? 1u : 0u);
                             }
                         } else {
-                            mma_tf32(dtm, sw32_desc(sA + s * A_BYTES), sw32_desc(sB + s * B_BYTES));
+                            mma_tf32<CG>(dtm, sw32_desc(sA + s * A_BYTES),
+                                         sw32_desc(sB + s * C::B_BYTES));
                         }
                     }
-                    mma_commit(empty_bar(s));
+                    mma_commit<CG>(empty_bar(s));
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1u;
                     }
                 }
-                mma_commit(tfull_bar(buf));
+                mma_commit<CG>(tfull_bar(buf));
             }
         }
         __syncwarp();
-    } else if (warp >= FIRST_EPI_WARP) {
+    } else {
         // ---------------- epilogue
         const int q = warp & 3;          // TMEM lane quarter this warp may access
         const int h = (warp - FIRST_EPI_WARP) >> 2;   // column half of the accumulator
@@ -404,20 +535,21 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         PairWriter wr;
         writer_init(wr);
         int lt = 0;
-        for (int64_t t = blockIdx.x; t < sch.total; t += gridDim.x, ++lt) {
-            int rb, ct;
-            tile_coords(sch, t, rb, ct);
-            const int64_t row0 = a.row_begin + (int64_t)rb * BM;
+        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
+            int rt, ct;
+            tile_coords(sch, t, rt, ct);
+            const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M + 128 * rank;
             const int64_t col0 = a.col_begin + (int64_t)ct * BN;
             const int64_t iw = row0 + q * 32;
             const int64_t i = iw + lane;
-            const bool row_ok = i < a.n_logical;
+            const bool row_ok = i < a.n_logical && i < a.row_end;
             const int buf = lt & 1;
             const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
-            // chunks of 32 columns inside [col0 + 128h, col_end)
+            // chunks of 32 columns inside [col0 + 128h, col_end); none if this
+            // CTA's rows lie past the range end
             const int64_t left = a.col_end - (col0 + h * 128);
             int nchunks = left <= 0 ? 0 : (left >= 128 ? 4 : (int)(left / 32));
-            if (a.diag_flags & FASTED_JOIN_DIAG_NOEPI) nchunks = 0;
+            if (row0 >= a.row_end || (a.diag_flags & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
             const uint32_t tcol = tmem_base + lane_base + (uint32_t)(buf * BN + h * 128);
             mbar_wait(tfull_bar(buf), aph);
             tc_fence_after();
@@ -439,7 +571,10 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(tempty_bar(buf));
+            if (lane == 0) {
+                if (CG == 1 || leader) mbar_arrive(tempty_bar(buf));
+                else mbar_arrive_remote(tempty_bar(buf), 0);
+            }
             const int64_t jb = col0 + h * 128;
             if (nchunks > 0) epi_chunk(a, wr, r0, jb, i, iw, row_ok);
             if (nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok);
@@ -450,12 +585,17 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
     }
 
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     if (warp == 0) {
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(TMEM_COLS)
-                     : "memory");
+        if constexpr (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS)
+                         : "memory");
     }
 }
 
@@ -528,6 +668,43 @@ static int encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base,
     return FASTED_OK;
 }
 
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+template <int CG>
+static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
+                                  const CUtensorMap& mb, const JoinArgs& a, const tc::Sched& sch,
+                                  cudaStream_t s) {
+    using namespace tc;
+    auto kern = join_tc_kernel<CG>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cfg<CG>::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int sms = sm_count_current();
+    const int64_t units = sms / CG;   // CTAs (or CTA pairs) resident at once
+    const int64_t work = sch.total < units ? sch.total : units;
+    if (work <= 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(work * CG));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = Cfg<CG>::SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, mx, ma, mb, a, sch);
+}
+
 int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     using namespace tc;
     if ((a.d_pad % 8) != 0 || (reinterpret_cast<uintptr_t>(X) & 15u) != 0) {
@@ -538,6 +715,14 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         set_error("join_tc: n_pad exceeds TMA int32 coordinates");
         return FASTED_ERR_ARGUMENT;
     }
+    // Variant choice (profiles/round1/tune_*.txt, 1M-point shapes on B200):
+    // the CTA pair reaches ~88% tensor-pipe utilisation per clock and wins
+    // where the join is not power bound (d <= 256: 733 vs 632 TFLOPS at
+    // 1M x 128); at d = 960 the chip sits at the 1 kW cap and the single-CTA
+    // form delivers more TFLOPS per joule (0.81 vs 0.79-1.05 pJ/flop, the
+    // pair being run-to-run unstable).  FASTED_CTA_GROUP=1|2 overrides.
+    const int cg_env = env_int("FASTED_CTA_GROUP", 0);
+    const int cg = cg_env == 1 ? 1 : cg_env == 2 ? 2 : (a.d_pad <= 256 ? 2 : 1);
     // per-call augment rows (eps-dependent), stream ordered
     float4* aug = nullptr;
     const size_t aug_bytes = (size_t)a.n_pad * 64;   // two [n_pad][8] FP32 arrays
@@ -556,35 +741,28 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     int st = encode_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, X, a.d_pad, a.n_pad, a.d_pad * 2, BK,
                        BM, CU_TENSOR_MAP_SWIZZLE_128B);
     if (st == FASTED_OK)
-        st = encode_2d(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, aug_a, AUG_K, a.n_pad, 32, AUG_K, BM,
-                       CU_TENSOR_MAP_SWIZZLE_32B);
+        st = encode_2d(&ma, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, aug_a, AUG_K, a.n_pad, AUG_ROW_BYTES,
+                       AUG_K, BM, CU_TENSOR_MAP_SWIZZLE_32B);
     if (st == FASTED_OK)
-        st = encode_2d(&mb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, aug_b, AUG_K, a.n_pad, 32, AUG_K, BM,
-                       CU_TENSOR_MAP_SWIZZLE_32B);
+        st = encode_2d(&mb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, aug_b, AUG_K, a.n_pad, AUG_ROW_BYTES,
+                       AUG_K, BM, CU_TENSOR_MAP_SWIZZLE_32B);
     if (st != FASTED_OK) {
         cudaFreeAsync(aug, s);
         return st;
     }
     Sched sch;
-    sch.row_blocks = (int)((a.row_end - a.row_begin) / BM);
+    const int tile_m = BM * cg;
+    sch.row_tiles = (int)((a.row_end - a.row_begin + tile_m - 1) / tile_m);
     sch.col_tiles = (int)((a.col_end - a.col_begin + BN - 1) / BN);
-    sch.group = GROUP;
+    // grouped raster: GROUP row tiles (default 8192 rows) sweep all columns
+    // (2048 rows measured best for the single-CTA form at 1M x 960: 0.82 vs
+    // 0.93 pJ/flop for 8192)
+    sch.group = env_int("FASTED_GROUP_ROWS", 2048) / tile_m;
+    if (sch.group < 1) sch.group = 1;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
-    sch.total = (int64_t)sch.row_blocks * sch.col_tiles;
-    const int sms = sm_count_current();
-    const int64_t grid = sch.total < sms ? sch.total : sms;
-    static bool attr_set = false;
-    if (!attr_set) {
-        e = cudaFuncSetAttribute(join_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 SMEM_BYTES);
-        if (e != cudaSuccess) {
-            cudaFreeAsync(aug, s);
-            return cuda_status(e, "cudaFuncSetAttribute(join_tc_kernel)");
-        }
-        attr_set = true;
-    }
-    if (grid > 0) join_tc_kernel<<<(unsigned)grid, THREADS, SMEM_BYTES, s>>>(mx, ma, mb, a, sch);
-    e = cudaGetLastError();
+    sch.total = (int64_t)sch.row_tiles * sch.col_tiles;
+    e = cg == 2 ? launch_variant<2>(mx, ma, mb, a, sch, s) : launch_variant<1>(mx, ma, mb, a, sch, s);
+    if (e == cudaSuccess) e = cudaGetLastError();
     cudaFreeAsync(aug, s);
     if (e != cudaSuccess) return cuda_status(e, "join_tc_kernel");
     return FASTED_OK;
