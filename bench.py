@@ -168,7 +168,9 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOPS",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "strong",
+        # the full workload on the CPU, extrapolated from the sampled rate
+        "ms_per_step": 2.0 * n * n * d / (v * 1e12) * 1e3, "higher_is_better": True,
+        "scaling": "strong",
         "vs_baseline": None, "dtype": "fp16 in / fp32 RZ accumulate", "data": "synthetic",
         "config": {"workload": f"{args.workload}: {name}", "n": n, "d": d, "epsilon": eps,
                    "seed": SEED},
@@ -190,6 +192,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-accuracy", action="store_true")
+    ap.add_argument("--accuracy-blocks", type=int, default=8)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -211,7 +215,8 @@ def main():
     # ---- data: every rank holds the full FP16 dataset
     ds = F.generate_synthetic(n, d, seed=SEED)
     hd = F.to_half(ds, pin_host=True)          # GPU quantise; device copy cached
-    del ds
+    if rank != 0 or args.no_accuracy:
+        del ds
     n_dev = -(-hd.n_padded // 128) * 128
     rows = engine.partition_rows(n_dev, world)[rank]
     dd = engine.upload(hd, device)
@@ -299,6 +304,22 @@ def main():
     e2e_s = statistics.median(e2e_times)
     h2d = hd.values.nbytes + hd.norms.nbytes
 
+    # ---- pair accuracy vs FP64 (Eq. 3) on sampled whole row blocks: the
+    # tcgen05 path and the reference arithmetic (exact kernel) side by side
+    acc = None
+    if rank == 0 and not args.no_accuracy:
+        from paper_2508_21230_b200 import accuracy
+
+        arows = accuracy.sample_row_blocks(n, blocks=args.accuracy_blocks, seed=0)
+        dd_a = engine.upload(hd, device)
+        acc = {"sample": f"{args.accuracy_blocks} random 128-row blocks ({len(arows)} points) "
+                         "x all columns; FP64 truth = fasted_fp64_rows (oracle.py order)"}
+        for label, exact in (("tcgen05", False), ("reference_arithmetic_exact_kernel", True)):
+            part = accuracy.join_row_blocks(dd_a, eps, arows, exact=exact)
+            acc[label] = accuracy.accuracy_vs_fp64(ds.values, part, eps, arows, device)
+        del dd_a, ds
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -334,6 +355,7 @@ def main():
             "e2e": {"value": flops / e2e_s / 1e12, "unit": "TFLOPS",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_s, "api": "paper_2508_21230_b200.self_join"},
+            "accuracy_vs_fp64": acc,
             "gpu_launches": args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

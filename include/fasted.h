@@ -130,6 +130,19 @@ int fasted_sort_pairs(const void* records, uint64_t slots, int64_t row_begin, in
                       uint32_t* tmp_j, float* tmp_d, void* workspace, size_t workspace_bytes,
                       void* stream);
 
+/*
+ * FP64 ground truth for `nq` sampled query rows (device int64 indices,
+ * 0-based) of the ORIGINAL FP32 dataset x [n, d]: every (q, j) with
+ * sqrt(sum_k (x_qk - x_jk)^2) <= epsilon, accumulated in FP64 in ascending
+ * k exactly as the reference's oracle (oracle.py:26-64, numpy order, no
+ * FMA).  Records are 16 bytes {uint32 q+1, uint32 j+1, float64 dist_sq},
+ * unordered; *count (device uint64, zeroed here) is the exact total.
+ * Used to report pair accuracy vs FP64 (the paper's Eq. 3) at scale.
+ */
+int fasted_fp64_rows(const float* x, int64_t n, int64_t d, const int64_t* qrows, int64_t nq,
+                     double epsilon, void* out_records, uint64_t capacity,
+                     unsigned long long* count, void* stream);
+
 /* Number of SMs and device name of the current device (for reports). */
 int fasted_device_info(int* sm_count, char* name, int name_len);
 

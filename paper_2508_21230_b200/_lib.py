@@ -24,7 +24,7 @@ JOIN_TC, JOIN_EXACT, JOIN_COUNT = 0, 1, 2
 EXPORTS = (
     "fasted_abi_version", "fasted_strerror", "fasted_last_error", "fasted_device_check",
     "fasted_device_info", "fasted_quantize", "fasted_norms", "fasted_join",
-    "fasted_sort_workspace_bytes", "fasted_sort_pairs",
+    "fasted_sort_workspace_bytes", "fasted_sort_pairs", "fasted_fp64_rows",
 )
 
 _lib = None
@@ -65,6 +65,8 @@ def load():
         L.fasted_sort_pairs.restype = ci
         L.fasted_sort_pairs.argtypes = [p, u64, i64, i64, i64, p, p, p, p, p, p,
                                         ctypes.c_size_t, p]
+        L.fasted_fp64_rows.restype = ci
+        L.fasted_fp64_rows.argtypes = [p, i64, i64, p, i64, ctypes.c_double, p, u64, p, p]
         if L.fasted_abi_version() != 1:
             raise DeviceError("libfasted ABI version mismatch")
         _lib = L
