@@ -126,6 +126,7 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     a.out = reinterpret_cast<uint4*>(out_records);
     a.capacity = count_only ? 0ull : (unsigned long long)capacity;
     a.count = count;
+    a.gram_diag = nullptr;
     const __half* X = reinterpret_cast<const __half*>(values16);
     return kind == FASTED_JOIN_EXACT ? launch_join_exact(X, a, s) : launch_join_tc(X, a, s);
 }

@@ -15,6 +15,7 @@ struct JoinArgs {
     uint4* out;                        // records {i, j, dist_sq bits, 0}
     unsigned long long capacity;       // record slots available in out
     unsigned long long* count;         // [0] exact pair total, [1] chunks taken
+    float* gram_diag;                  // diagonal pre-pass output (tcgen05 kernel), else null
 };
 
 // ((-2 a) + s_i) + s_j in FP32 round-to-nearest, clamped at 0

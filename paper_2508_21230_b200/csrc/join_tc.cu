@@ -85,6 +85,7 @@ struct Sched {
     int group;
     int nkb;
     int64_t total;
+    int diag;   // 1: Gram-diagonal pre-pass (tiles (r, r), no augment step)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -350,7 +351,7 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
     }
 }
 
-template <int CG>
+template <int CG, bool DIAG>
 __global__ void __launch_bounds__(THREADS, 1)
 join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                const __grid_constant__ CUtensorMap tmap_aug_a,
@@ -429,14 +430,14 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 int rt, ct;
                 tile_coords(sch, t, rt, ct);
                 const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M;
-                const int64_t col0 = a.col_begin + (int64_t)ct * BN;
+                const int64_t col0 = DIAG ? row0 : a.col_begin + (int64_t)ct * BN;
                 // which 128-row halves exist (a half past the range end is skipped:
                 // its rows/columns are masked in the epilogue)
                 const bool a_hi = row0 + 128 < a.row_end;
                 const bool b_hi = col0 + 128 < a.col_end;
                 const int my_a = (int)(row0 + 128 * rank);
                 const bool a_mine = rank == 0 || a_hi;
-                for (int kb = 0; kb <= sch.nkb; kb++) {
+                for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
                     mbar_wait(empty_bar(s), ph ^ 1u);
                     const uint32_t fb = full_bar(s);
                     if (kb < sch.nkb) {
@@ -500,7 +501,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 mbar_wait(tempty_bar(buf), aph ^ 1u);
                 tc_fence_after();
                 const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
-                for (int kb = 0; kb <= sch.nkb; kb++) {
+                for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
                     mbar_wait(full_bar(s), ph);
                     tc_fence_after();
                     if (!no_mma) {
@@ -545,6 +546,22 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const bool row_ok = i < a.n_logical && i < a.row_end;
             const int buf = lt & 1;
             const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
+            if constexpr (DIAG) {
+                // Gram-diagonal pre-pass (CG = 1, col0 = row0): lane i's own
+                // column i - row0 = 32 q + lane sits in chunk q of half 0.
+                mbar_wait(tfull_bar(buf), aph);
+                tc_fence_after();
+                uint32_t r0[32];
+                if (h == 0) {
+                    tmem_ld32(tmem_base + lane_base + (uint32_t)(buf * BN + q * 32), r0);
+                    tmem_ld_wait(r0);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty_bar(buf));
+                if (h == 0 && i < a.row_end) a.gram_diag[i] = __uint_as_float(pick32(r0, lane));
+                continue;
+            }
             // chunks of 32 columns inside [col0 + 128h, col_end); none if this
             // CTA's rows lie past the range end
             const int64_t left = a.col_end - (col0 + h * 128);
@@ -673,12 +690,12 @@ static int env_int(const char* name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 
-template <int CG>
+template <int CG, bool DIAG = false>
 static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
                                   const CUtensorMap& mb, const JoinArgs& a, const tc::Sched& sch,
                                   cudaStream_t s) {
     using namespace tc;
-    auto kern = join_tc_kernel<CG>;
+    auto kern = join_tc_kernel<CG, DIAG>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -723,20 +740,23 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     // pair being run-to-run unstable).  FASTED_CTA_GROUP=1|2 overrides.
     const int cg_env = env_int("FASTED_CTA_GROUP", 0);
     const int cg = cg_env == 1 ? 1 : cg_env == 2 ? 2 : (a.d_pad <= 256 ? 2 : 1);
-    // per-call augment rows (eps-dependent), stream ordered
+    // per-call scratch (stream ordered): augment rows (two [n_pad][8] FP32,
+    // eps-dependent) and the tensor-core Gram diagonal
     float4* aug = nullptr;
-    const size_t aug_bytes = (size_t)a.n_pad * 64;   // two [n_pad][8] FP32 arrays
+    const size_t aug_bytes = (size_t)a.n_pad * 64 + (size_t)a.n_pad * 4;
     cudaError_t e = cudaMallocAsync(&aug, aug_bytes, s);
     if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(augment rows)");
     float4* aug_a = aug;
     float4* aug_b = aug + 2 * a.n_pad;
-    aug_prepare_kernel<<<(unsigned)((a.n_pad + 255) / 256), 256, 0, s>>>(a.norms, a.n_pad,
-                                                                         a.eps_sq, aug_a, aug_b);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) {
-        cudaFreeAsync(aug, s);
-        return cuda_status(e, "aug_prepare_kernel");
-    }
+    float* gram = reinterpret_cast<float*>(aug + 4 * a.n_pad);
+    // Norms for the augment rows: by default the tensor core's own a_ii
+    // (Gram-diagonal pre-pass, ~1/(n/128) of the join's work), so the norm
+    // terms carry the same accumulation error as a_ij and cancel in
+    // d2 = a_ii + a_jj - 2 a_ij (the reference's own RZ norms paired with
+    // tensor-core a_ij bias d2 low by ~2e-3 relative at d = 960, measured
+    // as a 0.43% vs 0.14% Eq. 3 loss).  It also makes exact duplicates
+    // distance 0, as in the reference.  FASTED_TC_NORMS=0 uses the RZ norms.
+    const bool tc_norms = env_int("FASTED_TC_NORMS", 1) != 0;
     CUtensorMap mx, ma, mb;
     int st = encode_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, X, a.d_pad, a.n_pad, a.d_pad * 2, BK,
                        BM, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -750,7 +770,39 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         cudaFreeAsync(aug, s);
         return st;
     }
+    if (tc_norms) {
+        JoinArgs ad = a;
+        ad.row_begin = 0;
+        ad.row_end = a.n_pad;
+        ad.col_begin = 0;
+        ad.col_end = a.n_pad;
+        ad.count_only = 1;
+        ad.capacity = 0;
+        ad.diag_flags = 0;
+        ad.gram_diag = gram;
+        Sched sd;
+        sd.row_tiles = (int)(a.n_pad / BM);
+        sd.col_tiles = 1;
+        sd.group = 1;
+        sd.nkb = (int)((a.d_pad + BK - 1) / BK);
+        sd.total = sd.row_tiles;
+        sd.diag = 1;
+        e = launch_variant<1, true>(mx, ma, mb, ad, sd, s);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            cudaFreeAsync(aug, s);
+            return cuda_status(e, "join_tc_kernel (Gram diagonal)");
+        }
+    }
+    aug_prepare_kernel<<<(unsigned)((a.n_pad + 255) / 256), 256, 0, s>>>(
+        tc_norms ? gram : a.norms, a.n_pad, a.eps_sq, aug_a, aug_b);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFreeAsync(aug, s);
+        return cuda_status(e, "aug_prepare_kernel");
+    }
     Sched sch;
+    sch.diag = 0;
     const int tile_m = BM * cg;
     sch.row_tiles = (int)((a.row_end - a.row_begin + tile_m - 1) / tile_m);
     sch.col_tiles = (int)((a.col_end - a.col_begin + BN - 1) / BN);
