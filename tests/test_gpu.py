@@ -195,10 +195,11 @@ def test_duplicates_eps_zero(golden):
     rs = F.self_join(hd, 0.0, mode="exact")
     assert np.array_equal(rs.i, golden["dup_i"]) and np.array_equal(rs.j, golden["dup_j"])
     tc = F.self_join(hd, 0.0)
-    # diagonal always present; exact-duplicate pairs at eps = 0 are the
-    # documented zero-width-band exception
-    assert tc.index_pairs() <= rs.index_pairs()
-    assert {(k, k) for k in range(1, hd.n_logical + 1)} <= tc.index_pairs()
+    # the augment step uses the tensor core's own a_ii as norms, so an exact
+    # duplicate gives D = a - a/2 - a/2 = 0, i.e. distance 0, as in the
+    # reference (whose a_ij and s_i are the same RZ chain)
+    assert tc.index_pairs() == rs.index_pairs()
+    assert not tc.dist_sq.any()
 
 
 def test_c1_tc_vs_reference(golden_meta, oracle):
