@@ -21,7 +21,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _header_symbols():
     src = open(os.path.join(ROOT, "include", "fasted.h")).read()
-    return sorted(set(re.findall(r"\b(fasted_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(fasted_[a-z_0-9]+)\s*\(", src)))
 
 
 def test_library_exports_every_header_symbol():
