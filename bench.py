@@ -264,7 +264,13 @@ def main():
         pairs = int(c.item())
     flops = 2.0 * n * n * d
     value = flops / (ms / 1e3) / 1e12
-    peak, peak_sus, peak_src = load_peaks()
+    peak_burst, peak_sus, peak_src = load_peaks()
+    # A join launch at C4 runs ~1.4 s back to back under the 1 kW cap: the
+    # "kernel inside a long step" case, whose denominator is the sustained
+    # cuBLAS figure (B200_PROFILING.md); the burst fraction is kept beside it.
+    peak = peak_sus if peak_sus else peak_burst
+    peak_kind = "bf16_tflops_sustained" if peak_sus else "bf16_tflops (burst)"
+    kernel_name = _lib.load().fasted_join_kernel_name(dd.d_pad, _lib.JOIN_TC).decode()
     # roofline of the dominant kernel (the join): algorithmic flops per launch
     rows_logical = max(0, min(rows[1], n) - min(rows[0], n))
     flops_launch = 2.0 * rows_logical * n * d
@@ -343,20 +349,24 @@ def main():
                 "parallelism": f"row-block shard x{world} (no collective)",
                 "l2": "inputs %.2f GB >> 126 MB L2; no flush" % (h2d / 1e9),
             },
-            "pct_of_fp16_peak": {"measured_burst": value / peak, "measured_sustained":
+            "pct_of_fp16_peak": {"measured_burst": value / peak_burst, "measured_sustained":
                                  (value / peak_sus if peak_sus else None),
                                  "nominal_2250": value / 2250.0},
             "pairs_per_s": pairs / (ms / 1e3),
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
                          "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": peak_src + " bf16_tflops (burst)",
-                         "kernel": "fasted::tc::join_tc_kernel",
+                         "peak_source": f"{peak_src} {peak_kind} (MEASURED_PEAKS.json)",
+                         "frac_of_burst": achieved / peak_burst,
+                         "kernel": kernel_name,
+                         "launch_includes": "Gram-diagonal pre-pass + augment-row prep "
+                                            "(~1/7800 of the join) + the join",
                          "output_write_bound_ms": pairs_local * 12 / 6552e9 * 1e3},
             "e2e": {"value": flops / e2e_s / 1e12, "unit": "TFLOPS",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_s, "api": "paper_2508_21230_b200.self_join"},
             "accuracy_vs_fp64": acc,
-            "gpu_launches": args.steps,
+            # per step: Gram-diagonal pre-pass, aug_prepare_kernel, the join
+            "gpu_launches": 3 * args.steps,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
             "per_step_ms": per_step,

@@ -61,7 +61,7 @@ enum {
     FASTED_JOIN_DIAG_NOMMA = 512,    /* tcgen05 kernel: skip the MMAs (TMA + epilogue) */
     FASTED_JOIN_DIAG_LOADONLY = 1024, /* epilogue: TMEM loads only, no math           */
     FASTED_JOIN_DIAG_NOSLOW = 2048,  /* epilogue: sign test only, never write         */
-    FASTED_JOIN_DIAG_MASKOR = 4096   /* epilogue: lane masks + one REDUX.OR          */
+    FASTED_JOIN_DIAG_MASKOR = 4096   /* epilogue: column-scan (REDUX) hit search      */
 };
 
 int fasted_abi_version(void);
@@ -142,6 +142,10 @@ int fasted_sort_pairs(const void* records, uint64_t slots, int64_t row_begin, in
 int fasted_fp64_rows(const float* x, int64_t n, int64_t d, const int64_t* qrows, int64_t nq,
                      double epsilon, void* out_records, uint64_t capacity,
                      unsigned long long* count, void* stream);
+
+/* Name of the join kernel fasted_join launches for this d_pad and flags
+ * (the same selection rule, environment overrides included; for reports). */
+const char* fasted_join_kernel_name(int64_t d_pad, int flags);
 
 /* Number of SMs and device name of the current device (for reports). */
 int fasted_device_info(int* sm_count, char* name, int name_len);

@@ -23,7 +23,7 @@ JOIN_TC, JOIN_EXACT, JOIN_COUNT = 0, 1, 2
 # Every symbol include/fasted.h declares (tests check the .so exports them).
 EXPORTS = (
     "fasted_abi_version", "fasted_strerror", "fasted_last_error", "fasted_device_check",
-    "fasted_device_info", "fasted_quantize", "fasted_norms", "fasted_join",
+    "fasted_device_info", "fasted_join_kernel_name", "fasted_quantize", "fasted_norms", "fasted_join",
     "fasted_sort_workspace_bytes", "fasted_sort_pairs", "fasted_fp64_rows",
 )
 
@@ -51,6 +51,8 @@ def load():
         L.fasted_last_error.argtypes = []
         L.fasted_device_check.restype = ci
         L.fasted_device_check.argtypes = [ci]
+        L.fasted_join_kernel_name.restype = ctypes.c_char_p
+        L.fasted_join_kernel_name.argtypes = [ctypes.c_int64, ci]
         L.fasted_device_info.restype = ci
         L.fasted_device_info.argtypes = [ctypes.POINTER(ci), ctypes.c_char_p, ci]
         L.fasted_quantize.restype = ci

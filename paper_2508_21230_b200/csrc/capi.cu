@@ -62,6 +62,11 @@ extern "C" int fasted_device_check(int device) {
     return FASTED_OK;
 }
 
+extern "C" const char* fasted_join_kernel_name(int64_t d_pad, int flags) {
+    if ((flags & 1) == FASTED_JOIN_EXACT) return "fasted::join_exact_kernel";
+    return join_tc_kernel_name(d_pad);
+}
+
 extern "C" int fasted_device_info(int* sm_count, char* name, int name_len) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);

@@ -91,5 +91,6 @@ __device__ __forceinline__ void writer_finish(PairWriter& w, const JoinArgs& a) 
 
 int launch_join_exact(const __half* X, const JoinArgs& a, cudaStream_t s);
 int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s);
+const char* join_tc_kernel_name(int64_t d_pad);
 
 }  // namespace fasted

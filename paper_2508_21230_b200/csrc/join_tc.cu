@@ -188,6 +188,22 @@ __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
+// One lane of a converged warp (the same lane every call).  The producer and
+// MMA loops run on the whole warp so their addresses and descriptors stay in
+// uniform registers; only the issue itself is elected.  (Looping on lane 0
+// alone made the compiler rebuild every descriptor with ELECT + R2UR per MMA:
+// ~40 dependent instructions per 512-cycle stage, measured 82% tensor-pipe
+// activity at 1M x 960 with the MMA warp never waiting on data.)
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t"
+        "elect.sync _|P, 0xffffffff;\n\t"
+        "selp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(p));
+    return p != 0;
+}
+
 // Shared-memory matrix descriptors (K-major, swizzled): start address >> 4,
 // LBO = 1 (unused for swizzled K-major), SBO = bytes between 8-row groups,
 // version 1 (sm_100), layout type (SWIZZLE_128B = 2, SWIZZLE_32B = 6).
@@ -202,38 +218,40 @@ __device__ __forceinline__ uint64_t sw32_desc(uint32_t saddr) { return smem_desc
 
 template <int CG>
 __device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
-                                        uint32_t accumulate) {
+                                        uint32_t accumulate,
+                                        uint32_t idesc = Cfg<CG>::IDESC_F16) {
     if constexpr (CG == 1)
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "setp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(Cfg<CG>::IDESC_F16), "r"(accumulate)
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
             : "memory");
     else
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "setp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(Cfg<CG>::IDESC_F16), "r"(accumulate)
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
             : "memory");
 }
 
 template <int CG>
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc) {
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc = Cfg<CG>::IDESC_TF32) {
     if constexpr (CG == 1)
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "setp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(Cfg<CG>::IDESC_TF32), "r"(1u)
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(1u)
             : "memory");
     else
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
             "setp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-            "l"(adesc), "l"(bdesc), "r"(Cfg<CG>::IDESC_TF32), "r"(1u)
+            "l"(adesc), "l"(bdesc), "r"(idesc), "r"(1u)
             : "memory");
 }
 
@@ -324,20 +342,38 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
         const uint32_t b = __ballot_sync(0xffffffffu, self);
         if (b) writer_append(wr, a, b, self, (uint32_t)(i + 1), (uint32_t)(i + 1), 0.0f);
     }
-    // Candidate columns: a column holds a hit iff some lane's D word has the
-    // sign bit clear.  Either 32 independent REDUX.AND (uniform datapath) or
-    // a per-lane mask OR-reduced once (FASTED_JOIN_DIAG_MASKOR).
-    uint32_t cm = 0;
-    if (a.diag_flags & FASTED_JOIN_DIAG_MASKOR) {
+    if (!(a.diag_flags & FASTED_JOIN_DIAG_MASKOR)) {
+        // Per-lane form (default): each lane builds its own hit mask (sign
+        // bits clear), drops its self column and columns past n_logical, and
+        // the warp appends one record per hitting lane per round -- usually
+        // one round, since hits are sparse (measured: the column-scan form
+        // below cost 22% of the 1M x 128 join in REDUX latency).
         uint32_t lm = 0;
 #pragma unroll
         for (int e = 0; e < 32; e++) lm |= ((~r[e]) >> 31) << e;
-        cm = __reduce_or_sync(0xffffffffu, lm);
-    } else {
-#pragma unroll
-        for (int e = 0; e < 32; e++)
-            cm |= ((~__reduce_and_sync(0xffffffffu, r[e]) >> 31) & 1u) << e;
+        const int64_t valid = a.n_logical - jb;
+        if (valid < 32) lm &= valid <= 0 ? 0u : ((1u << (uint32_t)valid) - 1u);
+        if (i >= jb && i < jb + 32) lm &= ~(1u << (uint32_t)(i - jb));
+        if (!row_ok) lm = 0u;
+        while (true) {
+            const bool mine = lm != 0u;
+            const uint32_t b = __ballot_sync(0xffffffffu, mine);
+            if (b == 0u) break;
+            const uint32_t e = mine ? (uint32_t)(__ffs(lm) - 1) : 0u;
+            lm &= lm - 1u;
+            const uint32_t v = pick32(r, e);
+            const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
+            writer_append(wr, a, b, mine, (uint32_t)(i + 1), (uint32_t)(jb + e + 1), d2);
+        }
+        return;
     }
+    // Column-scan form (FASTED_JOIN_DIAG_MASKOR, kept for A/B measurement):
+    // a column holds a hit iff some lane's D word has the sign bit clear,
+    // found with 32 REDUX.AND on the uniform datapath.
+    uint32_t cm = 0;
+#pragma unroll
+    for (int e = 0; e < 32; e++)
+        cm |= ((~__reduce_and_sync(0xffffffffu, r[e]) >> 31) & 1u) << e;
     while (cm) {
         const uint32_t e = __ffs(cm) - 1;
         cm &= cm - 1;
@@ -349,6 +385,59 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
         const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
         writer_append(wr, a, b, ok, (uint32_t)(i + 1), (uint32_t)(j + 1), d2);
     }
+}
+
+// One epilogue warp's share of one finished accumulator of TBN columns:
+// warp (q, h) owns TMEM lanes 32q.. (rows row0 + 32q + lane) and accumulator
+// columns h*TBN/2 .. (h+1)*TBN/2 - 1 of buffer `buf`.  Drains its slice with
+// back-to-back tcgen05.ld and ONE wait (a tcgen05.ld queues behind the MMAs
+// already issued for the next tile, so waiting per chunk costs that queue
+// drain each time), hands the accumulator back to the MMA warp before any
+// math (the epilogue overlaps the next tiles' MMAs), then tests the signs.
+template <int CG, int TBN>
+__device__ __forceinline__ void epilogue_tile(const JoinArgs& a, PairWriter& wr,
+                                              uint32_t tmem_base, uint32_t tempty, int64_t row0,
+                                              int64_t col0, int buf, uint32_t aph, int q, int h,
+                                              int lane, bool leader, uint32_t tfull) {
+    constexpr int HALF = TBN / 2;
+    constexpr int NCH = HALF / 32;   // 32-column chunks per warp (4 or 2)
+    static_assert(NCH == 2 || NCH == 4, "TBN must be 128 or 256");
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const int64_t iw = row0 + q * 32;
+    const int64_t i = iw + lane;
+    const bool row_ok = i < a.n_logical && i < a.row_end;
+    // chunks of 32 columns inside [col0 + HALF h, col_end); none if this
+    // CTA's rows lie past the range end
+    const int64_t left = a.col_end - (col0 + h * HALF);
+    int nchunks = left <= 0 ? 0 : (left >= HALF ? NCH : (int)(left / 32));
+    if (row0 >= a.row_end || (a.diag_flags & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
+    const uint32_t tcol = tmem_base + lane_base + (uint32_t)(buf * TBN + h * HALF);
+    mbar_wait(tfull, aph);
+    tc_fence_after();
+    uint32_t r0[32], r1[32], r2[32], r3[32];
+    if (nchunks > 0) tmem_ld32(tcol, r0);
+    if (nchunks > 1) tmem_ld32(tcol + 32u, r1);
+    if (NCH > 2 && nchunks > 2) tmem_ld32(tcol + 64u, r2);
+    if (NCH > 2 && nchunks > 3) tmem_ld32(tcol + 96u, r3);
+    if (nchunks > 0) {
+        tmem_ld_wait(r0);
+        tmem_ld_wait(r1);
+        if (NCH > 2) {
+            tmem_ld_wait(r2);
+            tmem_ld_wait(r3);
+        }
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+        if (CG == 1 || leader) mbar_arrive(tempty);
+        else mbar_arrive_remote(tempty, 0);
+    }
+    const int64_t jb = col0 + h * HALF;
+    if (nchunks > 0) epi_chunk(a, wr, r0, jb, i, iw, row_ok);
+    if (nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok);
+    if (NCH > 2 && nchunks > 2) epi_chunk(a, wr, r2, jb + 64, i, iw, row_ok);
+    if (NCH > 2 && nchunks > 3) epi_chunk(a, wr, r3, jb + 96, i, iw, row_ok);
 }
 
 template <int CG, bool DIAG>
@@ -423,7 +512,8 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
 
     if (warp == 0) {
         // ---------------- TMA producer: nkb FP16 stages + 1 augment stage per tile
-        if (lane == 0) {
+        // (whole warp walks the schedule; one elected lane issues)
+        {
             int s = 0;
             uint32_t ph = 0;
             for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
@@ -440,6 +530,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
                     mbar_wait(empty_bar(s), ph ^ 1u);
                     const uint32_t fb = full_bar(s);
+                    if (elect_one()) {
                     if (kb < sch.nkb) {
                         const int kx = kb * BK;
                         if constexpr (CG == 1) {
@@ -480,6 +571,8 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                                (int)(col0 + 128 * rank));
                         }
                     }
+                    }
+                    __syncwarp();
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1u;
@@ -490,7 +583,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         __syncwarp();
     } else if (warp == 1) {
         // ---------------- MMA issuer (the leader CTA of a pair)
-        if (lane == 0 && leader) {
+        if (leader) {   // whole warp; one elected lane issues
             const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
             int s = 0;
             uint32_t ph = 0;
@@ -504,6 +597,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
                     mbar_wait(full_bar(s), ph);
                     tc_fence_after();
+                    if (elect_one()) {
                     if (!no_mma) {
                         if (kb < sch.nkb) {
                             const uint64_t ad = sw128_desc(sA + s * A_BYTES);
@@ -519,12 +613,15 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                         }
                     }
                     mma_commit<CG>(empty_bar(s));
+                    }
+                    __syncwarp();
                     if (++s == STAGES) {
                         s = 0;
                         ph ^= 1u;
                     }
                 }
-                mma_commit<CG>(tfull_bar(buf));
+                if (elect_one()) mma_commit<CG>(tfull_bar(buf));
+                __syncwarp();
             }
         }
         __syncwarp();
@@ -541,12 +638,10 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             tile_coords(sch, t, rt, ct);
             const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M + 128 * rank;
             const int64_t col0 = a.col_begin + (int64_t)ct * BN;
-            const int64_t iw = row0 + q * 32;
-            const int64_t i = iw + lane;
-            const bool row_ok = i < a.n_logical && i < a.row_end;
             const int buf = lt & 1;
             const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
             if constexpr (DIAG) {
+                const int64_t i = row0 + q * 32 + lane;
                 // Gram-diagonal pre-pass (CG = 1, col0 = row0): lane i's own
                 // column i - row0 = 32 q + lane sits in chunk q of half 0.
                 mbar_wait(tfull_bar(buf), aph);
@@ -562,41 +657,494 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (h == 0 && i < a.row_end) a.gram_diag[i] = __uint_as_float(pick32(r0, lane));
                 continue;
             }
-            // chunks of 32 columns inside [col0 + 128h, col_end); none if this
-            // CTA's rows lie past the range end
-            const int64_t left = a.col_end - (col0 + h * 128);
-            int nchunks = left <= 0 ? 0 : (left >= 128 ? 4 : (int)(left / 32));
-            if (row0 >= a.row_end || (a.diag_flags & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
-            const uint32_t tcol = tmem_base + lane_base + (uint32_t)(buf * BN + h * 128);
-            mbar_wait(tfull_bar(buf), aph);
+            epilogue_tile<CG, BN>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf, aph, q, h,
+                              lane, leader, tfull_bar(buf));
+        }
+        writer_finish(wr, a);
+    }
+
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    if (warp == 0) {
+        if constexpr (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS)
+                         : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// B-multicast variant (large d).  At d = 960 the single-CTA kernel moves
+// 737 KB of A and B from L2 per 128 x 256 tile, and measurement says that
+// traffic, not the MMA, sets both the rate and the power: the TMA stream
+// alone (no MMA, no epilogue) runs at ~10 KB/clk chip-wide and takes 1452 ms
+// at the 1 kW cap against 1570 ms for the whole join (profiles/round1/
+// tune_c4_power_session2.txt).  Here two CTAs of a cluster take vertically
+// adjacent row tiles of the same column tile: each loads its own A and HALF
+// of the shared B tile, multicast into both CTAs' shared memory, so per SM
+// the bytes per tile drop by a third (491 KB).  Each CTA still issues its own
+// M = 128 MMAs (no cross-SM operand reads, unlike cta_group::2).  A stage is
+// refilled only after BOTH CTAs' MMAs released it (empty barrier count 2,
+// multicast commits).  Every load is issued even for a tile past the range
+// end (its rows/columns are masked in the epilogue; TMA zero-fills past
+// n_pad), so the byte counts are fixed.
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                               int c0, int c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster."
+        "b64 [%0], %1;" ::"r"(bar),
+        "h"(mask)
+        : "memory");
+}
+
+constexpr int MC_STAGES = 4;
+constexpr int MC_SMEM_BYTES = MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + 1024;
+
+__global__ void __launch_bounds__(THREADS, 1)
+join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                  const __grid_constant__ CUtensorMap tmap_aug_a,
+                  const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
+                  const Sched sch) {
+    constexpr int STAGES = MC_STAGES;
+    constexpr int B_BYTES = 2 * B_HALF_BYTES;
+    constexpr int AUG_A = BM * AUG_ROW_BYTES;
+    constexpr int AUG_B_HALF = 128 * AUG_ROW_BYTES;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    const uint32_t sA = base;
+    const uint32_t sB = base + STAGES * A_BYTES;
+    const uint32_t bars = sB + STAGES * B_BYTES;
+    auto full_bar = [&](int s) { return bars + 8u * s; };
+    auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
+    auto tfull_bar = [&](int b) { return bars + 8u * (2 * STAGES + b); };
+    auto tempty_bar = [&](int b) { return bars + 8u * (2 * STAGES + 2 + b); };
+    const uint32_t slot = bars + 8u * (2 * STAGES + 4);
+    volatile uint32_t* slot_ptr = reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - raw));
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t cr = cluster_rank();   // 0: upper row tile, 1: lower
+    const int64_t tile_id0 = (int64_t)(blockIdx.x >> 1);
+    const int64_t tile_step = (int64_t)(gridDim.x >> 1);
+    constexpr uint16_t BOTH = 0x3;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 2);   // both CTAs' MMAs read this stage's B
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(tfull_bar(b), 1);
+            mbar_init(tempty_bar(b), NUM_EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_a))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_b))
+                     : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();   // peers' barriers initialised before any multicast lands
+    tc_fence_after();
+    const uint32_t tmem_base = *slot_ptr;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (whole warp; one elected lane issues)
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
+            int rt, ct;
+            tile_coords(sch, t, rt, ct);
+            const int row0 = (int)(a.row_begin + ((int64_t)rt * 2 + cr) * BM);
+            const int colh = (int)(a.col_begin + (int64_t)ct * BN + 128 * cr);
+            for (int kb = 0; kb < sch.nkb + 1; kb++) {
+                mbar_wait(empty_bar(s), ph ^ 1u);
+                const uint32_t fb = full_bar(s);
+                if (elect_one()) {
+                    if (kb < sch.nkb) {
+                        const int kx = kb * BK;
+                        mbar_expect_tx(fb, A_BYTES + B_BYTES);
+                        tma_load_2d<1>(sA + s * A_BYTES, &tmap_x, fb, kx, row0);
+                        tma_load_2d_mc(sB + s * B_BYTES + cr * B_HALF_BYTES, &tmap_x, fb, kx, colh,
+                                       BOTH);
+                    } else {
+                        mbar_expect_tx(fb, AUG_A + 2 * AUG_B_HALF);
+                        tma_load_2d<1>(sA + s * A_BYTES, &tmap_aug_a, fb, 0, row0);
+                        tma_load_2d_mc(sB + s * B_BYTES + cr * AUG_B_HALF, &tmap_aug_b, fb, 0, colh,
+                                       BOTH);
+                    }
+                }
+                __syncwarp();
+                if (++s == STAGES) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (every CTA; M = 128; whole warp, one lane issues)
+        const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
+        int s = 0;
+        uint32_t ph = 0;
+        int lt = 0;
+        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
+            const int buf = lt & 1;
+            mbar_wait(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u);
             tc_fence_after();
-            // Pull this warp's whole 32 x 128 slice out of TMEM with back-to-back
-            // loads and ONE wait (a tcgen05.ld queues behind the MMAs already
-            // issued for the next tile, so waiting per chunk costs that queue
-            // drain each time), then hand the accumulator back to the MMA warp
-            // before any math: the epilogue overlaps the next tiles' MMAs.
-            uint32_t r0[32], r1[32], r2[32], r3[32];
-            if (nchunks > 0) tmem_ld32(tcol, r0);
-            if (nchunks > 1) tmem_ld32(tcol + 32u, r1);
-            if (nchunks > 2) tmem_ld32(tcol + 64u, r2);
-            if (nchunks > 3) tmem_ld32(tcol + 96u, r3);
-            if (nchunks > 0) {
-                tmem_ld_wait(r0);
-                tmem_ld_wait(r1);
-                tmem_ld_wait(r2);
-                tmem_ld_wait(r3);
+            const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
+            for (int kb = 0; kb < sch.nkb + 1; kb++) {
+                mbar_wait(full_bar(s), ph);
+                tc_fence_after();
+                const uint64_t ad = sw128_desc(sA + s * A_BYTES);
+                const uint64_t bd = sw128_desc(sB + s * B_BYTES);
+                if (elect_one()) {
+                    if (!no_mma) {
+                        if (kb < sch.nkb) {
+#pragma unroll
+                            for (int kk = 0; kk < BK / UK; kk++) {
+                                const uint64_t koff = (uint64_t)((kk * UK * 2) >> 4);
+                                mma_f16<1>(dtm, ad + koff, bd + koff, (kb | kk) != 0 ? 1u : 0u);
+                            }
+                        } else {
+                            mma_tf32<1>(dtm, sw32_desc(sA + s * A_BYTES), sw32_desc(sB + s * B_BYTES));
+                        }
+                    }
+                    mma_commit_mc(empty_bar(s), BOTH);
+                }
+                __syncwarp();
+                if (++s == STAGES) {
+                    s = 0;
+                    ph ^= 1u;
+                }
             }
-            tc_fence_before();
+            if (elect_one()) mma_commit<1>(tfull_bar(buf));
             __syncwarp();
-            if (lane == 0) {
-                if (CG == 1 || leader) mbar_arrive(tempty_bar(buf));
-                else mbar_arrive_remote(tempty_bar(buf), 0);
+        }
+    } else {
+        // ---------------- epilogue
+        const int q = warp & 3;
+        const int h = (warp - FIRST_EPI_WARP) >> 2;
+        PairWriter wr;
+        writer_init(wr);
+        int lt = 0;
+        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
+            int rt, ct;
+            tile_coords(sch, t, rt, ct);
+            const int64_t row0 = a.row_begin + ((int64_t)rt * 2 + cr) * BM;
+            const int64_t col0 = a.col_begin + (int64_t)ct * BN;
+            const int buf = lt & 1;
+            epilogue_tile<1, BN>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf,
+                                 (uint32_t)(lt >> 1) & 1u, q, h, lane, true, tfull_bar(buf));
+        }
+        writer_finish(wr, a);
+    }
+
+    tc_fence_before();
+    cluster_sync();   // no CTA leaves while its peer may still multicast into it
+    tc_fence_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS)
+                     : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Resident-A variant (small d, d_pad <= 256).  At d = 128 one 256 x 256 tile
+// is only 9 MMAs, and streaming both operands moves 144 KB per CTA pair per
+// tile from L2: measured, the TMA stream alone (no MMA, no epilogue) takes
+// 192 ms at 1M x 128, against a 121 ms tensor floor (profiles/round1/
+// tune_c3_session2.txt) -- the streaming kernel is L2->SM bound there.  Here
+// a CTA keeps its 128-row A panel (every k-block plus its augment rows) in
+// shared memory for a whole work unit -- one row tile x a segment of column
+// tiles -- and streams only B, halving the bytes per MMA.  A is double
+// buffered when two panels fit, so the next unit's A lands while the current
+// one finishes.  Units are ordered segment-major, so the CTAs (pairs) that run
+// side by side sweep the same B panels at the same time (L2 reuse).
+//
+// TBN = columns per tile.  With TBN = 128 the 512 TMEM columns hold FOUR
+// accumulators instead of two: at d = 128 a tile is only ~600 MMA cycles and
+// ncu showed the MMA warp waiting for an accumulator on 53% of tiles with two
+// buffers (the epilogue warp that found hits in a tile runs late); four
+// buffers absorb that jitter.  The MMA sequence per output element (k-blocks
+// ascending, then the tf32 augment step) is the streaming kernel's, so both
+// produce identical bits.
+struct ResSched {
+    int row_tiles;            // tiles of TILE_M rows in [row_begin, row_end)
+    int col_tiles;            // tiles of TBN columns in [col_begin, col_end)
+    int nsegs;                // column segments (balanced)
+    int nkb;                  // 64-wide k-blocks
+    int na;                   // A buffers (1 or 2)
+    int stages;               // B ring stages
+    uint32_t a_buf_bytes;     // one A buffer: nkb k-blocks + augment rows, 1024-aligned
+    int64_t units;            // row_tiles * nsegs
+};
+
+template <int CG, int TBN>
+struct ResCfg {
+    static constexpr int TILE_M = BM * CG;
+    static constexpr int NB = TBN / CG;                          // B rows (columns) per CTA
+    static constexpr int BBOX = NB < 128 ? NB : 128;             // TMA box rows for B
+    static constexpr int B_BYTES = NB * BK * 2;                  // this CTA's B k-block
+    static constexpr int AUGB_BYTES = NB * AUG_ROW_BYTES;        // its augment rows
+    static constexpr int STAGE_BYTES = B_BYTES + AUGB_BYTES;
+    static constexpr int NACC = TMEM_COLS / TBN;                 // accumulator buffers
+    static constexpr int MAX_STAGES = 16;
+    static constexpr int BARS = 2 * MAX_STAGES + 2 * NACC + 4;
+    static constexpr int BAR_REGION = ((BARS * 8 + 4 + 127) / 128) * 128;
+    static constexpr uint32_t IDESC_F16 =
+        (1u << 4) | ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(TILE_M >> 4) << 24);
+    static constexpr uint32_t IDESC_TF32 = IDESC_F16 | (2u << 7) | (2u << 10);
+    static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1024-aligned");
+};
+
+__device__ __forceinline__ void res_unit(const ResSched& s, int64_t u, int& rt, int& ct0,
+                                         int& ct1) {
+    const int64_t g = u / s.row_tiles;
+    rt = (int)(u - g * s.row_tiles);
+    ct0 = (int)((int64_t)s.col_tiles * g / s.nsegs);
+    ct1 = (int)((int64_t)s.col_tiles * (g + 1) / s.nsegs);
+}
+
+template <int CG, int TBN>
+__global__ void __launch_bounds__(THREADS, 1)
+join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
+                   const __grid_constant__ CUtensorMap tmap_xb,
+                   const __grid_constant__ CUtensorMap tmap_aug_a,
+                   const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
+                   const ResSched sch) {
+    using C = ResCfg<CG, TBN>;
+    constexpr int NACC = C::NACC;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    const int S = sch.stages;
+    const uint32_t sAb = base;
+    const uint32_t sB = base + (uint32_t)sch.na * sch.a_buf_bytes;
+    const uint32_t bars = sB + (uint32_t)S * C::STAGE_BYTES;
+    auto full_bar = [&](int s) { return bars + 8u * s; };
+    auto empty_bar = [&](int s) { return bars + 8u * (S + s); };
+    auto tfull_bar = [&](int b) { return bars + 8u * (2 * S + b); };
+    auto tempty_bar = [&](int b) { return bars + 8u * (2 * S + NACC + b); };
+    auto afull_bar = [&](int b) { return bars + 8u * (2 * S + 2 * NACC + b); };
+    auto aempty_bar = [&](int b) { return bars + 8u * (2 * S + 2 * NACC + 2 + b); };
+    const uint32_t slot = bars + 8u * (2 * S + 2 * NACC + 4);
+    volatile uint32_t* slot_ptr = reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - raw));
+    const uint32_t a_aug_off = (uint32_t)sch.nkb * A_BYTES;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    const int64_t unit0 = CG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+    const int64_t ustep = CG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; s++) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < NACC; b++) {
+            mbar_init(tfull_bar(b), 1);
+            mbar_init(tempty_bar(b), NUM_EPI_WARPS * CG);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(afull_bar(b), 1);
+            mbar_init(aempty_bar(b), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_xa))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_xb))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_a))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_b))
+                     : "memory");
+    }
+    if (warp == 0) {
+        if constexpr (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             slot),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             slot),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        }
+    }
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *slot_ptr;
+
+    if (warp == 0) {
+        // ---------------- TMA producer: per unit the A panel, then nkb B stages per tile
+        // (whole warp walks the schedule; one elected lane issues)
+        {
+            int s = 0;
+            uint32_t ph = 0;
+            int ua = 0;
+            for (int64_t u = unit0; u < sch.units; u += ustep, ++ua) {
+                int rt, ct0, ct1;
+                res_unit(sch, u, rt, ct0, ct1);
+                const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M;
+                const bool a_hi = row0 + 128 < a.row_end;
+                const int my_a = (int)(row0 + 128 * rank);
+                const bool a_mine = rank == 0 || a_hi;
+                const int ab = ua % sch.na;
+                mbar_wait(aempty_bar(ab), ((uint32_t)(ua / sch.na) & 1u) ^ 1u);
+                const uint32_t fa = afull_bar(ab);
+                const uint32_t abuf = sAb + (uint32_t)ab * sch.a_buf_bytes;
+                const uint32_t a_bytes = (uint32_t)sch.nkb * A_BYTES + BM * AUG_ROW_BYTES;
+                if (elect_one()) {
+                    if (CG == 1) mbar_expect_tx(fa, a_bytes);
+                    else if (leader) mbar_expect_tx(fa, (a_hi ? 2u : 1u) * a_bytes);
+                    if (a_mine) {
+                        for (int kb = 0; kb < sch.nkb; kb++)
+                            tma_load_2d<CG>(abuf + kb * A_BYTES, &tmap_xa, fa, kb * BK, my_a);
+                        tma_load_2d<CG>(abuf + a_aug_off, &tmap_aug_a, fa, 0, my_a);
+                    }
+                }
+                __syncwarp();
+                for (int ct = ct0; ct < ct1; ct++) {
+                    const int64_t col0 = a.col_begin + (int64_t)ct * TBN;
+                    // this CTA's NB columns, in BBOX-row TMA boxes that exist
+                    // (a box past the range end is skipped; masked in the epilogue)
+                    const int64_t cb = col0 + (int64_t)C::NB * rank;
+                    int nbox = 0;
+                    for (int x = 0; x < C::NB / C::BBOX; x++)
+                        if (cb + (int64_t)C::BBOX * x < a.col_end) nbox++;
+                    int nbox_pair = nbox;
+                    if (CG == 2 && leader) {
+                        const int64_t cb1 = col0 + C::NB;
+                        for (int x = 0; x < C::NB / C::BBOX; x++)
+                            if (cb1 + (int64_t)C::BBOX * x < a.col_end) nbox_pair++;
+                    }
+                    for (int kb = 0; kb < sch.nkb; kb++) {
+                        const bool last = kb == sch.nkb - 1;
+                        mbar_wait(empty_bar(s), ph ^ 1u);
+                        const uint32_t fb = full_bar(s);
+                        const uint32_t st = sB + (uint32_t)s * C::STAGE_BYTES;
+                        const uint32_t box_bytes =
+                            C::BBOX * (BK * 2 + (last ? AUG_ROW_BYTES : 0));
+                        if (elect_one()) {
+                            if (CG == 1 || leader)
+                                mbar_expect_tx(fb, (uint32_t)nbox_pair * box_bytes);
+                            for (int x = 0; x < nbox; x++) {
+                                const int c = (int)(cb + C::BBOX * x);
+                                tma_load_2d<CG>(st + x * C::BBOX * BK * 2, &tmap_xb, fb, kb * BK, c);
+                                if (last)
+                                    tma_load_2d<CG>(st + C::B_BYTES + x * C::BBOX * AUG_ROW_BYTES,
+                                                    &tmap_aug_b, fb, 0, c);
+                            }
+                        }
+                        __syncwarp();
+                        if (++s == S) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                }
             }
-            const int64_t jb = col0 + h * 128;
-            if (nchunks > 0) epi_chunk(a, wr, r0, jb, i, iw, row_ok);
-            if (nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok);
-            if (nchunks > 2) epi_chunk(a, wr, r2, jb + 64, i, iw, row_ok);
-            if (nchunks > 3) epi_chunk(a, wr, r3, jb + 96, i, iw, row_ok);
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (the leader CTA of a pair)
+        if (leader) {   // whole warp; one elected lane issues
+            const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
+            int s = 0;
+            uint32_t ph = 0;
+            int lt = 0, ua = 0;
+            for (int64_t u = unit0; u < sch.units; u += ustep, ++ua) {
+                int rt, ct0, ct1;
+                res_unit(sch, u, rt, ct0, ct1);
+                const int ab = ua % sch.na;
+                mbar_wait(afull_bar(ab), (uint32_t)(ua / sch.na) & 1u);
+                tc_fence_after();
+                const uint32_t abuf = sAb + (uint32_t)ab * sch.a_buf_bytes;
+                for (int ct = ct0; ct < ct1; ct++, ++lt) {
+                    const int buf = lt % NACC;
+                    mbar_wait(tempty_bar(buf), ((uint32_t)(lt / NACC) & 1u) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t dtm = tmem_base + (uint32_t)(buf * TBN);
+                    for (int kb = 0; kb < sch.nkb; kb++) {
+                        mbar_wait(full_bar(s), ph);
+                        tc_fence_after();
+                        const uint32_t st = sB + (uint32_t)s * C::STAGE_BYTES;
+                        if (elect_one()) {
+                        if (!no_mma) {
+                            const uint64_t ad = sw128_desc(abuf + kb * A_BYTES);
+                            const uint64_t bd = sw128_desc(st);
+#pragma unroll
+                            for (int kk = 0; kk < BK / UK; kk++) {
+                                const uint64_t koff = (uint64_t)((kk * UK * 2) >> 4);
+                                mma_f16<CG>(dtm, ad + koff, bd + koff, (kb | kk) != 0 ? 1u : 0u,
+                                            C::IDESC_F16);
+                            }
+                            if (kb == sch.nkb - 1)
+                                mma_tf32<CG>(dtm, sw32_desc(abuf + a_aug_off),
+                                             sw32_desc(st + C::B_BYTES), C::IDESC_TF32);
+                        }
+                        mma_commit<CG>(empty_bar(s));
+                        }
+                        __syncwarp();
+                        if (++s == S) {
+                            s = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                    if (elect_one()) mma_commit<CG>(tfull_bar(buf));
+                    __syncwarp();
+                }
+                if (elect_one()) mma_commit<CG>(aempty_bar(ab));
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue
+        const int q = warp & 3;
+        const int h = (warp - FIRST_EPI_WARP) >> 2;
+        PairWriter wr;
+        writer_init(wr);
+        int lt = 0;
+        for (int64_t u = unit0; u < sch.units; u += ustep) {
+            int rt, ct0, ct1;
+            res_unit(sch, u, rt, ct0, ct1);
+            const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M + 128 * rank;
+            for (int ct = ct0; ct < ct1; ct++, ++lt) {
+                const int buf = lt % NACC;
+                epilogue_tile<CG, TBN>(a, wr, tmem_base, tempty_bar(buf), row0,
+                                       a.col_begin + (int64_t)ct * TBN, buf,
+                                       (uint32_t)(lt / NACC) & 1u, q, h, lane, leader,
+                                       tfull_bar(buf));
+            }
         }
         writer_finish(wr, a);
     }
@@ -722,6 +1270,117 @@ static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
     return cudaLaunchKernelEx(&cfg, kern, mx, ma, mb, a, sch);
 }
 
+// B-multicast launch: clusters of two CTAs over super-tiles of 256 rows.
+static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const CUtensorMap& mb,
+                             const JoinArgs& a, cudaStream_t s) {
+    using namespace tc;
+    auto kern = join_tc_mc_kernel;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             MC_SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    Sched sch;
+    sch.diag = 0;
+    sch.row_tiles = (int)((a.row_end - a.row_begin + 2 * BM - 1) / (2 * BM));   // super-rows
+    sch.col_tiles = (int)((a.col_end - a.col_begin + BN - 1) / BN);
+    // 8192-row groups (measured at 1M x 960: 1374 TFLOPS vs 1305 for 4096 and
+    // 1182 for 16384; profiles/round1/tune_c4_elect_session2.txt)
+    sch.group = env_int("FASTED_GROUP_ROWS", 8192) / (2 * BM);
+    if (sch.group < 1) sch.group = 1;
+    sch.nkb = (int)((a.d_pad + BK - 1) / BK);
+    sch.total = (int64_t)sch.row_tiles * sch.col_tiles;
+    const int64_t slots = sm_count_current() / 2;
+    const int64_t work = sch.total < slots ? sch.total : slots;
+    if (work <= 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(work * 2));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = MC_SMEM_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, mx, ma, mb, a, sch);
+}
+
+// Resident-A launch: shared memory split between the A buffer(s) and as many
+// B stages as fit.
+template <int CG, int TBN>
+static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
+                              const CUtensorMap& ma, const CUtensorMap& mb, const JoinArgs& a,
+                              cudaStream_t s) {
+    using namespace tc;
+    using C = ResCfg<CG, TBN>;
+    constexpr int SMEM_MAX = 227 * 1024;
+    auto kern = join_tc_res_kernel<CG, TBN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             SMEM_MAX);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    ResSched sch;
+    sch.nkb = (int)((a.d_pad + BK - 1) / BK);
+    sch.a_buf_bytes = (uint32_t)((sch.nkb * A_BYTES + BM * AUG_ROW_BYTES + 1023) & ~1023);
+    const int budget = SMEM_MAX - 1024 - C::BAR_REGION;
+    sch.na = 2 * (int)sch.a_buf_bytes <= 80 * 1024 ? 2 : 1;
+    sch.stages = (budget - sch.na * (int)sch.a_buf_bytes) / C::STAGE_BYTES;
+    if (sch.stages > C::MAX_STAGES) sch.stages = C::MAX_STAGES;
+    if (sch.stages < 2) return cudaErrorInvalidValue;
+    sch.row_tiles = (int)((a.row_end - a.row_begin + C::TILE_M - 1) / C::TILE_M);
+    sch.col_tiles = (int)((a.col_end - a.col_begin + TBN - 1) / TBN);
+    // a segment of ~16K columns per unit: the A panel load is amortised over
+    // many tiles and the units stay small enough to balance
+    int seg = env_int("FASTED_SEG_TILES", 16384 / TBN);
+    if (seg < 1) seg = 1;
+    sch.nsegs = (sch.col_tiles + seg - 1) / seg;
+    sch.units = (int64_t)sch.row_tiles * sch.nsegs;
+    const int smem =
+        sch.na * (int)sch.a_buf_bytes + sch.stages * C::STAGE_BYTES + C::BAR_REGION + 1024;
+    const int64_t slots = sm_count_current() / CG;
+    const int64_t work = sch.units < slots ? sch.units : slots;
+    if (work <= 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(work * CG));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, mxa, mxb, ma, mb, a, sch);
+}
+
+// Which tcgen05 join kernel a launch with this d_pad uses (env overrides:
+// FASTED_CTA_GROUP=1|2 forces the streaming kernel, FASTED_RESIDENT=0 and
+// FASTED_MC=0 disable the resident and multicast forms).
+enum { TC_STREAMING = 0, TC_RESIDENT = 1, TC_MULTICAST = 2 };
+static int tc_variant(int64_t d_pad) {
+    if (d_pad <= 256) return env_int("FASTED_RESIDENT", 1) != 0 ? TC_RESIDENT : TC_STREAMING;
+    if (env_int("FASTED_CTA_GROUP", 0) != 0 || env_int("FASTED_MC", 1) == 0) return TC_STREAMING;
+    return TC_MULTICAST;
+}
+
+const char* join_tc_kernel_name(int64_t d_pad) {
+    switch (tc_variant(d_pad)) {
+        case TC_RESIDENT: return "fasted::tc::join_tc_res_kernel";
+        case TC_MULTICAST: return "fasted::tc::join_tc_mc_kernel";
+        default: return "fasted::tc::join_tc_kernel";
+    }
+}
+
 int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     using namespace tc;
     if ((a.d_pad % 8) != 0 || (reinterpret_cast<uintptr_t>(X) & 15u) != 0) {
@@ -732,14 +1391,17 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         set_error("join_tc: n_pad exceeds TMA int32 coordinates");
         return FASTED_ERR_ARGUMENT;
     }
-    // Variant choice (profiles/round1/tune_*.txt, 1M-point shapes on B200):
-    // the CTA pair reaches ~88% tensor-pipe utilisation per clock and wins
-    // where the join is not power bound (d <= 256: 733 vs 632 TFLOPS at
-    // 1M x 128); at d = 960 the chip sits at the 1 kW cap and the single-CTA
-    // form delivers more TFLOPS per joule (0.81 vs 0.79-1.05 pJ/flop, the
-    // pair being run-to-run unstable).  FASTED_CTA_GROUP=1|2 overrides.
+    // Variant choice (profiles/round1/tune_*.txt, measured on B200):
+    //   d_pad <= 256: resident-A CTA pair (join_tc_res_kernel; 1M x 128:
+    //                 1013 TFLOPS vs 693 for the streaming pair);
+    //   d_pad >  256: B-multicast clusters of single-CTA MMAs
+    //                 (join_tc_mc_kernel; 1M x 960: 1374 vs 1226 single-CTA
+    //                 and ~980 for the CTA pair, which at the 1 kW cap runs
+    //                 its clock down to ~920 MHz; 60K x 512: 1373 vs 1307).
+    // FASTED_CTA_GROUP=1|2 forces the streaming kernel with that CTA group.
     const int cg_env = env_int("FASTED_CTA_GROUP", 0);
     const int cg = cg_env == 1 ? 1 : cg_env == 2 ? 2 : (a.d_pad <= 256 ? 2 : 1);
+    const int variant = tc_variant(a.d_pad);
     // per-call scratch (stream ordered): augment rows (two [n_pad][8] FP32,
     // eps-dependent) and the tensor-core Gram diagonal
     float4* aug = nullptr;
@@ -800,6 +1462,41 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) {
         cudaFreeAsync(aug, s);
         return cuda_status(e, "aug_prepare_kernel");
+    }
+    // Resident-A form for d_pad <= 256 (FASTED_RESIDENT=0 selects streaming);
+    // FASTED_RES_BN = 256 (default: two accumulators) or 128 (four; measured
+    // slower: 372 vs 283 ms at 1M x 128, the N=128 MMAs re-read A per 64 cycles).
+    if (variant == TC_RESIDENT) {
+        const int tbn = env_int("FASTED_RES_BN", 256) == 128 ? 128 : 256;
+        const int nb = tbn / cg, bbox = nb < 128 ? nb : 128;
+        CUtensorMap mxb, mbb;
+        st = encode_2d(&mxb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, X, a.d_pad, a.n_pad, a.d_pad * 2,
+                       BK, bbox, CU_TENSOR_MAP_SWIZZLE_128B);
+        if (st == FASTED_OK)
+            st = encode_2d(&mbb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, aug_b, AUG_K, a.n_pad,
+                           AUG_ROW_BYTES, AUG_K, bbox, CU_TENSOR_MAP_SWIZZLE_32B);
+        if (st != FASTED_OK) {
+            cudaFreeAsync(aug, s);
+            return st;
+        }
+        if (cg == 2)
+            e = tbn == 128 ? launch_res<2, 128>(mx, mxb, ma, mbb, a, s)
+                           : launch_res<2, 256>(mx, mxb, ma, mbb, a, s);
+        else
+            e = tbn == 128 ? launch_res<1, 128>(mx, mxb, ma, mbb, a, s)
+                           : launch_res<1, 256>(mx, mxb, ma, mbb, a, s);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        cudaFreeAsync(aug, s);
+        if (e != cudaSuccess) return cuda_status(e, "join_tc_res_kernel");
+        return FASTED_OK;
+    }
+    // Large d: B-multicast clusters unless FASTED_MC=0 (or a CTA group is forced).
+    if (variant == TC_MULTICAST) {
+        e = launch_mc(mx, ma, mb, a, s);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        cudaFreeAsync(aug, s);
+        if (e != cudaSuccess) return cuda_status(e, "join_tc_mc_kernel");
+        return FASTED_OK;
     }
     Sched sch;
     sch.diag = 0;

@@ -322,3 +322,64 @@ def test_sort_pairs_random_records(n_rows, maxc):
     assert np.array_equal(oi.cpu().numpy(), i[order])
     assert np.array_equal(oj.cpu().numpy(), j[order])
     assert np.array_equal(od.cpu().numpy(), d[order])
+
+
+def _tc_variant(hd, eps, rows=None, cols=None, **env):
+    """One tcgen05 join with kernel-selection env knobs (read per launch)."""
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update({k: str(v) for k, v in env.items()})
+    try:
+        dd = engine.upload(hd, 0)
+        es = float(np.float32(np.float32(eps) ** 2))
+        return engine.to_host(engine.join_device(dd, es, rows=rows, cols=cols))
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("n,d,eps,seg", [(3000, 128, 3.7, 64), (2999, 100, 3.3, 3),
+                                         (1100, 16, 1.0, 1), (2048, 256, 5.6, 2),
+                                         (777, 200, 5.0, 64), (5000, 64, 2.6, 7)])
+def test_resident_kernel_bit_identical_to_streaming(n, d, eps, seg):
+    """The resident-A kernel (d_pad <= 256) issues the streaming kernel's MMA
+    sequence per tile, so every record is bit-identical, for both CTA-group
+    forms, ragged segments and ragged row/column ranges."""
+    hd = F.to_half(F.generate_synthetic(n, d, seed=n + d))
+    for cg in (2, 1):
+        ref = _tc_variant(hd, eps, FASTED_RESIDENT=0, FASTED_CTA_GROUP=cg)
+        assert len(ref[0]) > n
+        for bn in (128, 256):
+            res = _tc_variant(hd, eps, FASTED_RESIDENT=1, FASTED_CTA_GROUP=cg,
+                              FASTED_SEG_TILES=seg, FASTED_RES_BN=bn)
+            for x, y in zip(ref, res):
+                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (cg, bn, n, d)
+    # a ragged row range x column range (the multi-GPU shard shape)
+    n_dev = -(-hd.n_padded // 128) * 128
+    rows, cols = (128, min(n_dev, 1152)), (256, n_dev)
+    ref = _tc_variant(hd, eps, rows, cols, FASTED_RESIDENT=0)
+    res = _tc_variant(hd, eps, rows, cols, FASTED_RESIDENT=1, FASTED_SEG_TILES=seg)
+    for x, y in zip(ref, res):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
+@pytest.mark.parametrize("n,d,eps", [(3000, 512, 8.6), (2999, 300, 6.8), (1100, 960, 12.0),
+                                     (777, 384, 7.7)])
+def test_multicast_kernel_bit_identical_to_single_cta(n, d, eps):
+    """The B-multicast cluster kernel (d_pad > 256) issues the single-CTA
+    kernel's M=128 MMA sequence per tile: identical bits, including odd
+    row-tile counts (a masked partner tile) and ragged shard ranges."""
+    hd = F.to_half(F.generate_synthetic(n, d, seed=n * 7 + d))
+    ref = _tc_variant(hd, eps, FASTED_CTA_GROUP=1)
+    mc = _tc_variant(hd, eps, FASTED_MC=1, FASTED_CTA_GROUP=0)
+    assert len(ref[0]) > n
+    for x, y in zip(ref, mc):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    n_dev = -(-hd.n_padded // 128) * 128
+    rows, cols = (128, min(n_dev, 1152)), (256, n_dev)
+    ref = _tc_variant(hd, eps, rows, cols, FASTED_CTA_GROUP=1)
+    mc = _tc_variant(hd, eps, rows, cols, FASTED_MC=1, FASTED_CTA_GROUP=0)
+    for x, y in zip(ref, mc):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
