@@ -389,19 +389,19 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
 
 // One epilogue warp's share of one finished accumulator of TBN columns:
 // warp (q, h) owns TMEM lanes 32q.. (rows row0 + 32q + lane) and accumulator
-// columns h*TBN/2 .. (h+1)*TBN/2 - 1 of buffer `buf`.  Drains its slice with
+// columns h*TBN/NSPLIT .. (h+1)*TBN/NSPLIT - 1 of buffer `buf`.  Drains its slice with
 // back-to-back tcgen05.ld and ONE wait (a tcgen05.ld queues behind the MMAs
 // already issued for the next tile, so waiting per chunk costs that queue
 // drain each time), hands the accumulator back to the MMA warp before any
 // math (the epilogue overlaps the next tiles' MMAs), then tests the signs.
-template <int CG, int TBN>
+template <int CG, int TBN, int NSPLIT = 2>
 __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, PairWriter& wr,
                                               uint32_t tmem_base, uint32_t tempty, int64_t row0,
                                               int64_t col0, int buf, uint32_t aph, int q, int h,
                                               int lane, bool leader, uint32_t tfull) {
-    constexpr int HALF = TBN / 2;
-    constexpr int NCH = HALF / 32;   // 32-column chunks per warp (4 or 2)
-    static_assert(NCH == 2 || NCH == 4, "TBN must be 128 or 256");
+    constexpr int HALF = TBN / NSPLIT;   // columns per warp
+    constexpr int NCH = HALF / 32;       // 32-column chunks per warp (4 or 2)
+    static_assert(NCH == 2 || NCH == 4, "a warp covers 64 or 128 columns");
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int64_t iw = row0 + q * 32;
     const int64_t i = iw + lane;
@@ -927,8 +927,8 @@ __device__ __forceinline__ void res_unit(const ResSched& s, int64_t u, int& rt, 
     ct1 = (int)((int64_t)s.col_tiles * (g + 1) / s.nsegs);
 }
 
-template <int CG, int TBN>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int CG, int TBN, int NEPI>
+__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI) * 32, 1)
 join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                    const __grid_constant__ CUtensorMap tmap_xb,
                    const __grid_constant__ CUtensorMap tmap_aug_a,
@@ -967,7 +967,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         }
         for (int b = 0; b < NACC; b++) {
             mbar_init(tfull_bar(b), 1);
-            mbar_init(tempty_bar(b), NUM_EPI_WARPS * CG);
+            mbar_init(tempty_bar(b), NEPI * CG);
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(afull_bar(b), 1);
@@ -1129,8 +1129,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         __syncwarp();
     } else {
         // ---------------- epilogue
-        const int q = warp & 3;
-        const int h = (warp - FIRST_EPI_WARP) >> 2;
+        const int q = warp & 3;                       // TMEM lane quarter
+        const int h = (warp - FIRST_EPI_WARP) >> 2;   // column group (NEPI / 4 of them)
         PairWriter wr;
         writer_init(wr);
         int lt = 0;
@@ -1140,7 +1140,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
             const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M + 128 * rank;
             for (int ct = ct0; ct < ct1; ct++, ++lt) {
                 const int buf = lt % NACC;
-                epilogue_tile<CG, TBN>(a, wr, tmem_base, tempty_bar(buf), row0,
+                epilogue_tile<CG, TBN, NEPI / 4>(a, wr, tmem_base, tempty_bar(buf), row0,
                                        a.col_begin + (int64_t)ct * TBN, buf,
                                        (uint32_t)(lt / NACC) & 1u, q, h, lane, leader,
                                        tfull_bar(buf));
@@ -1312,14 +1312,14 @@ static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const
 
 // Resident-A launch: shared memory split between the A buffer(s) and as many
 // B stages as fit.
-template <int CG, int TBN>
+template <int CG, int TBN, int NEPI>
 static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
                               const CUtensorMap& ma, const CUtensorMap& mb, const JoinArgs& a,
                               cudaStream_t s) {
     using namespace tc;
     using C = ResCfg<CG, TBN>;
     constexpr int SMEM_MAX = 227 * 1024;
-    auto kern = join_tc_res_kernel<CG, TBN>;
+    auto kern = join_tc_res_kernel<CG, TBN, NEPI>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1350,7 +1350,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     if (work <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * CG));
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1479,12 +1479,14 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
             cudaFreeAsync(aug, s);
             return st;
         }
+        // 8 epilogue warps (NEPI = 16, each draining 64 columns, measured
+        // slower at 1M x 128: 263 vs 248 ms, its 96-register cap spills)
         if (cg == 2)
-            e = tbn == 128 ? launch_res<2, 128>(mx, mxb, ma, mbb, a, s)
-                           : launch_res<2, 256>(mx, mxb, ma, mbb, a, s);
+            e = tbn == 128 ? launch_res<2, 128, 8>(mx, mxb, ma, mbb, a, s)
+                           : launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
         else
-            e = tbn == 128 ? launch_res<1, 128>(mx, mxb, ma, mbb, a, s)
-                           : launch_res<1, 256>(mx, mxb, ma, mbb, a, s);
+            e = tbn == 128 ? launch_res<1, 128, 8>(mx, mxb, ma, mbb, a, s)
+                           : launch_res<1, 256, 8>(mx, mxb, ma, mbb, a, s);
         if (e == cudaSuccess) e = cudaGetLastError();
         cudaFreeAsync(aug, s);
         if (e != cudaSuccess) return cuda_status(e, "join_tc_res_kernel");

@@ -61,6 +61,7 @@ for cfg in configs:
         os.environ.pop("FASTED_SEG_TILES", None)
     os.environ["FASTED_RES_BN"] = kv.get("BN", "256")
     os.environ["FASTED_MC"] = kv.get("MC", "1")
+    os.environ["FASTED_RES_EPI"] = kv.get("EPI", "16")
     flags = int(kv.get("F", "0"))
     engine.join_raw(dd, es, flags, (0, dd.n_dev), (0, dd.n_dev), rec, cap, cnt, stream.cuda_stream)
     torch.cuda.synchronize()

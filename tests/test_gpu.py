@@ -351,11 +351,11 @@ def test_resident_kernel_bit_identical_to_streaming(n, d, eps, seg):
     for cg in (2, 1):
         ref = _tc_variant(hd, eps, FASTED_RESIDENT=0, FASTED_CTA_GROUP=cg)
         assert len(ref[0]) > n
-        for bn in (128, 256):
+        for bn, epi in ((256, 8), (128, 8)):
             res = _tc_variant(hd, eps, FASTED_RESIDENT=1, FASTED_CTA_GROUP=cg,
-                              FASTED_SEG_TILES=seg, FASTED_RES_BN=bn)
+                              FASTED_SEG_TILES=seg, FASTED_RES_BN=bn, FASTED_RES_EPI=epi)
             for x, y in zip(ref, res):
-                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (cg, bn, n, d)
+                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (cg, bn, epi, n, d)
     # a ragged row range x column range (the multi-GPU shard shape)
     n_dev = -(-hd.n_padded // 128) * 128
     rows, cols = (128, min(n_dev, 1152)), (256, n_dev)
