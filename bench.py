@@ -292,13 +292,19 @@ def main():
     hd.device_cache.clear()
     torch.cuda.empty_cache()
     e2e_times = []
+    phases = []
     d2h = 0
     for s in range(args.e2e_steps + 1):
         barrier()
+        st = F.EngineStats()
         t0 = time.perf_counter()
-        rs = F.self_join(hd_host, eps, shard=(rank, world))
+        rs = F.self_join(hd_host, eps, stats_out=st, shard=(rank, world))
         torch.cuda.synchronize()
         dt = time.perf_counter() - t0
+        if s > 0:
+            phases.append({"h2d_s": st.stage_seconds, "join_kernels_s": st.kernel_wall_seconds,
+                           "sort_d2h_not_hidden_s": st.merge_seconds, "wall_s": dt,
+                           "engine": st.per_device})
         if world > 1:
             t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{device}")
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -363,7 +369,8 @@ def main():
                          "output_write_bound_ms": pairs_local * 12 / 6552e9 * 1e3},
             "e2e": {"value": flops / e2e_s / 1e12, "unit": "TFLOPS",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "seconds_per_step": e2e_s, "api": "paper_2508_21230_b200.self_join"},
+                    "seconds_per_step": e2e_s, "api": "paper_2508_21230_b200.self_join",
+                    "phases_per_step": phases},
             "accuracy_vs_fp64": acc,
             # per step: Gram-diagonal pre-pass, aug_prepare_kernel, the join
             "gpu_launches": 3 * args.steps,

@@ -62,13 +62,18 @@ def partition_rows(n_dev: int, parts: int) -> list:
     return [((R * g // parts) * BLOCK, (R * (g + 1) // parts) * BLOCK) for g in range(parts)]
 
 
-def hole_slack(device: int) -> int:
+def max_holes(device: int) -> int:
     """Upper bound on unused record slots: every warp may leave one partly
     filled chunk (64 warps per SM is the hardware maximum)."""
     import torch
 
     sms = torch.cuda.get_device_properties(device).multi_processor_count
     return sms * 64 * RECORD_CHUNK
+
+
+def hole_slack(device: int) -> int:
+    """Record slots added to a count (estimate) when sizing a buffer."""
+    return max_holes(device)
 
 
 def upload(hd, device: int) -> DeviceData:
@@ -132,6 +137,44 @@ def _estimate_capacity(dd: DeviceData, eps_sq: float, rows, cols, flags: int, st
     return int(tot * nblk / samples * 1.25) + 65536
 
 
+def _sort_records(dd: DeviceData, rec, slots: int, count: int, rows, stream, out=None,
+                  timed: bool = True):
+    """fasted_sort_pairs of `slots` raw records into canonical (i, j) SoA
+    order on the device.  `out` = preallocated (i, j, d) tensors of length
+    >= count, else allocated here.  Returns (i, j, d, sort_ms)."""
+    import torch
+
+    L = _lib.load()
+    dev = f"cuda:{dd.device}"
+    if out is None:
+        oi = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
+        oj = torch.empty_like(oi)
+        od = torch.empty(max(count, 1), dtype=torch.float32, device=dev)
+    else:
+        oi, oj, od = out
+    sort_ms = 0.0
+    if count:
+        ws_bytes = L.fasted_sort_workspace_bytes(rows[1] - rows[0], dd.n_dev)
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        tj = torch.empty(count, dtype=torch.int32, device=dev)
+        td = torch.empty(count, dtype=torch.float32, device=dev)
+        if timed:
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(stream)
+        _lib.check(L.fasted_sort_pairs(rec.data_ptr(), slots, rows[0], rows[1], dd.n_dev,
+                                       oi.data_ptr(), oj.data_ptr(), od.data_ptr(),
+                                       tj.data_ptr(), td.data_ptr(), ws.data_ptr(), ws_bytes,
+                                       stream.cuda_stream),
+                   "fasted_sort_pairs")
+        if timed:
+            s1.record(stream)
+            s1.synchronize()
+            sort_ms = s0.elapsed_time(s1)
+        del ws, tj, td   # stream-ordered reuse by the caching allocator is safe
+    return oi, oj, od, sort_ms
+
+
 def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool = False,
                 capacity: int | None = None, sort: bool = True) -> DeviceResult:
     """Run the join for rows x cols on dd.device; results stay on the device.
@@ -178,27 +221,7 @@ def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool
         rec = rec[:slots]
         if not sort:
             return DeviceResult(None, None, None, count, kernel_ms, 0.0, reruns, slots, rec)
-        oi = torch.empty(max(count, 1), dtype=torch.int32, device=dev)
-        oj = torch.empty_like(oi)
-        od = torch.empty(max(count, 1), dtype=torch.float32, device=dev)
-        sort_ms = 0.0
-        if count:
-            s0 = torch.cuda.Event(enable_timing=True)
-            s1 = torch.cuda.Event(enable_timing=True)
-            ws_bytes = L.fasted_sort_workspace_bytes(rows[1] - rows[0], dd.n_dev)
-            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-            tj = torch.empty(count, dtype=torch.int32, device=dev)
-            td = torch.empty(count, dtype=torch.float32, device=dev)
-            s0.record(stream)
-            _lib.check(L.fasted_sort_pairs(rec.data_ptr(), slots, rows[0], rows[1], dd.n_dev,
-                                           oi.data_ptr(), oj.data_ptr(), od.data_ptr(),
-                                           tj.data_ptr(), td.data_ptr(), ws.data_ptr(), ws_bytes,
-                                           sp),
-                       "fasted_sort_pairs")
-            s1.record(stream)
-            s1.synchronize()
-            sort_ms = s0.elapsed_time(s1)
-            del ws, tj, td
+        oi, oj, od, sort_ms = _sort_records(dd, rec, slots, count, rows, stream)
         del rec
     return DeviceResult(oi[:count], oj[:count], od[:count], count, kernel_ms, sort_ms, reruns,
                         slots)
@@ -225,10 +248,214 @@ def to_host(res: DeviceResult):
     return hi.numpy().view(np.uint32), hj.numpy().view(np.uint32), hd_.numpy()
 
 
+class HostPairs:
+    """Pinned host (i, j, dist_sq) arrays the pipeline appends into with
+    async D2H copies; grows (rarely: the capacity starts from the sampled
+    estimate) by reallocating and copying what is already there."""
+
+    def __init__(self, capacity: int):
+        self.cap = 0
+        self.n = 0
+        self.trace = None
+        self._alloc(max(int(capacity), 1))
+
+    def _alloc(self, cap):
+        import torch
+
+        new = [torch.empty(cap, dtype=torch.int32, pin_memory=True),
+               torch.empty(cap, dtype=torch.int32, pin_memory=True),
+               torch.empty(cap, dtype=torch.float32, pin_memory=True)]
+        if self.n:
+            for a, b in zip(new, self.t):
+                a[:self.n].copy_(b[:self.n])
+        self.t = new
+        self.cap = cap
+
+    def reserve(self, extra: int, sync_streams=()):
+        """Room for `extra` more pairs; waits for in-flight copies first if
+        the buffers must move."""
+        if self.n + extra <= self.cap:
+            return
+        for st in sync_streams:
+            st.synchronize()
+        self._alloc(max(self.n + extra, int(self.cap * 1.5)))
+
+    def append_async(self, i, j, d, count: int, stream):
+        """Enqueue the D2H of `count` pairs on `stream` (reserve() first)."""
+        import torch
+
+        if count:
+            with torch.cuda.stream(stream):
+                for dst, src in zip(self.t, (i, j, d)):
+                    dst[self.n:self.n + count].copy_(src[:count], non_blocking=True)
+        self.n += count
+
+    def arrays(self):
+        return (self.t[0][:self.n].numpy().view(np.uint32),
+                self.t[1][:self.n].numpy().view(np.uint32), self.t[2][:self.n].numpy())
+
+
+def plan_row_chunks(rows, est_records: int, budget_records: int, min_chunks: int = 1) -> list:
+    """Split a 128-aligned row range into contiguous chunks whose expected
+    record count fits `budget_records` (at least `min_chunks` when the range
+    allows)."""
+    r0, r1 = rows
+    nblk = (r1 - r0) // BLOCK
+    if nblk <= 0:
+        return [rows]
+    k = max(1, min_chunks, -(-int(est_records) // max(int(budget_records), 1)))
+    k = min(k, nblk)
+    return [(r0 + (nblk * c // k) * BLOCK, r0 + (nblk * (c + 1) // k) * BLOCK) for c in range(k)]
+
+
+# Chunking policy: a device streams its rows in chunks when the expected
+# output is large -- bounded device memory (records + sorted copies of one
+# chunk in flight, double buffered) and the sort + D2H of chunk c overlap
+# the join of chunk c + 1.
+PIPELINE_MIN_RECORDS = 1 << 22      # below this: one chunk (overlap not worth a launch)
+PIPELINE_CHUNKS = 4                 # chunks for mid-size outputs (overlap)
+BYTES_PER_RECORD_IN_FLIGHT = 2 * 16 + 2 * 12 + 8   # raw x2, sorted x2, sort scratch
+
+
+def _chunk_budget(device: int) -> int:
+    import torch
+
+    free, _ = torch.cuda.mem_get_info(device)
+    return max(1 << 20, int(free * 0.5) // BYTES_PER_RECORD_IN_FLIGHT)
+
+
+def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPairs,
+                budget_records: int | None = None):
+    """Row-chunked join -> sort -> D2H pipeline on one device, appending the
+    canonical (i, j)-ordered pairs of `rows` x all columns to `host`.
+
+    GPU stream order: join_0, join_1, sort_0, join_2, sort_1, ... so the
+    host read of chunk c's count never leaves the GPU idle; the D2H of chunk
+    c runs on a copy stream beside join c + 2.  Returns (kernel_ms, sort_ms,
+    reruns, chunks)."""
+    import torch
+
+    flags = _lib.JOIN_EXACT if exact else _lib.JOIN_TC
+    cols = (0, dd.n_dev)
+    dev = f"cuda:{dd.device}"
+    with torch.cuda.device(dd.device):
+        comp = torch.cuda.current_stream()
+        copy = torch.cuda.Stream(dd.device)
+        sp = comp.cuda_stream
+        key = (dd.n_dev, dd.d_pad, dd.n_logical, float(eps_sq), rows, cols, flags,
+               dd.values.data_ptr())
+        tr = {"estimate": 0.0, "reserve": 0.0, "wait_join": 0.0, "enqueue": 0.0, "drain": 0.0}
+        tc0 = time.perf_counter()
+        with _memo_lock:
+            est = _count_memo.get(key)
+        if est is None:
+            est = _estimate_capacity(dd, eps_sq, rows, cols, flags, sp)
+        budget = budget_records or _chunk_budget(dd.device)
+        min_chunks = PIPELINE_CHUNKS if est >= PIPELINE_MIN_RECORDS else 1
+        chunks = plan_row_chunks(rows, est, budget, min_chunks)
+        tr["estimate"] = time.perf_counter() - tc0
+        tc0 = time.perf_counter()
+        host.reserve(int(est * 1.05) + 1024)
+        tr["reserve"] += time.perf_counter() - tc0
+        slack = hole_slack(dd.device)
+        nrows = rows[1] - rows[0]
+
+        def cap_for(ch):
+            return int(est * (ch[1] - ch[0]) / max(nrows, 1) * 1.25) + slack
+
+        rec = [None, None]
+        cnt = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(2)]
+        ev_join = [None, None]
+        d2h_done = [None, None]
+        sorted_out = [None, None]
+        kernel_ms = 0.0
+        sort_ms = 0.0
+        reruns = 0
+        total = 0
+        tj = [None, None]
+        sort_ev = []
+
+        def launch_join(c):
+            b = c % 2
+            cap = cap_for(chunks[c])
+            if rec[b] is None or rec[b].shape[0] < cap:
+                rec[b] = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(comp)
+            join_raw(dd, eps_sq, flags, chunks[c], cols, rec[b], rec[b].shape[0], cnt[b], sp)
+            e1.record(comp)
+            tj[b] = (e0, e1)
+
+        launch_join(0)
+        for c in range(len(chunks)):
+            b = c % 2
+            if c + 1 < len(chunks):
+                launch_join(c + 1)
+            e0, e1 = tj[b]
+            tc0 = time.perf_counter()
+            e1.synchronize()
+            count, used = (int(v) for v in cnt[b].tolist())
+            tr["wait_join"] += time.perf_counter() - tc0
+            tc0 = time.perf_counter()
+            slots = used * RECORD_CHUNK
+            kernel_ms += e0.elapsed_time(e1)
+            if slots > rec[b].shape[0]:          # estimate too low: rerun this chunk
+                reruns += 1
+                comp.synchronize()
+                rec[b] = torch.empty((count + max_holes(dd.device), 4), dtype=torch.int32,
+                                     device=dev)
+                r0 = torch.cuda.Event(enable_timing=True)
+                r1 = torch.cuda.Event(enable_timing=True)
+                r0.record(comp)
+                join_raw(dd, eps_sq, flags, chunks[c], cols, rec[b], rec[b].shape[0], cnt[b], sp)
+                r1.record(comp)
+                r1.synchronize()
+                kernel_ms += r0.elapsed_time(r1)
+                count, used = (int(v) for v in cnt[b].tolist())
+                slots = used * RECORD_CHUNK
+            # sort_c lands behind join_{c+1} on the compute stream; its output
+            # buffers are reused only after their previous D2H finished
+            if d2h_done[b] is not None:
+                comp.wait_event(d2h_done[b])
+            out = sorted_out[b]
+            if out is None or out[0].shape[0] < max(count, 1):
+                n_alloc = max(count, 1)
+                out = (torch.empty(n_alloc, dtype=torch.int32, device=dev),
+                       torch.empty(n_alloc, dtype=torch.int32, device=dev),
+                       torch.empty(n_alloc, dtype=torch.float32, device=dev))
+                sorted_out[b] = out
+            s0 = torch.cuda.Event(enable_timing=True)
+            s1 = torch.cuda.Event(enable_timing=True)
+            s0.record(comp)
+            _sort_records(dd, rec[b], slots, count, chunks[c], comp, out=out, timed=False)
+            s1.record(comp)
+            tr["enqueue"] += time.perf_counter() - tc0
+            tc0 = time.perf_counter()
+            host.reserve(count, sync_streams=(copy,))
+            tr["reserve"] += time.perf_counter() - tc0
+            copy.wait_event(s1)
+            host.append_async(out[0], out[1], out[2], count, copy)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            d2h_done[b] = ev
+            total += count
+            sort_ev.append((s0, s1))
+        tc0 = time.perf_counter()
+        copy.synchronize()
+        comp.synchronize()
+        tr["drain"] = time.perf_counter() - tc0
+        sort_ms = sum(a.elapsed_time(b) for a, b in sort_ev)
+        host.trace = {k: round(v * 1e3, 2) for k, v in tr.items()}
+        with _memo_lock:
+            _count_memo[key] = total
+    return kernel_ms, sort_ms, reruns, len(chunks)
+
+
 @dataclass
 class JoinReport:
     kernel_seconds: float      # max over devices of the join kernel time
-    merge_seconds: float       # sort + D2H (reference: merge)
+    merge_seconds: float       # pipeline time not hidden behind the join (sort + D2H tail)
     stage_seconds: float       # H2D upload
     wall_seconds: float
     per_device: list
@@ -253,27 +480,34 @@ def self_join_devices(hd, eps_sq: float, devices, exact: bool = False, row_range
             dd = upload(hd, dev)
             torch.cuda.current_stream().synchronize()
             t_up = time.perf_counter() - t0
-            res = join_device(dd, eps_sq, rows=parts[g], cols=(0, dd.n_dev), exact=exact)
             t1 = time.perf_counter()
-            out = to_host(res)
-            t_d2h = time.perf_counter() - t1
-            return out, res, t_up, t_d2h
+            host = HostPairs(1)
+            kms, sms, reruns, nch = stream_join(dd, eps_sq, parts[g], exact, host)
+            t_all = time.perf_counter() - t1
+            return host, (kms, sms, reruns, nch), t_up, t_all
 
     if len(devices) == 1:
         results = [run(0)]
     else:
         with ThreadPoolExecutor(max_workers=len(devices)) as ex:
             results = list(ex.map(run, range(len(devices))))
-    i = np.concatenate([r[0][0] for r in results])
-    j = np.concatenate([r[0][1] for r in results])
-    d = np.concatenate([r[0][2] for r in results])
+    if len(results) == 1:
+        # the pinned host buffers ARE the result arrays (no concatenation copy)
+        i, j, d = results[0][0].arrays()
+    else:
+        arrs = [r[0].arrays() for r in results]
+        i = np.concatenate([a[0] for a in arrs])
+        j = np.concatenate([a[1] for a in arrs])
+        d = np.concatenate([a[2] for a in arrs])
     rep = JoinReport(
-        kernel_seconds=max(r[1].kernel_ms for r in results) / 1e3,
-        merge_seconds=max(r[1].sort_ms / 1e3 + r[3] for r in results),
+        kernel_seconds=max(r[1][0] for r in results) / 1e3,
+        merge_seconds=max(r[3] - r[1][0] / 1e3 for r in results),
         stage_seconds=max(r[2] for r in results),
         wall_seconds=time.perf_counter() - t_start,
-        per_device=[{"device": devices[g], "rows": parts[g], "pairs": results[g][1].count,
-                     "kernel_ms": results[g][1].kernel_ms, "sort_ms": results[g][1].sort_ms,
-                     "reruns": results[g][1].reruns} for g in range(len(devices))],
+        per_device=[{"device": devices[g], "rows": parts[g], "pairs": results[g][0].n,
+                     "kernel_ms": results[g][1][0], "sort_ms": results[g][1][1],
+                     "reruns": results[g][1][2], "chunks": results[g][1][3],
+                     "host_ms": getattr(results[g][0], "trace", None)}
+                    for g in range(len(devices))],
     )
     return i, j, d, rep

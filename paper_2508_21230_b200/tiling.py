@@ -21,7 +21,7 @@ compile-time property of the kernels (128x256 CTA tiles, 4-stage TMA ring).
 from __future__ import annotations
 
 import time
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -132,6 +132,7 @@ class EngineStats:
     kernel_wall_seconds: float = 0.0
     merge_seconds: float = 0.0
     wall_seconds: float = 0.0
+    per_device: list = field(default_factory=list)   # engine per-GPU report (chunks, host ms)
 
     @property
     def reuse_per_staged_element(self) -> float:
@@ -263,5 +264,6 @@ def self_join(hd: HalfDataset, epsilon: float, cfg: TileConfig | None = None,
         stats_out.add(st)
         stats_out.kernel_wall_seconds = rep.kernel_seconds
         stats_out.merge_seconds = rep.merge_seconds
+        stats_out.per_device = rep.per_device
         stats_out.wall_seconds = time.perf_counter() - t0
     return rs

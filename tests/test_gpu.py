@@ -383,3 +383,31 @@ def test_multicast_kernel_bit_identical_to_single_cta(n, d, eps):
     mc = _tc_variant(hd, eps, rows, cols, FASTED_MC=1, FASTED_CTA_GROUP=0)
     for x, y in zip(ref, mc):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
+@pytest.mark.parametrize("budget", [None, 20000, 3000])
+def test_stream_join_pipeline_matches_single_shot(budget, monkeypatch):
+    """The row-chunked join -> sort -> D2H pipeline (chunks sized from a
+    record budget, double-buffered, D2H on a copy stream) gives exactly the
+    single-launch result; a too-low estimate exercises the per-chunk rerun
+    and the pinned host buffer growth."""
+    hd = F.to_half(F.generate_synthetic(6000, 96, seed=11))
+    dd = engine.upload(hd, 0)
+    es = float(np.float32(np.float32(3.2) ** 2))
+    ref = engine.to_host(engine.join_device(dd, es))
+    engine._count_memo.clear()
+    if budget == 3000:
+        monkeypatch.setattr(engine, "_estimate_capacity", lambda *a, **k: 10)
+        monkeypatch.setattr(engine, "hole_slack", lambda dev: 0)
+    host = engine.HostPairs(1)
+    kms, sms, reruns, nch = engine.stream_join(dd, es, (0, dd.n_dev), False, host,
+                                               budget_records=budget)
+    got = host.arrays()
+    assert len(got[0]) == len(ref[0]) > 6000
+    for x, y in zip(ref, got):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    if budget == 20000:
+        assert nch > 1
+    if budget == 3000:
+        assert reruns >= 1
+    engine._count_memo.clear()
