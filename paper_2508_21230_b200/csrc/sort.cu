@@ -7,13 +7,17 @@
 //   1. row histogram (atomics, one per record)
 //   2. exclusive scan of the counts -> 64-bit row offsets
 //   3. scatter into row segments
-//   4. per-row ordering by j.  j values of a row are distinct, so a record's
-//      final slot is its rank among the row's j values:
+//   4. per-row ordering by j (j values of a row are distinct):
 //        - rows <= SHORT_MAX records: one warp per row, rank by comparison
 //          against the row staged in shared memory;
+//        - rows <= MID_MAX: one CTA per row, bitonic sort of (j << 32 | d)
+//          keys in shared memory (O(len log^2 len)) -- the high-selectivity
+//          case (S ~ 1000-4000 at 5M x 384);
 //        - longer rows: a bitmap of the row's j range is set, prefix
 //          popcounts give every record's rank in O(n_cols/32 + len).
-// All passes are bandwidth-trivial next to the join (|R| * 12 bytes).
+//          (This was the path for every row > 1024 before: at S = 4096 it
+//          cleared and scanned a 625 KB bitmap per row, 3.1 s for 2.56e9
+//          records; profiles/round1/c5_sweep_session2.jsonl.)
 #include "common.cuh"
 
 namespace fasted {
@@ -21,8 +25,10 @@ namespace fasted {
 constexpr int SCAN_THREADS = 1024;
 constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
-constexpr int SHORT_MAX = 1024;
+constexpr int SHORT_MAX = 256;
 constexpr int SHORT_WARPS = 4;
+constexpr int MID_MAX = 8192;                  // keys per CTA bitonic sort (64 KB smem)
+constexpr int MID_THREADS = 512;
 constexpr int LONG_BLOCKS = 32;
 constexpr int LONG_THREADS = 512;
 
@@ -33,6 +39,8 @@ struct SortWs {
     unsigned long long* bsum;    // n_scan_blocks + 1
     uint32_t* long_rows;         // n_rows
     uint32_t* long_count;        // 1
+    uint32_t* mid_rows;          // n_rows
+    uint32_t* mid_count;         // 1
     uint32_t* bitmap;            // LONG_BLOCKS * 2 * words
 };
 
@@ -55,6 +63,8 @@ static size_t carve(void* base, int64_t n_rows, int64_t n_cols, SortWs* ws) {
     w.bsum = reinterpret_cast<unsigned long long*>(take((nsb + 1) * 8));
     w.long_rows = reinterpret_cast<uint32_t*>(take(n_rows * 4));
     w.long_count = reinterpret_cast<uint32_t*>(take(4));
+    w.mid_rows = reinterpret_cast<uint32_t*>(take(n_rows * 4));
+    w.mid_count = reinterpret_cast<uint32_t*>(take(4));
     w.bitmap = reinterpret_cast<uint32_t*>(take((size_t)LONG_BLOCKS * 2 * words * 4));
     if (ws) *ws = w;
     return off;
@@ -178,7 +188,8 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
                   const unsigned long long* __restrict__ offsets, int64_t n_rows,
                   int64_t row_begin, uint32_t* __restrict__ oi, uint32_t* __restrict__ oj,
                   float* __restrict__ od, uint32_t* __restrict__ long_rows,
-                  uint32_t* __restrict__ long_count) {
+                  uint32_t* __restrict__ long_count, uint32_t* __restrict__ mid_rows,
+                  uint32_t* __restrict__ mid_count) {
     __shared__ uint32_t keys[SHORT_WARPS][SHORT_MAX];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t r = (int64_t)blockIdx.x * SHORT_WARPS + w; r < n_rows;
@@ -187,7 +198,10 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
         const uint32_t len = (uint32_t)(s1 - s0);
         if (len == 0) continue;
         if (len > SHORT_MAX) {
-            if (lane == 0) long_rows[atomicAdd(long_count, 1u)] = (uint32_t)r;
+            if (lane == 0) {
+                if (len <= MID_MAX) mid_rows[atomicAdd(mid_count, 1u)] = (uint32_t)r;
+                else long_rows[atomicAdd(long_count, 1u)] = (uint32_t)r;
+            }
             continue;
         }
         for (uint32_t e = lane; e < len; e += 32) keys[w][e] = tj[s0 + e];
@@ -201,6 +215,53 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
             od[s0 + rank] = td[s0 + e];
         }
         __syncwarp();
+    }
+}
+
+// One CTA per mid-length row: bitonic sort of 64-bit (j << 32 | d bits)
+// keys in shared memory (padding with all-ones keys to the next power of 2);
+// j is unique within a row, so key order is j order.
+__global__ void __launch_bounds__(MID_THREADS)
+mid_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
+                const unsigned long long* __restrict__ offsets, int64_t row_begin,
+                const uint32_t* __restrict__ mid_rows, const uint32_t* __restrict__ mid_count,
+                uint32_t* __restrict__ oi, uint32_t* __restrict__ oj, float* __restrict__ od) {
+    extern __shared__ unsigned long long key[];   // MID_MAX entries (dynamic: 64 KB)
+    const uint32_t nm = *mid_count;
+    for (uint32_t mi = blockIdx.x; mi < nm; mi += gridDim.x) {
+        const int64_t r = mid_rows[mi];
+        const unsigned long long s0 = offsets[r];
+        const uint32_t len = (uint32_t)(offsets[r + 1] - s0);
+        uint32_t n = 1;
+        while (n < len) n <<= 1;
+        for (uint32_t e = threadIdx.x; e < n; e += MID_THREADS)
+            key[e] = e < len ? ((unsigned long long)tj[s0 + e] << 32) |
+                                   (unsigned long long)__float_as_uint(td[s0 + e])
+                             : ~0ull;
+        __syncthreads();
+        for (uint32_t k = 2; k <= n; k <<= 1) {
+            for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+                for (uint32_t t = threadIdx.x; t < (n >> 1); t += MID_THREADS) {
+                    const uint32_t i = ((t & ~(jj - 1)) << 1) | (t & (jj - 1));
+                    const uint32_t l = i + jj;
+                    const unsigned long long a = key[i], b = key[l];
+                    const bool up = (i & k) == 0;
+                    if ((a > b) == up) {
+                        key[i] = b;
+                        key[l] = a;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        const uint32_t row1 = (uint32_t)(row_begin + r + 1);
+        for (uint32_t e = threadIdx.x; e < len; e += MID_THREADS) {
+            const unsigned long long v = key[e];
+            oi[s0 + e] = row1;
+            oj[s0 + e] = (uint32_t)(v >> 32);
+            od[s0 + e] = __uint_as_float((uint32_t)v);
+        }
+        __syncthreads();
     }
 }
 
@@ -293,6 +354,7 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
     cudaMemsetAsync(ws.counts, 0, n_rows * 4, s);
     cudaMemsetAsync(ws.cursor, 0, n_rows * 4, s);
     cudaMemsetAsync(ws.long_count, 0, 4, s);
+    cudaMemsetAsync(ws.mid_count, 0, 4, s);
     const int sms = sm_count_current();
     const unsigned rec_grid = (unsigned)((count + 255) / 256 < (uint64_t)sms * 16
                                              ? (count + 255) / 256
@@ -314,8 +376,21 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
     short_rows_kernel<<<(unsigned)(sgrid < (int64_t)sms * 64 ? sgrid : (int64_t)sms * 64),
                         SHORT_WARPS * 32, 0, s>>>(tmp_j, tmp_d, ws.offsets, n_rows, row_begin,
                                                   out_i, out_j, out_d, ws.long_rows,
-                                                  ws.long_count);
+                                                  ws.long_count, ws.mid_rows, ws.mid_count);
     FASTED_CHECK_LAUNCH("short_rows_kernel");
+    static bool mid_attr = false;
+    if (!mid_attr) {
+        cudaError_t e = cudaFuncSetAttribute(mid_rows_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             MID_MAX * 8);
+        if (e != cudaSuccess) return cuda_status(e, "mid_rows_kernel attribute");
+        mid_attr = true;
+    }
+    mid_rows_kernel<<<(unsigned)(sms * 3), MID_THREADS, MID_MAX * 8, s>>>(tmp_j, tmp_d, ws.offsets,
+                                                                row_begin, ws.mid_rows,
+                                                                ws.mid_count, out_i, out_j,
+                                                                out_d);
+    FASTED_CHECK_LAUNCH("mid_rows_kernel");
     long_rows_kernel<<<LONG_BLOCKS, LONG_THREADS, 0, s>>>(tmp_j, tmp_d, ws.offsets, row_begin,
                                                           n_cols, ws.long_rows, ws.long_count,
                                                           ws.bitmap, out_i, out_j, out_d);

@@ -294,14 +294,16 @@ def test_c3_full_size_tc_vs_exact(oracle):
     assert es > 0
 
 
-@pytest.mark.parametrize("n_rows,maxc", [(5000, 150), (20000, 100), (3000, 2000)])
+@pytest.mark.parametrize("n_rows,maxc", [(5000, 150), (20000, 100), (3000, 2000),
+                                         (1500, 9000), (200, 20000)])
 def test_sort_pairs_random_records(n_rows, maxc):
-    """fasted_sort_pairs on shuffled records with unused slots (i == 0),
-    short rows (warp rank path) and long rows (> 1024: bitmap path)."""
+    """fasted_sort_pairs on shuffled records with unused slots (i == 0):
+    short rows (<= 256: warp rank path), mid rows (<= 8192: CTA bitonic
+    sort) and long rows (> 8192: bitmap path)."""
     rng = np.random.default_rng(n_rows)
     counts = rng.integers(0, maxc, n_rows)
     i = np.repeat(np.arange(1, n_rows + 1), counts).astype(np.int32)
-    n_cols = n_rows * 2
+    n_cols = max(n_rows * 2, 3 * maxc)
     j = np.concatenate([rng.choice(n_cols, c, replace=False) + 1 for c in counts]).astype(np.int32)
     d = rng.random(len(i)).astype(np.float32)
     rec = np.zeros((len(i) + 777, 4), np.int32)
