@@ -1,0 +1,100 @@
+"""Epsilon calibration on the GPU.
+
+The reference calibrates epsilon by bisection on the FP64 distances of a
+1024-point sample (analysis.py:237-300, mirrored in analysis.calibrate_epsilon):
+its selectivity estimate sees only 1024 x 1024 distances, so the achieved S
+can miss the target badly (C1: target 64, achieved 72.2).  This bisection
+instead counts, with the product kernel in count-only mode (no records, no
+sort), every neighbour of `sample_blocks` random 128-row blocks over ALL n
+columns: at 1M points and 16 blocks that is 2048 x 1M distances per
+estimate, ~1 ms each at d = 960.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _lib, engine
+from .analysis import CalibrationResult
+from .errors import ArgumentError, CalibrationError
+
+
+def _count_fn(hd, sample_blocks: int, seed: int, device):
+    import torch
+
+    if device is None:
+        device = torch.cuda.current_device()
+    dd = engine.upload(hd, device)
+    nblk = dd.n_dev // engine.BLOCK
+    valid_blk = -(-hd.n_logical // engine.BLOCK)
+    k = min(sample_blocks, valid_blk)
+    rng = np.random.default_rng(seed)
+    blocks = np.sort(rng.choice(valid_blk, size=k, replace=False))
+    m = int(sum(min(engine.BLOCK, hd.n_logical - b * engine.BLOCK) for b in blocks))
+    cnt = torch.zeros(2, dtype=torch.int64, device=f"cuda:{device}")
+    stream = torch.cuda.current_stream(device).cuda_stream
+
+    def count(eps_sq: float) -> int:
+        tot = 0
+        for b in blocks:
+            r0 = int(b) * engine.BLOCK
+            engine.join_raw(dd, eps_sq, _lib.JOIN_TC | _lib.JOIN_COUNT,
+                            (r0, min(r0 + engine.BLOCK, dd.n_dev)), (0, dd.n_dev), None, 0,
+                            cnt, stream)
+            tot += int(cnt[0].item())
+        return tot
+
+    max_norm = float(np.max(hd.norms[:hd.n_logical])) if hd.n_logical else 0.0
+    del nblk
+    return count, m, max_norm
+
+
+def calibrate_epsilon_device(hd, target_s: float, tol: float = 0.01, sample_blocks: int = 16,
+                             seed: int = 0, device: int | None = None,
+                             max_iter: int = 60) -> CalibrationResult:
+    """Bisection on epsilon until the selectivity of `sample_blocks` random
+    row blocks against every column is within tol * target_s of target_s.
+
+    Returns the reference's CalibrationResult (epsilon, estimated
+    selectivity, iterations, sample size = rows counted).  Raises the
+    reference's errors for unreachable targets."""
+    if target_s <= 0:
+        raise ArgumentError(f"target_s must be > 0, got {target_s}")
+    if sample_blocks < 1:
+        raise ArgumentError(f"sample_blocks must be >= 1, got {sample_blocks}")
+    n = int(hd.n_logical)
+    if target_s > n - 1:
+        raise CalibrationError(
+            f"target selectivity {target_s} unreachable: at most n - 1 = {n - 1} neighbors exist")
+    count, m, max_norm = _count_fn(hd, sample_blocks, seed, device)
+
+    def estimate(eps: float) -> float:
+        es = float(np.float32(np.float32(eps) * np.float32(eps)))
+        return (count(es) - m) / m
+
+    band = tol * target_s
+    lo, est_lo = 0.0, estimate(0.0)
+    if abs(est_lo - target_s) <= band:
+        return CalibrationResult(lo, est_lo, 0, m)
+    if est_lo > target_s:
+        raise CalibrationError(f"initial interval does not bracket target {target_s}: "
+                               f"selectivity is already {est_lo:.4g} at epsilon 0")
+    # ||x - y|| <= ||x|| + ||y||: every pair is within 2 max ||x|| (+ slack)
+    hi = 2.0 * math.sqrt(max_norm) * 1.001 + 1e-6
+    est_hi = estimate(hi)
+    if est_hi < target_s - band:
+        raise CalibrationError(f"initial interval does not bracket target {target_s}: "
+                               f"achieved selectivity range is [{est_lo:.4g}, {est_hi:.4g}]")
+    mid, est_mid = hi, est_hi
+    for it in range(1, max_iter + 1):
+        mid = 0.5 * (lo + hi)
+        est_mid = estimate(mid)
+        if abs(est_mid - target_s) <= band:
+            return CalibrationResult(mid, est_mid, it, m)
+        if est_mid < target_s:
+            lo = mid
+        else:
+            hi = mid
+    return CalibrationResult(mid, est_mid, max_iter, m)

@@ -413,3 +413,21 @@ def test_stream_join_pipeline_matches_single_shot(budget, monkeypatch):
     if budget == 3000:
         assert reruns >= 1
     engine._count_memo.clear()
+
+
+def test_device_calibration_hits_target_on_full_data(golden_meta):
+    """GPU count-only bisection (16 row blocks x all columns): the full
+    join at the calibrated epsilon lands within a few percent of the target
+    selectivity -- the reference's 1024-point FP64 sample gave 72.2 for a
+    target of 64 on C1."""
+    c1 = golden_meta["C1"]
+    hd = F.to_half(F.generate_synthetic(c1["n"], c1["d"], seed=c1["seed"]))
+    cal = F.calibrate_epsilon_device(hd, 64.0, tol=0.01, sample_blocks=16)
+    assert abs(cal.estimated_selectivity - 64.0) <= 0.64
+    assert cal.sample_size == 16 * 128
+    rs = F.self_join(hd, cal.epsilon)
+    s_full = F.selectivity(rs)
+    print("device calibration:", cal, "full-data S:", s_full)
+    assert abs(s_full - 64.0) / 64.0 < 0.04
+    with pytest.raises(F.CalibrationError):
+        F.calibrate_epsilon_device(hd, float(c1["n"]))

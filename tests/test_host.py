@@ -230,3 +230,15 @@ def test_error_hierarchy():
     assert issubclass(F.RangeError, ValueError) and issubclass(F.RangeError, F.MPJoinError)
     assert issubclass(F.AccumulatorOverflow, ArithmeticError)
     assert issubclass(F.DeviceError, RuntimeError)
+
+
+def test_device_calibration_validates_before_device_use():
+    import paper_2508_21230_b200 as F
+
+    hd = F.HalfDataset(4, 16, np.zeros((128, 16), np.float16), np.zeros(128, np.float32))
+    with pytest.raises(F.ArgumentError):
+        F.calibrate_epsilon_device(hd, 0.0)
+    with pytest.raises(F.ArgumentError):
+        F.calibrate_epsilon_device(hd, 1.0, sample_blocks=0)
+    with pytest.raises(F.CalibrationError):
+        F.calibrate_epsilon_device(hd, 10.0)
