@@ -56,6 +56,11 @@ enum {
     FASTED_JOIN_TC = 0,     /* tcgen05/TMEM fused kernel (the product path)          */
     FASTED_JOIN_EXACT = 1,  /* CUDA-core FFMA.RZ kernel, bit-exact with the reference */
     FASTED_JOIN_COUNT = 2,  /* OR-able: count only, write no records                 */
+    /* OR-able, tcgen05 only, needs row range == column range: compute only the
+     * tiles on or above the diagonal and write every off-diagonal pair in both
+     * orientations, (i, j) and (j, i), with the same dist_sq -- half the MMA
+     * work for the same record set (and the set is exactly symmetric). */
+    FASTED_JOIN_SYMMETRIC = 4,
     /* Diagnostics for power/throughput attribution (results are NOT valid): */
     FASTED_JOIN_DIAG_NOEPI = 256,    /* tcgen05 kernel: skip the epilogue entirely     */
     FASTED_JOIN_DIAG_NOMMA = 512,    /* tcgen05 kernel: skip the MMAs (TMA + epilogue) */

@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfasted.so")
 
 OK, ERR_ARGUMENT, ERR_RANGE, ERR_CAPACITY, ERR_CUDA, ERR_UNSUPPORTED = 0, 2, 3, 4, 5, 6
-JOIN_TC, JOIN_EXACT, JOIN_COUNT = 0, 1, 2
+JOIN_TC, JOIN_EXACT, JOIN_COUNT, JOIN_SYMMETRIC = 0, 1, 2, 4
 
 # Every symbol include/fasted.h declares (tests check the .so exports them).
 EXPORTS = (

@@ -110,6 +110,12 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
         set_error("fasted_join: 16-byte aligned record buffer required unless FASTED_JOIN_COUNT");
         return FASTED_ERR_ARGUMENT;
     }
+    const bool symmetric = (flags & FASTED_JOIN_SYMMETRIC) != 0;
+    if (symmetric && (kind == FASTED_JOIN_EXACT || row_begin != col_begin || row_end != col_end)) {
+        set_error("fasted_join: FASTED_JOIN_SYMMETRIC needs the tcgen05 kernel and row range == "
+                  "column range");
+        return FASTED_ERR_ARGUMENT;
+    }
     cudaStream_t s = as_stream(stream);
     cudaError_t e = cudaMemsetAsync(count, 0, 2 * sizeof(unsigned long long), s);
     if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(count)");
@@ -125,6 +131,7 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     a.col_end = col_end;
     a.eps_sq = eps_sq;
     a.count_only = count_only ? 1 : 0;
+    a.symmetric = symmetric ? 1 : 0;
     a.diag_flags = flags & (FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA |
                             FASTED_JOIN_DIAG_LOADONLY | FASTED_JOIN_DIAG_NOSLOW |
                             FASTED_JOIN_DIAG_MASKOR);

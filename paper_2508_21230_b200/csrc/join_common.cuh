@@ -12,6 +12,7 @@ struct JoinArgs {
     float eps_sq;
     int count_only;
     int diag_flags;                    // FASTED_JOIN_DIAG_* (experiments only)
+    int symmetric;                     // FASTED_JOIN_SYMMETRIC: upper tiles, mirrored records
     uint4* out;                        // records {i, j, dist_sq bits, 0}
     unsigned long long capacity;       // record slots available in out
     unsigned long long* count;         // [0] exact pair total, [1] chunks taken

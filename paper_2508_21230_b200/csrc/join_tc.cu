@@ -309,6 +309,16 @@ __device__ __forceinline__ void tile_coords(const Sched& s, int64_t t, int& rt, 
     rt = (int)(g * s.group + r % rows_in);
 }
 
+// FASTED_JOIN_SYMMETRIC: a tile wholly below the diagonal (every column index
+// smaller than every row index) is skipped alike by the producer, the MMA
+// warp and the epilogue; its pairs arrive as the mirrored records of the
+// tile across the diagonal.  (Loops that count processed tiles undo their
+// increment on a skip.)
+__device__ __forceinline__ bool sym_skip(const JoinArgs& a, int64_t row0, int64_t col0,
+                                         int tile_cols) {
+    return a.symmetric && col0 + tile_cols - 1 < row0;
+}
+
 // r[e] for a warp-uniform runtime e without local memory: a 5-level
 // select tree (31 SEL), so the rare path never spills the chunk.
 __device__ __forceinline__ uint32_t pick32(const uint32_t (&r)[32], uint32_t e) {
@@ -342,7 +352,7 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
         const uint32_t b = __ballot_sync(0xffffffffu, self);
         if (b) writer_append(wr, a, b, self, (uint32_t)(i + 1), (uint32_t)(i + 1), 0.0f);
     }
-    if (!(a.diag_flags & FASTED_JOIN_DIAG_MASKOR)) {
+    if (!(a.diag_flags & FASTED_JOIN_DIAG_MASKOR) || a.symmetric) {
         // Per-lane form (default): each lane builds its own hit mask (sign
         // bits clear), drops its self column and columns past n_logical, and
         // the warp appends one record per hitting lane per round -- usually
@@ -354,6 +364,12 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
         const int64_t valid = a.n_logical - jb;
         if (valid < 32) lm &= valid <= 0 ? 0u : ((1u << (uint32_t)valid) - 1u);
         if (i >= jb && i < jb + 32) lm &= ~(1u << (uint32_t)(i - jb));
+        if (a.symmetric) {
+            // upper triangle only (j > i); the mirrored record covers (j, i)
+            const int64_t off = i - jb;   // columns jb .. i are not above the diagonal
+            if (off >= 31) lm = 0u;
+            else if (off >= 0) lm &= ~((2u << (uint32_t)off) - 1u);
+        }
         if (!row_ok) lm = 0u;
         while (true) {
             const bool mine = lm != 0u;
@@ -364,6 +380,8 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
             const uint32_t v = pick32(r, e);
             const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
             writer_append(wr, a, b, mine, (uint32_t)(i + 1), (uint32_t)(jb + e + 1), d2);
+            if (a.symmetric)
+                writer_append(wr, a, b, mine, (uint32_t)(jb + e + 1), (uint32_t)(i + 1), d2);
         }
         return;
     }
@@ -521,6 +539,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 tile_coords(sch, t, rt, ct);
                 const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M;
                 const int64_t col0 = DIAG ? row0 : a.col_begin + (int64_t)ct * BN;
+                if (sym_skip(a, row0, col0, BN)) continue;
                 // which 128-row halves exist (a half past the range end is skipped:
                 // its rows/columns are masked in the epilogue)
                 const bool a_hi = row0 + 128 < a.row_end;
@@ -589,6 +608,15 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             uint32_t ph = 0;
             int lt = 0;
             for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
+                if (a.symmetric) {
+                    int rt, ct;
+                    tile_coords(sch, t, rt, ct);
+                    if (sym_skip(a, a.row_begin + (int64_t)rt * C::TILE_M,
+                                 a.col_begin + (int64_t)ct * BN, BN)) {
+                        --lt;
+                        continue;
+                    }
+                }
                 const int buf = lt & 1;
                 const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
                 mbar_wait(tempty_bar(buf), aph ^ 1u);
@@ -638,6 +666,10 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             tile_coords(sch, t, rt, ct);
             const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M + 128 * rank;
             const int64_t col0 = a.col_begin + (int64_t)ct * BN;
+            if (sym_skip(a, a.row_begin + (int64_t)rt * C::TILE_M, col0, BN)) {
+                --lt;
+                continue;
+            }
             const int buf = lt & 1;
             const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
             if constexpr (DIAG) {
@@ -777,6 +809,9 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
             int rt, ct;
             tile_coords(sch, t, rt, ct);
+            if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM, a.col_begin + (int64_t)ct * BN,
+                         BN))
+                continue;
             const int row0 = (int)(a.row_begin + ((int64_t)rt * 2 + cr) * BM);
             const int colh = (int)(a.col_begin + (int64_t)ct * BN + 128 * cr);
             for (int kb = 0; kb < sch.nkb + 1; kb++) {
@@ -810,6 +845,15 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         uint32_t ph = 0;
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
+            if (a.symmetric) {
+                int rt, ct;
+                tile_coords(sch, t, rt, ct);
+                if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM,
+                             a.col_begin + (int64_t)ct * BN, BN)) {
+                    --lt;
+                    continue;
+                }
+            }
             const int buf = lt & 1;
             mbar_wait(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u);
             tc_fence_after();
@@ -854,6 +898,10 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             tile_coords(sch, t, rt, ct);
             const int64_t row0 = a.row_begin + ((int64_t)rt * 2 + cr) * BM;
             const int64_t col0 = a.col_begin + (int64_t)ct * BN;
+            if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM, col0, BN)) {
+                --lt;
+                continue;
+            }
             const int buf = lt & 1;
             epilogue_tile<1, BN>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf,
                                  (uint32_t)(lt >> 1) & 1u, q, h, lane, true, tfull_bar(buf));
@@ -925,6 +973,20 @@ __device__ __forceinline__ void res_unit(const ResSched& s, int64_t u, int& rt, 
     rt = (int)(u - g * s.row_tiles);
     ct0 = (int)((int64_t)s.col_tiles * g / s.nsegs);
     ct1 = (int)((int64_t)s.col_tiles * (g + 1) / s.nsegs);
+}
+
+// res_unit with FASTED_JOIN_SYMMETRIC applied: the unit's column tiles start
+// at the first one reaching the diagonal (an emptied unit still loads its A
+// panel and commits it, so every role walks the same unit sequence).
+template <int TILE_M, int TBN>
+__device__ __forceinline__ void res_unit_sym(const ResSched& s, const JoinArgs& a, int64_t u,
+                                             int& rt, int& ct0, int& ct1) {
+    res_unit(s, u, rt, ct0, ct1);
+    if (a.symmetric) {
+        const int64_t num = (int64_t)rt * TILE_M - TBN + 1;   // ct * TBN + TBN - 1 >= rt * TILE_M
+        const int ct_min = num <= 0 ? 0 : (int)((num + TBN - 1) / TBN);
+        if (ct0 < ct_min) ct0 = ct_min < ct1 ? ct_min : ct1;
+    }
 }
 
 template <int CG, int TBN, int NEPI>
@@ -1012,7 +1074,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
             int ua = 0;
             for (int64_t u = unit0; u < sch.units; u += ustep, ++ua) {
                 int rt, ct0, ct1;
-                res_unit(sch, u, rt, ct0, ct1);
+                res_unit_sym<C::TILE_M, TBN>(sch, a, u, rt, ct0, ct1);
                 const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M;
                 const bool a_hi = row0 + 128 < a.row_end;
                 const int my_a = (int)(row0 + 128 * rank);
@@ -1083,7 +1145,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
             int lt = 0, ua = 0;
             for (int64_t u = unit0; u < sch.units; u += ustep, ++ua) {
                 int rt, ct0, ct1;
-                res_unit(sch, u, rt, ct0, ct1);
+                res_unit_sym<C::TILE_M, TBN>(sch, a, u, rt, ct0, ct1);
                 const int ab = ua % sch.na;
                 mbar_wait(afull_bar(ab), (uint32_t)(ua / sch.na) & 1u);
                 tc_fence_after();
@@ -1136,7 +1198,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         int lt = 0;
         for (int64_t u = unit0; u < sch.units; u += ustep) {
             int rt, ct0, ct1;
-            res_unit(sch, u, rt, ct0, ct1);
+            res_unit_sym<C::TILE_M, TBN>(sch, a, u, rt, ct0, ct1);
             const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M + 128 * rank;
             for (int ct = ct0; ct < ct1; ct++, ++lt) {
                 const int buf = lt % NACC;
@@ -1441,6 +1503,7 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         ad.count_only = 1;
         ad.capacity = 0;
         ad.diag_flags = 0;
+        ad.symmetric = 0;
         ad.gram_diag = gram;
         Sched sd;
         sd.row_tiles = (int)(a.n_pad / BM);

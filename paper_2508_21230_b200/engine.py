@@ -138,7 +138,7 @@ def _estimate_capacity(dd: DeviceData, eps_sq: float, rows, cols, flags: int, st
 
 
 def _sort_records(dd: DeviceData, rec, slots: int, count: int, rows, stream, out=None,
-                  timed: bool = True):
+                  timed: bool = True, tmp=None, ws=None):
     """fasted_sort_pairs of `slots` raw records into canonical (i, j) SoA
     order on the device.  `out` = preallocated (i, j, d) tensors of length
     >= count, else allocated here.  Returns (i, j, d, sort_ms)."""
@@ -155,16 +155,20 @@ def _sort_records(dd: DeviceData, rec, slots: int, count: int, rows, stream, out
     sort_ms = 0.0
     if count:
         ws_bytes = L.fasted_sort_workspace_bytes(rows[1] - rows[0], dd.n_dev)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-        tj = torch.empty(count, dtype=torch.int32, device=dev)
-        td = torch.empty(count, dtype=torch.float32, device=dev)
+        if ws is None or ws.numel() < ws_bytes:
+            ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        if tmp is None or tmp[0].shape[0] < count:
+            tj = torch.empty(count, dtype=torch.int32, device=dev)
+            td = torch.empty(count, dtype=torch.float32, device=dev)
+        else:
+            tj, td = tmp
         if timed:
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             s0.record(stream)
         _lib.check(L.fasted_sort_pairs(rec.data_ptr(), slots, rows[0], rows[1], dd.n_dev,
                                        oi.data_ptr(), oj.data_ptr(), od.data_ptr(),
-                                       tj.data_ptr(), td.data_ptr(), ws.data_ptr(), ws_bytes,
+                                       tj.data_ptr(), td.data_ptr(), ws.data_ptr(), ws.numel(),
                                        stream.cuda_stream),
                    "fasted_sort_pairs")
         if timed:
@@ -325,18 +329,28 @@ def _chunk_budget(device: int) -> int:
 
 
 def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPairs,
-                budget_records: int | None = None):
+                budget_records: int | None = None, symmetric: bool = False):
     """Row-chunked join -> sort -> D2H pipeline on one device, appending the
     canonical (i, j)-ordered pairs of `rows` x all columns to `host`.
 
-    GPU stream order: join_0, join_1, sort_0, join_2, sort_1, ... so the
-    host read of chunk c's count never leaves the GPU idle; the D2H of chunk
-    c runs on a copy stream beside join c + 2.  Returns (kernel_ms, sort_ms,
-    reruns, chunks)."""
+    GPU stream order: join_0, join_1, sort_0, join_2, sort_1, ... : chunk
+    c's count comes back on a side stream as soon as join c ends (while join
+    c+1 runs), so sort c and join c+2 are queued before the GPU needs them;
+    the D2H of chunk c runs on a copy stream beside join c + 2.  All buffers
+    are allocated before the first launch.  Returns (kernel_ms, sort_ms,
+    reruns, chunks).
+
+    symmetric=True (tcgen05 only, rows = all rows): FASTED_JOIN_SYMMETRIC --
+    only the tiles on or above the diagonal, each off-diagonal pair written
+    in both orientations.  Mirrored records belong to any row, so the whole
+    range is one chunk (one sort); if that does not fit the memory budget the
+    full-matrix join runs instead (same pair set)."""
     import torch
 
     flags = _lib.JOIN_EXACT if exact else _lib.JOIN_TC
     cols = (0, dd.n_dev)
+    if symmetric and (exact or tuple(rows) != cols):
+        raise ArgumentError("symmetric join needs the tcgen05 path over all rows")
     dev = f"cuda:{dd.device}"
     with torch.cuda.device(dd.device):
         comp = torch.cuda.current_stream()
@@ -353,6 +367,12 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
         budget = budget_records or _chunk_budget(dd.device)
         min_chunks = PIPELINE_CHUNKS if est >= PIPELINE_MIN_RECORDS else 1
         chunks = plan_row_chunks(rows, est, budget, min_chunks)
+        if symmetric:
+            if est <= budget:
+                chunks = [tuple(rows)]
+                flags |= _lib.JOIN_SYMMETRIC
+            else:
+                symmetric = False
         tr["estimate"] = time.perf_counter() - tc0
         tc0 = time.perf_counter()
         host.reserve(int(est * 1.05) + 1024)
@@ -363,39 +383,77 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
         def cap_for(ch):
             return int(est * (ch[1] - ch[0]) / max(nrows, 1) * 1.25) + slack
 
-        rec = [None, None]
+        # Every buffer of the pipeline is allocated here, before the first
+        # launch: a cudaMalloc issued while a join runs blocks the host until
+        # the GPU drains (measured: 0.5 s GPU-idle gaps per call when the
+        # sort outputs were allocated mid-pipeline).
+        nbuf = 2 if len(chunks) > 1 else 1
+        cap_max = max(cap_for(ch) for ch in chunks)
+        out_cap = max(cap_max - slack, 1024)
+        L = _lib.load()
+        rec = [torch.empty((cap_max, 4), dtype=torch.int32, device=dev) for _ in range(nbuf)]
+        if nbuf == 1:
+            rec.append(rec[0])
+        sorted_out = [(torch.empty(out_cap, dtype=torch.int32, device=dev),
+                       torch.empty(out_cap, dtype=torch.int32, device=dev),
+                       torch.empty(out_cap, dtype=torch.float32, device=dev))
+                      for _ in range(nbuf)]
+        if nbuf == 1:
+            sorted_out.append(sorted_out[0])
+        sort_tmp = (torch.empty(out_cap, dtype=torch.int32, device=dev),
+                    torch.empty(out_cap, dtype=torch.float32, device=dev))
+        max_rows = max(ch[1] - ch[0] for ch in chunks)
+        sort_ws = torch.empty(max(L.fasted_sort_workspace_bytes(max_rows, dd.n_dev), 1),
+                              dtype=torch.uint8, device=dev)
         cnt = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in range(2)]
-        ev_join = [None, None]
+        # counts come back on a side stream that waits only for ITS join: a
+        # plain .tolist() would queue behind join c+1 on the compute stream
+        # and leave the GPU idle until the host enqueued more work
+        aux = torch.cuda.Stream(dd.device)
+        cnt_h = torch.zeros((2, 2), dtype=torch.int64, pin_memory=True)
+        cnt_ev = [None, None]
         d2h_done = [None, None]
-        sorted_out = [None, None]
         kernel_ms = 0.0
         sort_ms = 0.0
         reruns = 0
         total = 0
         tj = [None, None]
         sort_ev = []
+        join_ev = []
+
+        host_t0 = time.perf_counter()
+        marks = []
+
+        def mark(what):
+            marks.append((what, round((time.perf_counter() - host_t0) * 1e3, 2)))
 
         def launch_join(c):
             b = c % 2
-            cap = cap_for(chunks[c])
-            if rec[b] is None or rec[b].shape[0] < cap:
-                rec[b] = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+            mark("launch%d" % c)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(comp)
             join_raw(dd, eps_sq, flags, chunks[c], cols, rec[b], rec[b].shape[0], cnt[b], sp)
             e1.record(comp)
             tj[b] = (e0, e1)
+            join_ev.append((c, e0, e1))
+            aux.wait_event(e1)
+            with torch.cuda.stream(aux):
+                cnt_h[b].copy_(cnt[b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(aux)
+            cnt_ev[b] = ev
+            mark("launched%d" % c)
 
         launch_join(0)
+        if len(chunks) > 1:
+            launch_join(1)
         for c in range(len(chunks)):
             b = c % 2
-            if c + 1 < len(chunks):
-                launch_join(c + 1)
             e0, e1 = tj[b]
             tc0 = time.perf_counter()
-            e1.synchronize()
-            count, used = (int(v) for v in cnt[b].tolist())
+            cnt_ev[b].synchronize()
+            count, used = (int(v) for v in cnt_h[b].tolist())
             tr["wait_join"] += time.perf_counter() - tc0
             tc0 = time.perf_counter()
             slots = used * RECORD_CHUNK
@@ -405,6 +463,8 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
                 comp.synchronize()
                 rec[b] = torch.empty((count + max_holes(dd.device), 4), dtype=torch.int32,
                                      device=dev)
+                if nbuf == 1:
+                    rec[1 - b] = rec[b]
                 r0 = torch.cuda.Event(enable_timing=True)
                 r1 = torch.cuda.Event(enable_timing=True)
                 r0.record(comp)
@@ -419,18 +479,23 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
             if d2h_done[b] is not None:
                 comp.wait_event(d2h_done[b])
             out = sorted_out[b]
-            if out is None or out[0].shape[0] < max(count, 1):
+            if out[0].shape[0] < max(count, 1):      # estimate too low (rare)
+                comp.synchronize()
                 n_alloc = max(count, 1)
                 out = (torch.empty(n_alloc, dtype=torch.int32, device=dev),
                        torch.empty(n_alloc, dtype=torch.int32, device=dev),
                        torch.empty(n_alloc, dtype=torch.float32, device=dev))
                 sorted_out[b] = out
+                if nbuf == 1:
+                    sorted_out[1 - b] = out
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             s0.record(comp)
-            _sort_records(dd, rec[b], slots, count, chunks[c], comp, out=out, timed=False)
+            _sort_records(dd, rec[b], slots, count, chunks[c], comp, out=out, timed=False,
+                          tmp=sort_tmp, ws=sort_ws)
             s1.record(comp)
             tr["enqueue"] += time.perf_counter() - tc0
+            mark("sorted%d" % c)
             tc0 = time.perf_counter()
             host.reserve(count, sync_streams=(copy,))
             tr["reserve"] += time.perf_counter() - tc0
@@ -439,7 +504,11 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
             ev = torch.cuda.Event()
             ev.record(copy)
             d2h_done[b] = ev
+            mark("d2h%d" % c)
             total += count
+            # join c+2 reuses chunk c's record buffer: queued after sort c
+            if c + 2 < len(chunks):
+                launch_join(c + 2)
             sort_ev.append((s0, s1))
         tc0 = time.perf_counter()
         copy.synchronize()
@@ -447,6 +516,14 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
         tr["drain"] = time.perf_counter() - tc0
         sort_ms = sum(a.elapsed_time(b) for a, b in sort_ev)
         host.trace = {k: round(v * 1e3, 2) for k, v in tr.items()}
+        host.trace["host_marks"] = marks
+        if join_ev:   # GPU timeline (ms from the first join start): gaps = GPU idle
+            t0e = join_ev[0][1]
+            host.trace["gpu_timeline"] = (
+                [("join%d" % c, round(t0e.elapsed_time(a), 2), round(t0e.elapsed_time(b), 2))
+                 for c, a, b in join_ev] +
+                [("sort%d" % c, round(t0e.elapsed_time(a), 2), round(t0e.elapsed_time(b), 2))
+                 for c, (a, b) in enumerate(sort_ev)])
         with _memo_lock:
             _count_memo[key] = total
     return kernel_ms, sort_ms, reruns, len(chunks)
@@ -461,7 +538,8 @@ class JoinReport:
     per_device: list
 
 
-def self_join_devices(hd, eps_sq: float, devices, exact: bool = False, row_range=None):
+def self_join_devices(hd, eps_sq: float, devices, exact: bool = False, row_range=None,
+                      symmetric: bool = False):
     """Row-block partition of `row_range` (default: all rows) across
     `devices`; returns (i, j, d, JoinReport)."""
     import torch
@@ -482,7 +560,8 @@ def self_join_devices(hd, eps_sq: float, devices, exact: bool = False, row_range
             t_up = time.perf_counter() - t0
             t1 = time.perf_counter()
             host = HostPairs(1)
-            kms, sms, reruns, nch = stream_join(dd, eps_sq, parts[g], exact, host)
+            kms, sms, reruns, nch = stream_join(dd, eps_sq, parts[g], exact, host,
+                                                symmetric=symmetric)
             t_all = time.perf_counter() - t1
             return host, (kms, sms, reruns, nch), t_up, t_all
 

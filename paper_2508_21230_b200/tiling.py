@@ -216,7 +216,7 @@ def compute_block_tile(hd: HalfDataset, coord: TileCoord, eps_sq, cfg: TileConfi
 
 def self_join(hd: HalfDataset, epsilon: float, cfg: TileConfig | None = None,
               stats_out: EngineStats | None = None, *, mode: str = "tc",
-              devices=None, shard=None) -> ResultSet:
+              devices=None, shard=None, symmetric: bool = False) -> ResultSet:
     """Full epsilon self-join: every ordered pair with distance <= epsilon
     (tiling.py:288-359), on one or more B200s.
 
@@ -225,7 +225,10 @@ def self_join(hd: HalfDataset, epsilon: float, cfg: TileConfig | None = None,
     no collectives); default the current device.  shard=(rank, world): one
     process per GPU -- this call returns only the pairs whose i lies in the
     rank's contiguous row-block range; concatenating ranks in order gives
-    the full, sorted ResultSet.
+    the full, sorted ResultSet.  symmetric=True (tcgen05, one device, no
+    shard): compute only the tiles on or above the diagonal and mirror each
+    pair -- half the MMA work; every (i, j) then carries exactly the dist_sq
+    of (j, i), so the result is exactly symmetric.
     """
     if cfg is None:
         cfg = TileConfig()
@@ -237,6 +240,8 @@ def self_join(hd: HalfDataset, epsilon: float, cfg: TileConfig | None = None,
     eps_sq = _eps_sq(epsilon)
     if devices is None:
         devices = _default_devices()
+    if symmetric and (mode != "tc" or len(list(devices)) != 1 or shard is not None):
+        raise ArgumentError("symmetric=True needs mode 'tc' on a single device without shard")
     row_range = None
     if shard is not None:
         rank, world = shard
@@ -246,7 +251,8 @@ def self_join(hd: HalfDataset, epsilon: float, cfg: TileConfig | None = None,
         row_range = engine.partition_rows(n_dev, world)[rank]
     t0 = time.perf_counter()
     i, j, d, rep = engine.self_join_devices(hd, float(eps_sq), list(devices),
-                                            exact=(mode == "exact"), row_range=row_range)
+                                            exact=(mode == "exact"), row_range=row_range,
+                                            symmetric=symmetric)
     rs = ResultSet(i, j, d, n=int(hd.n_logical), epsilon=float(epsilon))
     if stats_out is not None:
         n_dev = -(-hd.n_padded // 128) * 128

@@ -431,3 +431,51 @@ def test_device_calibration_hits_target_on_full_data(golden_meta):
     assert abs(s_full - 64.0) / 64.0 < 0.04
     with pytest.raises(F.CalibrationError):
         F.calibrate_epsilon_device(hd, float(c1["n"]))
+
+
+@pytest.mark.parametrize("n,d,eps", [(3000, 64, 2.6), (2999, 128, 3.9), (1500, 300, 6.8),
+                                     (2100, 960, 12.0)])
+@pytest.mark.parametrize("env", [{}, {"FASTED_CTA_GROUP": "1"}, {"FASTED_CTA_GROUP": "2",
+                                                                  "FASTED_RESIDENT": "0"}])
+def test_symmetric_join(oracle, n, d, eps, env):
+    """FASTED_JOIN_SYMMETRIC (upper tiles + mirrored records) on every kernel
+    form: the pair set is exactly symmetric with equal dist_sq both ways,
+    equals the full join outside the 1e-3 band, and passes the band contract
+    against the reference oracle."""
+    hd = F.to_half(F.generate_synthetic(n, d, seed=n + 3 * d))
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        full = F.self_join(hd, eps)
+        sym = F.self_join(hd, eps, symmetric=True)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    assert len(sym) > n
+    # exact symmetry: (i, j, d) present <=> (j, i, d) present
+    key = (sym.i.astype(np.uint64) << np.uint64(32)) | sym.j.astype(np.uint64)
+    tkey = (sym.j.astype(np.uint64) << np.uint64(32)) | sym.i.astype(np.uint64)
+    o1, o2 = np.argsort(key), np.argsort(tkey)
+    assert np.array_equal(key[o1], tkey[o2])
+    assert np.array_equal(sym.dist_sq[o1].view(np.uint32), sym.dist_sq[o2].view(np.uint32))
+    assert np.all(sym.i[sym.i == sym.j] > 0) and np.all(sym.dist_sq[sym.i == sym.j] == 0)
+    es = float(oracle.eps_sq_of(eps))
+    rep = F.band_compare(sym.i, sym.j, sym.dist_sq, full.i, full.j, full.dist_sq, es,
+                         lambda i, j: oracle.pair_d2(hd.values, hd.norms, i, j))
+    assert rep.missing_out_of_band == 0 and rep.extra_out_of_band == 0, rep
+    oi, oj, od = oracle.join(hd.values, hd.norms, n, eps)
+    rep = _band_ok(oracle, hd, sym, oi, oj, od, eps)
+    assert rep.ok, rep
+
+
+def test_symmetric_rejects_shards_and_exact():
+    hd = F.to_half(F.generate_synthetic(500, 32, seed=1))
+    with pytest.raises(F.ArgumentError):
+        F.self_join(hd, 1.0, symmetric=True, devices=[0, 0])
+    with pytest.raises(F.ArgumentError):
+        F.self_join(hd, 1.0, symmetric=True, mode="exact")
+    with pytest.raises(F.ArgumentError):
+        F.self_join(hd, 1.0, symmetric=True, shard=(0, 2))
