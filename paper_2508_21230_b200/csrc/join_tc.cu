@@ -141,6 +141,35 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
+// Pure-spin variant (no suspend hint): FASTED_JOIN_DIAG_SPIN A/B experiments.
+__device__ __forceinline__ bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+__device__ __forceinline__ void mbar_wait2(uint32_t bar, uint32_t parity, bool spin) {
+    if (!spin) {
+        mbar_wait(bar, parity);
+        return;
+    }
+    if (mbar_test_wait(bar, parity)) return;
+    const uint64_t t0 = global_timer();
+    uint32_t spins = 0;
+    while (!mbar_test_wait(bar, parity)) {
+        if (++spins == 256u) {
+            spins = 0;
+            if (global_timer() - t0 > 20000000000ull) __trap();
+        }
+    }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -430,7 +459,7 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, PairWriter& wr,
     int nchunks = left <= 0 ? 0 : (left >= HALF ? NCH : (int)(left / 32));
     if (row0 >= a.row_end || (a.diag_flags & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
     const uint32_t tcol = tmem_base + lane_base + (uint32_t)(buf * TBN + h * HALF);
-    mbar_wait(tfull, aph);
+    mbar_wait2(tfull, aph, (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
     tc_fence_after();
     uint32_t r0[32], r1[32], r2[32], r3[32];
     if (nchunks > 0) tmem_ld32(tcol, r0);
@@ -452,6 +481,7 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, PairWriter& wr,
         else mbar_arrive_remote(tempty, 0);
     }
     const int64_t jb = col0 + h * HALF;
+    if (a.diag_flags & FASTED_JOIN_DIAG_LOADONLY) return;
     if (nchunks > 0) epi_chunk(a, wr, r0, jb, i, iw, row_ok);
     if (nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok);
     if (NCH > 2 && nchunks > 2) epi_chunk(a, wr, r2, jb + 64, i, iw, row_ok);
@@ -855,7 +885,8 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 }
             }
             const int buf = lt & 1;
-            mbar_wait(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u);
+            mbar_wait2(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u,
+                       (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
             tc_fence_after();
             const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
             for (int kb = 0; kb < sch.nkb + 1; kb++) {
@@ -1152,7 +1183,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                 const uint32_t abuf = sAb + (uint32_t)ab * sch.a_buf_bytes;
                 for (int ct = ct0; ct < ct1; ct++, ++lt) {
                     const int buf = lt % NACC;
-                    mbar_wait(tempty_bar(buf), ((uint32_t)(lt / NACC) & 1u) ^ 1u);
+                    mbar_wait2(tempty_bar(buf), ((uint32_t)(lt / NACC) & 1u) ^ 1u,
+                               (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
                     tc_fence_after();
                     const uint32_t dtm = tmem_base + (uint32_t)(buf * TBN);
                     for (int kb = 0; kb < sch.nkb; kb++) {

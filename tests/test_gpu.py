@@ -479,3 +479,45 @@ def test_symmetric_rejects_shards_and_exact():
         F.self_join(hd, 1.0, symmetric=True, mode="exact")
     with pytest.raises(F.ArgumentError):
         F.self_join(hd, 1.0, symmetric=True, shard=(0, 2))
+
+
+def test_c2_full_size_band_parity_all_schedules(oracle):
+    """C2 (60K x 512) in full: the product path (B-multicast kernel), its
+    symmetric schedule and a 3-way row sharding all meet the band contract
+    against the bit-exact kernel (itself pinned to the reference), and the
+    shards concatenate to the single-device result."""
+    n, d, eps = 60000, 512, 8.48414709018062
+    hd = F.to_half(F.generate_synthetic(n, d, seed=12345))
+    ref = F.self_join(hd, eps, mode="exact")
+    tc = F.self_join(hd, eps)
+    rep = _band_ok(oracle, hd, tc, ref.i, ref.j, ref.dist_sq, eps)
+    print("C2 band report:", rep)
+    assert rep.ok, rep
+    sym = F.self_join(hd, eps, symmetric=True)
+    rep = _band_ok(oracle, hd, sym, ref.i, ref.j, ref.dist_sq, eps)
+    assert rep.ok, rep
+    parts = [F.self_join(hd, eps, shard=(r, 3)) for r in range(3)]
+    assert np.array_equal(np.concatenate([p.i for p in parts]), tc.i)
+    assert np.array_equal(np.concatenate([p.j for p in parts]), tc.j)
+    assert np.array_equal(np.concatenate([p.dist_sq for p in parts]).view(np.uint32),
+                          tc.dist_sq.view(np.uint32))
+
+
+@pytest.mark.slow
+def test_c4_full_size_tc_vs_exact(oracle):
+    """The headline configuration in full (1M x 960, the bench's eps): the
+    tcgen05 pair set against the bit-exact kernel's (= the reference's
+    arithmetic) under the band contract; the exact kernel against the C
+    oracle on sampled row blocks at the full column range."""
+    n, d, eps = 1000000, 960, 11.700486640655093
+    hd = F.to_half(F.generate_synthetic(n, d, seed=12345))
+    ref = F.self_join(hd, eps, mode="exact")
+    rs = F.self_join(hd, eps)
+    rep = _band_ok(oracle, hd, rs, ref.i, ref.j, ref.dist_sq, eps)
+    print("C4 band report:", rep)
+    assert rep.ok, rep
+    for rb in (0, 7812):
+        oi, oj, od = oracle.join(hd.values, hd.norms, n, eps, rows=(rb * 128, rb * 128 + 128))
+        sel = (ref.i > rb * 128) & (ref.i <= rb * 128 + 128)
+        assert np.array_equal(oi, ref.i[sel]) and np.array_equal(oj, ref.j[sel])
+        assert np.array_equal(od.view(np.uint32), ref.dist_sq[sel].view(np.uint32))
