@@ -66,7 +66,7 @@ enum {
     FASTED_JOIN_DIAG_NOMMA = 512,    /* tcgen05 kernel: skip the MMAs (TMA + epilogue) */
     FASTED_JOIN_DIAG_LOADONLY = 1024, /* epilogue: TMEM loads only, no math           */
     FASTED_JOIN_DIAG_NOSLOW = 2048,  /* epilogue: sign test only, never write         */
-    FASTED_JOIN_DIAG_MASKOR = 4096,  /* epilogue: column-scan (REDUX) hit search      */
+    /* 4096: retired (column-scan hit search) */
     FASTED_JOIN_DIAG_SPIN = 8192     /* accumulator waits spin (no suspend hint)      */
 };
 

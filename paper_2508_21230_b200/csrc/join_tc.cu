@@ -174,6 +174,14 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 
+// Relaxed local arrive for the accumulator release: the TMEM reads are
+// ordered by tcgen05.fence::before_thread_sync; a (default) release arrive
+// would also order this thread's earlier pair-record stores, i.e. wait for
+// them, on the MMA's critical path.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint32_t bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 // Arrive on the barrier at the same offset in CTA `rank` of the cluster.
 // Relaxed: the only ordering needed (TMEM reads before the MMA reuses the
 // accumulator) comes from tcgen05.fence::before_thread_sync; a release
@@ -330,6 +338,19 @@ __device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
 
 __device__ __forceinline__ void tile_coords(const Sched& s, int64_t t, int& rt, int& ct) {
     const int64_t per_group = (int64_t)s.group * s.col_tiles;
+    if (s.total <= 0xffffffffLL && per_group <= 0xffffffffLL) {
+        // 32-bit divisions (every grid up to 2^32 tiles; 64-bit division is
+        // a ~70-instruction software routine on the per-tile path)
+        const uint32_t pg = (uint32_t)per_group, tt = (uint32_t)t;
+        const uint32_t g = tt / pg;
+        const uint32_t r = tt - g * pg;
+        const uint32_t left = (uint32_t)s.row_tiles - g * (uint32_t)s.group;
+        const uint32_t rows_in = left < (uint32_t)s.group ? left : (uint32_t)s.group;
+        const uint32_t c = r / rows_in;
+        ct = (int)c;
+        rt = (int)(g * (uint32_t)s.group + (r - c * rows_in));
+        return;
+    }
     const int64_t g = t / per_group;
     const int64_t r = t - g * per_group;
     const int64_t left = (int64_t)s.row_tiles - g * s.group;
@@ -381,12 +402,12 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
         const uint32_t b = __ballot_sync(0xffffffffu, self);
         if (b) writer_append(wr, a, b, self, (uint32_t)(i + 1), (uint32_t)(i + 1), 0.0f);
     }
-    if (!(a.diag_flags & FASTED_JOIN_DIAG_MASKOR) || a.symmetric) {
-        // Per-lane form (default): each lane builds its own hit mask (sign
-        // bits clear), drops its self column and columns past n_logical, and
-        // the warp appends one record per hitting lane per round -- usually
-        // one round, since hits are sparse (measured: the column-scan form
-        // below cost 22% of the 1M x 128 join in REDUX latency).
+    {
+        // Per lane: build the hit mask (sign bits clear), drop the self
+        // column and columns past n_logical; the warp appends one record per
+        // hitting lane per round -- usually one round, hits being sparse.
+        // (A column-scan form -- 32 REDUX.AND per chunk -- measured no faster
+        // at 1M x 128 and doubled the rare-path code; it was removed.)
         uint32_t lm = 0;
 #pragma unroll
         for (int e = 0; e < 32; e++) lm |= ((~r[e]) >> 31) << e;
@@ -412,25 +433,6 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
             if (a.symmetric)
                 writer_append(wr, a, b, mine, (uint32_t)(jb + e + 1), (uint32_t)(i + 1), d2);
         }
-        return;
-    }
-    // Column-scan form (FASTED_JOIN_DIAG_MASKOR, kept for A/B measurement):
-    // a column holds a hit iff some lane's D word has the sign bit clear,
-    // found with 32 REDUX.AND on the uniform datapath.
-    uint32_t cm = 0;
-#pragma unroll
-    for (int e = 0; e < 32; e++)
-        cm |= ((~__reduce_and_sync(0xffffffffu, r[e]) >> 31) & 1u) << e;
-    while (cm) {
-        const uint32_t e = __ffs(cm) - 1;
-        cm &= cm - 1;
-        const uint32_t v = pick32(r, e);
-        const int64_t j = jb + e;
-        const bool ok = ((int)v >= 0) && (i != j) && row_ok && j < a.n_logical;
-        const uint32_t b = __ballot_sync(0xffffffffu, ok);
-        if (b == 0u) continue;
-        const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
-        writer_append(wr, a, b, ok, (uint32_t)(i + 1), (uint32_t)(j + 1), d2);
     }
 }
 
@@ -477,7 +479,7 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, PairWriter& wr,
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
-        if (CG == 1 || leader) mbar_arrive(tempty);
+        if (CG == 1 || leader) mbar_arrive_relaxed(tempty);
         else mbar_arrive_remote(tempty, 0);
     }
     const int64_t jb = col0 + h * HALF;

@@ -18,12 +18,14 @@ wl = sys.argv[1]
 rows = int(sys.argv[2]) if len(sys.argv) > 2 else 148 * 256 * 2
 flags = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 name, n, d, eps = WORKLOADS[wl]
+if len(sys.argv) > 4:
+    eps = float(sys.argv[4])
 hd = F.to_half(F.generate_synthetic(n, d, seed=SEED))
 dd = engine.upload(hd, 0)
 es = float(np.float32(np.float32(eps) ** 2))
 r = (0, min(rows, dd.n_dev))
 # explicit capacity: no count-only sizing launches before the measured one
-first = engine.join_device(dd, es, rows=r, sort=False, capacity=(r[1] - r[0]) * 4096)
+first = engine.join_device(dd, es, rows=r, sort=False, capacity=(r[1] - r[0]) * 8192)
 cap = first.count + engine.hole_slack(0)
 rec = torch.empty((cap, 4), dtype=torch.int32, device="cuda")
 cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
