@@ -64,12 +64,16 @@ constexpr int FIRST_EPI_WARP = 2;
 constexpr int THREADS = (FIRST_EPI_WARP + NUM_EPI_WARPS) * 32;
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int BAR_BYTES = 256;
+// Pair-record staging (StagedWriter): per epilogue warp 2 buffers of STAGE
+// records of 16 bytes.
+constexpr int WSTAGE = 64;
+constexpr int WSTAGE_BYTES = NUM_EPI_WARPS * 2 * WSTAGE * 16;   // 16 KB
 
 template <int CG>
 struct Cfg {
     static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of B
     static constexpr int STAGES = CG == 2 ? 6 : 4;
-    static constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + BAR_BYTES + 1024;
+    static constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + BAR_BYTES + WSTAGE_BYTES + 1024;
     static constexpr int TILE_M = BM * CG;                // rows per tile
     // Instruction descriptors: D=F32 (bits 4-5 = 1); A/B format at bits
     // 7-9 / 10-12 (F16 = 0, TF32 = 2); both K-major; N>>3 at 17-22; M>>4 at
@@ -386,7 +390,8 @@ __device__ __forceinline__ uint32_t pick32(const uint32_t (&r)[32], uint32_t e) 
 
 // Epilogue of one 32-column chunk (columns jb.., row i = this lane).
 // r[e] = D_{i, jb+e} = (eps^2 - d2) / 2 as FP32 bits.
-__device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, const uint32_t (&r)[32],
+template <typename W>
+__device__ __forceinline__ void epi_chunk(const JoinArgs& a, W& wr, const uint32_t (&r)[32],
                                           int64_t jb, int64_t i, int64_t iw, bool row_ok) {
     // common path: is any D >= 0 (sign bit clear)?  16 three-input ANDs.
     uint32_t acc = 0xffffffffu;
@@ -443,8 +448,8 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, PairWriter& wr, con
 // already issued for the next tile, so waiting per chunk costs that queue
 // drain each time), hands the accumulator back to the MMA warp before any
 // math (the epilogue overlaps the next tiles' MMAs), then tests the signs.
-template <int CG, int TBN, int NSPLIT = 2>
-__device__ __forceinline__ void epilogue_tile(const JoinArgs& a, PairWriter& wr,
+template <int CG, int TBN, int NSPLIT = 2, typename W>
+__device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
                                               uint32_t tmem_base, uint32_t tempty, int64_t row0,
                                               int64_t col0, int buf, uint32_t aph, int q, int h,
                                               int lane, bool leader, uint32_t tfull) {
@@ -690,8 +695,8 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         const int q = warp & 3;          // TMEM lane quarter this warp may access
         const int h = (warp - FIRST_EPI_WARP) >> 2;   // column half of the accumulator
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-        PairWriter wr;
-        writer_init(wr);
+        StagedWriter<WSTAGE> wr;
+        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WSTAGE * 16);
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -775,7 +780,8 @@ __device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
 }
 
 constexpr int MC_STAGES = 4;
-constexpr int MC_SMEM_BYTES = MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + 1024;
+constexpr int MC_SMEM_BYTES =
+    MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + WSTAGE_BYTES + 1024;
 
 __global__ void __launch_bounds__(THREADS, 1)
 join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
@@ -923,8 +929,8 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         // ---------------- epilogue
         const int q = warp & 3;
         const int h = (warp - FIRST_EPI_WARP) >> 2;
-        PairWriter wr;
-        writer_init(wr);
+        StagedWriter<WSTAGE> wr;
+        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WSTAGE * 16);
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -981,6 +987,8 @@ struct ResSched {
     uint32_t a_buf_bytes;     // one A buffer: nkb k-blocks + augment rows, 1024-aligned
     int64_t units;            // row_tiles * nsegs
 };
+
+constexpr int RES_WSTAGE = 32;   // records per staging buffer (resident kernel: tight smem)
 
 template <int CG, int TBN>
 struct ResCfg {
@@ -1227,8 +1235,9 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         // ---------------- epilogue
         const int q = warp & 3;                       // TMEM lane quarter
         const int h = (warp - FIRST_EPI_WARP) >> 2;   // column group (NEPI / 4 of them)
-        PairWriter wr;
-        writer_init(wr);
+        StagedWriter<RES_WSTAGE> wr;
+        writer_init(wr, bars + C::BAR_REGION +
+                            (uint32_t)(warp - FIRST_EPI_WARP) * 2 * RES_WSTAGE * 16);
         int lt = 0;
         for (int64_t u = unit0; u < sch.units; u += ustep) {
             int rt, ct0, ct1;
@@ -1426,7 +1435,8 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     ResSched sch;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.a_buf_bytes = (uint32_t)((sch.nkb * A_BYTES + BM * AUG_ROW_BYTES + 1023) & ~1023);
-    const int budget = SMEM_MAX - 1024 - C::BAR_REGION;
+    const int wstage = NEPI * 2 * RES_WSTAGE * 16;
+    const int budget = SMEM_MAX - 1024 - C::BAR_REGION - wstage;
     sch.na = 2 * (int)sch.a_buf_bytes <= 80 * 1024 ? 2 : 1;
     sch.stages = (budget - sch.na * (int)sch.a_buf_bytes) / C::STAGE_BYTES;
     if (sch.stages > C::MAX_STAGES) sch.stages = C::MAX_STAGES;
@@ -1439,8 +1449,8 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     if (seg < 1) seg = 1;
     sch.nsegs = (sch.col_tiles + seg - 1) / seg;
     sch.units = (int64_t)sch.row_tiles * sch.nsegs;
-    const int smem =
-        sch.na * (int)sch.a_buf_bytes + sch.stages * C::STAGE_BYTES + C::BAR_REGION + 1024;
+    const int smem = sch.na * (int)sch.a_buf_bytes + sch.stages * C::STAGE_BYTES +
+                     C::BAR_REGION + wstage + 1024;
     const int64_t slots = sm_count_current() / CG;
     const int64_t work = sch.units < slots ? sch.units : slots;
     if (work <= 0) return cudaSuccess;

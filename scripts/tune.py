@@ -53,7 +53,10 @@ def sampler(stop, out):
 for cfg in configs:
     kv = dict(x.split("=") for x in cfg.split(","))
     os.environ["FASTED_CTA_GROUP"] = kv.get("CG", "0")
-    os.environ["FASTED_GROUP_ROWS"] = kv.get("G", "2048")
+    if "G" in kv:
+        os.environ["FASTED_GROUP_ROWS"] = kv["G"]
+    else:
+        os.environ.pop("FASTED_GROUP_ROWS", None)
     os.environ["FASTED_RESIDENT"] = kv.get("R", "1")
     if "SEG" in kv:
         os.environ["FASTED_SEG_TILES"] = kv["SEG"]
@@ -62,6 +65,7 @@ for cfg in configs:
     os.environ["FASTED_RES_BN"] = kv.get("BN", "256")
     os.environ["FASTED_MC"] = kv.get("MC", "1")
     os.environ["FASTED_RES_EPI"] = kv.get("EPI", "16")
+    os.environ["FASTED_DYN"] = kv.get("DYN", "1")
     flags = int(kv.get("F", "0"))
     engine.join_raw(dd, es, flags, (0, dd.n_dev), (0, dd.n_dev), rec, cap, cnt, stream.cuda_stream)
     torch.cuda.synchronize()
