@@ -67,7 +67,8 @@ enum {
     FASTED_JOIN_DIAG_LOADONLY = 1024, /* epilogue: TMEM loads only, no math           */
     FASTED_JOIN_DIAG_NOSLOW = 2048,  /* epilogue: sign test only, never write         */
     /* 4096: retired (column-scan hit search) */
-    FASTED_JOIN_DIAG_SPIN = 8192     /* accumulator waits spin (no suspend hint)      */
+    FASTED_JOIN_DIAG_SPIN = 8192,    /* accumulator waits spin (no suspend hint)      */
+    FASTED_JOIN_DIAG_LDX64 = 16384   /* epilogue: 32x32b.x64 TMEM loads               */
 };
 
 int fasted_abi_version(void);

@@ -134,7 +134,7 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     a.symmetric = symmetric ? 1 : 0;
     a.diag_flags = flags & (FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA |
                             FASTED_JOIN_DIAG_LOADONLY | FASTED_JOIN_DIAG_NOSLOW |
-                            FASTED_JOIN_DIAG_SPIN);
+                            FASTED_JOIN_DIAG_SPIN | FASTED_JOIN_DIAG_LDX64);
     a.out = reinterpret_cast<uint4*>(out_records);
     a.capacity = count_only ? 0ull : (unsigned long long)capacity;
     a.count = count;
