@@ -1625,6 +1625,7 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         // slower at 1M x 128: 263 vs 248 ms, its 96-register cap spills)
         if (cg == 2)
             e = tbn == 128 ? launch_res<2, 128, 8>(mx, mxb, ma, mbb, a, s)
+                : env_int("FASTED_RES_EPI", 8) == 16 ? launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s)
                            : launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
         else
             e = tbn == 128 ? launch_res<1, 128, 8>(mx, mxb, ma, mbb, a, s)

@@ -61,3 +61,26 @@ def test_join_exact_reproduces_reference_digest(tmp_path, golden_meta, capsys):
     assert rc == 0
     tc = json.loads((tmp_path / "tc.json").read_text())
     assert abs(tc["pairs"] - c1["pairs"]) < 1e-3 * c1["pairs"]
+
+
+@pytest.mark.gpu
+def test_join_symmetric_and_device_calibration(tmp_path, golden_meta):
+    """`join --symmetric` writes the same pairs file format with an exactly
+    symmetric pair set close to the full join's; `--target-selectivity` with
+    `--calibration-method device` lands near the target on the full data."""
+    c1 = golden_meta["C1"]
+    for extra, name in (([], "full"), (["--symmetric"], "sym")):
+        rc = cli.main(["join", "--synthetic", "16384x128", "--epsilon", repr(c1["epsilon"]),
+                       "--pairs-out", str(tmp_path / f"{name}.pairs")] + extra)
+        assert rc == 0
+    full = cli.read_pairs(tmp_path / "full.pairs", 16384, c1["epsilon"])
+    sym = cli.read_pairs(tmp_path / "sym.pairs", 16384, c1["epsilon"])
+    assert abs(len(sym) - len(full)) < 1e-3 * len(full)
+    assert set(zip(sym.i.tolist(), sym.j.tolist())) == set(zip(sym.j.tolist(), sym.i.tolist()))
+    rc = cli.main(["join", "--synthetic", "16384x128", "--target-selectivity", "64",
+                   "--calibration-method", "device", "--calibration-tol", "0.01",
+                   "--manifest", str(tmp_path / "cal.json")])
+    assert rc == 0
+    man = json.loads((tmp_path / "cal.json").read_text())
+    s = (man["pairs"] - 16384) / 16384
+    assert abs(s - 64) / 64 < 0.05, s
