@@ -230,8 +230,14 @@ def main():
     rec = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=f"cuda:{device}")
     cnt = torch.zeros(2, dtype=torch.int64, device=f"cuda:{device}")
 
+    nrows = max(rows[1] - rows[0], 1)
+    # the product path's kernel-form hint (engine.stream_join sets it the same way)
+    jflags = _lib.JOIN_TC | (_lib.JOIN_LOW_OUTPUT
+                             if cap - engine.hole_slack(device) <= engine.LOW_OUTPUT_PER_ROW * nrows
+                             else 0)
+
     def step():
-        engine.join_raw(dd, eps_sq, _lib.JOIN_TC, rows, (0, dd.n_dev), rec, cap, cnt,
+        engine.join_raw(dd, eps_sq, jflags, rows, (0, dd.n_dev), rec, cap, cnt,
                         stream.cuda_stream)
 
     def barrier():
@@ -259,7 +265,7 @@ def main():
     sym = None
     if world == 1 and not args.no_symmetric:
         def sym_step():
-            engine.join_raw(dd, eps_sq, _lib.JOIN_TC | _lib.JOIN_SYMMETRIC, rows,
+            engine.join_raw(dd, eps_sq, jflags | _lib.JOIN_SYMMETRIC, rows,
                             (0, dd.n_dev), rec, cap, cnt, stream.cuda_stream)
         sym_step()
         barrier()
@@ -296,7 +302,8 @@ def main():
     # cuBLAS figure (B200_PROFILING.md); the burst fraction is kept beside it.
     peak = peak_sus if peak_sus else peak_burst
     peak_kind = "bf16_tflops_sustained" if peak_sus else "bf16_tflops (burst)"
-    kernel_name = _lib.load().fasted_join_kernel_name(dd.d_pad, _lib.JOIN_TC).decode()
+    kernel_name = _lib.load().fasted_join_kernel_name(dd.d_pad, rows[1] - rows[0], dd.n_dev,
+                                                      jflags).decode()
     # roofline of the dominant kernel (the join): algorithmic flops per launch
     rows_logical = max(0, min(rows[1], n) - min(rows[0], n))
     flops_launch = 2.0 * rows_logical * n * d

@@ -61,6 +61,10 @@ enum {
      * orientations, (i, j) and (j, i), with the same dist_sq -- half the MMA
      * work for the same record set (and the set is exactly symmetric). */
     FASTED_JOIN_SYMMETRIC = 4,
+    /* OR-able hint: the caller expects <= 128 pairs per row.  Only picks the
+     * kernel form (results are identical): at d_pad > 256 on large joins the
+     * CTA-pair form, faster at low selectivity under the 1 kW power cap. */
+    FASTED_JOIN_LOW_OUTPUT = 8,
     /* Diagnostics for power/throughput attribution (results are NOT valid): */
     FASTED_JOIN_DIAG_NOEPI = 256,    /* tcgen05 kernel: skip the epilogue entirely     */
     FASTED_JOIN_DIAG_NOMMA = 512,    /* tcgen05 kernel: skip the MMAs (TMA + epilogue) */
@@ -150,9 +154,10 @@ int fasted_fp64_rows(const float* x, int64_t n, int64_t d, const int64_t* qrows,
                      double epsilon, void* out_records, uint64_t capacity,
                      unsigned long long* count, void* stream);
 
-/* Name of the join kernel fasted_join launches for this d_pad and flags
- * (the same selection rule, environment overrides included; for reports). */
-const char* fasted_join_kernel_name(int64_t d_pad, int flags);
+/* Name of the join kernel fasted_join launches for this d_pad, row and
+ * column counts and flags (the same selection rule, environment overrides
+ * included; for reports). */
+const char* fasted_join_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, int flags);
 
 /* Number of SMs and device name of the current device (for reports). */
 int fasted_device_info(int* sm_count, char* name, int name_len);

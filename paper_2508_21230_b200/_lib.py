@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfasted.so")
 
 OK, ERR_ARGUMENT, ERR_RANGE, ERR_CAPACITY, ERR_CUDA, ERR_UNSUPPORTED = 0, 2, 3, 4, 5, 6
-JOIN_TC, JOIN_EXACT, JOIN_COUNT, JOIN_SYMMETRIC = 0, 1, 2, 4
+JOIN_TC, JOIN_EXACT, JOIN_COUNT, JOIN_SYMMETRIC, JOIN_LOW_OUTPUT = 0, 1, 2, 4, 8
 
 # Every symbol include/fasted.h declares (tests check the .so exports them).
 EXPORTS = (
@@ -52,7 +52,7 @@ def load():
         L.fasted_device_check.restype = ci
         L.fasted_device_check.argtypes = [ci]
         L.fasted_join_kernel_name.restype = ctypes.c_char_p
-        L.fasted_join_kernel_name.argtypes = [ctypes.c_int64, ci]
+        L.fasted_join_kernel_name.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ci]
         L.fasted_device_info.restype = ci
         L.fasted_device_info.argtypes = [ctypes.POINTER(ci), ctypes.c_char_p, ci]
         L.fasted_quantize.restype = ci

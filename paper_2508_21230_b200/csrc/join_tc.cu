@@ -1504,21 +1504,40 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     return cudaLaunchKernelEx(&cfg, kern, mxa, mxb, ma, mb, a, sch);
 }
 
-// Which tcgen05 join kernel a launch with this d_pad uses (env overrides:
+// Which tcgen05 join kernel (and CTA group) a launch uses (env overrides:
 // FASTED_CTA_GROUP=1|2 forces the streaming kernel, FASTED_RESIDENT=0 and
 // FASTED_MC=0 disable the resident and multicast forms).
+//   d_pad <= 256                          resident-A CTA pair
+//   d_pad >  256, large, low output       streaming CTA pair, 16K-row raster
+//   d_pad >  256 otherwise                B-multicast clusters
+// The CTA pair (cta_group::2) reaches ~91% tensor-pipe utilisation per
+// clock but its power grows with the epilogue's record traffic: at the 1 kW
+// cap it wins at low selectivity (1M x 960, S = 48: 1376 vs 1333 TFLOPS;
+// 5M x 384 shard, S <= 16: 1342-1352 vs 1205-1261) and loses as pairs per
+// point grow (S ~ 250: 1053 vs 1234; S ~ 1000: 837 vs 1221), so the caller's
+// FASTED_JOIN_LOW_OUTPUT hint (<= 128 pairs per row expected) selects it.
+// Small joins are not power bound and the multicast form wins there
+// (60K x 512: 1203 vs 1186).
 enum { TC_STREAMING = 0, TC_RESIDENT = 1, TC_MULTICAST = 2 };
-static int tc_variant(int64_t d_pad) {
+static int tc_variant(int64_t d_pad, int64_t rows, int64_t cols, bool low_output, int* cg) {
+    const int cg_env = env_int("FASTED_CTA_GROUP", 0);
+    *cg = cg_env == 1 ? 1 : cg_env == 2 ? 2 : (d_pad <= 256 ? 2 : 1);
     if (d_pad <= 256) return env_int("FASTED_RESIDENT", 1) != 0 ? TC_RESIDENT : TC_STREAMING;
-    if (env_int("FASTED_CTA_GROUP", 0) != 0 || env_int("FASTED_MC", 1) == 0) return TC_STREAMING;
+    if (cg_env != 0 || env_int("FASTED_MC", 1) == 0) return TC_STREAMING;
+    if (low_output && (double)rows * (double)cols >= 68.7e9) {   // >= 2^36 pairs examined
+        *cg = 2;
+        return TC_STREAMING;
+    }
     return TC_MULTICAST;
 }
 
-const char* join_tc_kernel_name(int64_t d_pad) {
-    switch (tc_variant(d_pad)) {
-        case TC_RESIDENT: return "fasted::tc::join_tc_res_kernel";
+const char* join_tc_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, bool low_output) {
+    int cg = 0;
+    switch (tc_variant(d_pad, rows, cols, low_output, &cg)) {
+        case TC_RESIDENT: return cg == 2 ? "fasted::tc::join_tc_res_kernel<2>"
+                                         : "fasted::tc::join_tc_res_kernel<1>";
         case TC_MULTICAST: return "fasted::tc::join_tc_mc_kernel";
-        default: return "fasted::tc::join_tc_kernel";
+        default: return cg == 2 ? "fasted::tc::join_tc_kernel<2>" : "fasted::tc::join_tc_kernel<1>";
     }
 }
 
@@ -1540,9 +1559,9 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     //                 and ~980 for the CTA pair, which at the 1 kW cap runs
     //                 its clock down to ~920 MHz; 60K x 512: 1373 vs 1307).
     // FASTED_CTA_GROUP=1|2 forces the streaming kernel with that CTA group.
-    const int cg_env = env_int("FASTED_CTA_GROUP", 0);
-    const int cg = cg_env == 1 ? 1 : cg_env == 2 ? 2 : (a.d_pad <= 256 ? 2 : 1);
-    const int variant = tc_variant(a.d_pad);
+    int cg = 1;
+    const int variant = tc_variant(a.d_pad, a.row_end - a.row_begin, a.col_end - a.col_begin,
+                                   a.low_output != 0, &cg);
     // per-call scratch (stream ordered): augment rows (two [n_pad][8] FP32,
     // eps-dependent) and the tensor-core Gram diagonal
     float4* aug = nullptr;
@@ -1651,7 +1670,9 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     // grouped raster: GROUP row tiles (default 8192 rows) sweep all columns
     // (2048 rows measured best for the single-CTA form at 1M x 960: 0.82 vs
     // 0.93 pJ/flop for 8192)
-    sch.group = env_int("FASTED_GROUP_ROWS", 2048) / tile_m;
+    // (CTA pair: 16384 rows -- 1376 TFLOPS vs 1331 for 8192, 1031 for 2048
+    // and 1246 for 32768 at 1M x 960; profiles/round1/tune_c4_cg2b_session2.txt)
+    sch.group = env_int("FASTED_GROUP_ROWS", cg == 2 ? 16384 : 2048) / tile_m;
     if (sch.group < 1) sch.group = 1;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.total = (int64_t)sch.row_tiles * sch.col_tiles;

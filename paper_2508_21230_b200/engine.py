@@ -202,6 +202,8 @@ def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool
             if capacity is None:
                 capacity = _estimate_capacity(dd, eps_sq, rows, cols, flags, sp)
             capacity += slack
+        if not exact and capacity - slack <= LOW_OUTPUT_PER_ROW * 1.25 * max(rows[1] - rows[0], 1):
+            flags |= _lib.JOIN_LOW_OUTPUT      # kernel-form hint only (same results)
         cnt = torch.zeros(2, dtype=torch.int64, device=dev)
         reruns = 0
         kernel_ms = 0.0
@@ -317,6 +319,7 @@ def plan_row_chunks(rows, est_records: int, budget_records: int, min_chunks: int
 # chunk in flight, double buffered) and the sort + D2H of chunk c overlap
 # the join of chunk c + 1.
 PIPELINE_MIN_RECORDS = 1 << 22      # below this: one chunk (overlap not worth a launch)
+LOW_OUTPUT_PER_ROW = 128            # FASTED_JOIN_LOW_OUTPUT hint threshold (pairs per row)
 PIPELINE_CHUNKS = 4                 # chunks for mid-size outputs (overlap)
 BYTES_PER_RECORD_IN_FLIGHT = 2 * 16 + 2 * 12 + 8   # raw x2, sorted x2, sort scratch
 
@@ -365,6 +368,8 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
         if est is None:
             est = _estimate_capacity(dd, eps_sq, rows, cols, flags, sp)
         budget = budget_records or _chunk_budget(dd.device)
+        if not exact and est <= LOW_OUTPUT_PER_ROW * 1.25 * max(rows[1] - rows[0], 1):
+            flags |= _lib.JOIN_LOW_OUTPUT      # kernel-form hint only (same results)
         min_chunks = PIPELINE_CHUNKS if est >= PIPELINE_MIN_RECORDS else 1
         chunks = plan_row_chunks(rows, est, budget, min_chunks)
         if symmetric:

@@ -73,20 +73,23 @@ def main():
             e1.synchronize()
             return e0.elapsed_time(e1)
 
-        # count-only (exact count; sizes the record buffer)
+        # untimed count (sizes the record buffer and picks the kernel-form hint)
+        engine.join_raw(dd, es, _lib.JOIN_COUNT, rows, (0, dd.n_dev), None, 0, cnt, sp)
+        pairs = int(cnt[0].item())
+        cap = pairs + engine.max_holes(0)
+        jflags = _lib.JOIN_TC | (_lib.JOIN_LOW_OUTPUT
+                                 if pairs <= engine.LOW_OUTPUT_PER_ROW * nrows else 0)
         count_ms = []
         with ClockSampler(0) as clk_c:
             for _ in range(args.reps):
                 count_ms.append(timed(lambda: engine.join_raw(
-                    dd, es, _lib.JOIN_COUNT, rows, (0, dd.n_dev), None, 0, cnt, sp)))
-        pairs = int(cnt[0].item())
-        cap = pairs + engine.max_holes(0)
+                    dd, es, jflags | _lib.JOIN_COUNT, rows, (0, dd.n_dev), None, 0, cnt, sp)))
         rec = torch.empty((cap, 4), dtype=torch.int32, device="cuda")
         join_ms = []
         with ClockSampler(0) as clk_j:
             for _ in range(args.reps):
                 join_ms.append(timed(lambda: engine.join_raw(
-                    dd, es, _lib.JOIN_TC, rows, (0, dd.n_dev), rec, cap, cnt, sp)))
+                    dd, es, jflags, rows, (0, dd.n_dev), rec, cap, cnt, sp)))
         slots = int(cnt[1].item()) * engine.RECORD_CHUNK
         assert int(cnt[0].item()) == pairs
         sort_ms = timed(lambda: engine._sort_records(dd, rec, slots, pairs, rows, stream,
@@ -110,7 +113,8 @@ def main():
             "sort_ms": sort_ms,
             "sort_GBps_records": rec_bytes / (sort_ms / 1e3) / 1e9 if sort_ms else None,
             "eight_gpu_job_tflops_if_balanced": world * flops / jm / 1e9,
-            "kernel": L.fasted_join_kernel_name(dd.d_pad, _lib.JOIN_TC).decode(),
+            "kernel": L.fasted_join_kernel_name(dd.d_pad, rows[1] - rows[0], dd.n_dev,
+                                                jflags).decode(),
             "clocks_join": clk_j.summary(), "clocks_count": clk_c.summary(),
         }
         print(json.dumps(line), flush=True)
