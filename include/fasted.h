@@ -72,7 +72,8 @@ enum {
     FASTED_JOIN_DIAG_NOSLOW = 2048,  /* epilogue: sign test only, never write         */
     /* 4096: retired (column-scan hit search) */
     FASTED_JOIN_DIAG_SPIN = 8192,    /* accumulator waits spin (no suspend hint)      */
-    FASTED_JOIN_DIAG_LDX64 = 16384   /* epilogue: 32x32b.x64 TMEM loads               */
+    FASTED_JOIN_DIAG_LDX64 = 16384,  /* epilogue: 32x32b.x64 TMEM loads               */
+    FASTED_JOIN_DIAG_AEVL = 32768    /* CTA pair: A panel loads with L2 evict_last    */
 };
 
 int fasted_abi_version(void);

@@ -136,7 +136,8 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     a.low_output = (flags & FASTED_JOIN_LOW_OUTPUT) != 0 ? 1 : 0;
     a.diag_flags = flags & (FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA |
                             FASTED_JOIN_DIAG_LOADONLY | FASTED_JOIN_DIAG_NOSLOW |
-                            FASTED_JOIN_DIAG_SPIN | FASTED_JOIN_DIAG_LDX64);
+                            FASTED_JOIN_DIAG_SPIN | FASTED_JOIN_DIAG_LDX64 |
+                            FASTED_JOIN_DIAG_AEVL);
     a.out = reinterpret_cast<uint4*>(out_records);
     a.capacity = count_only ? 0ull : (unsigned long long)capacity;
     a.count = count;

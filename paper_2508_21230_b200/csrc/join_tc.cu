@@ -222,6 +222,16 @@ __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map
     }
 }
 
+// CTA-pair TMA load with an L2 cache policy (FASTED_A_EVICT_LAST experiments).
+__device__ __forceinline__ void tma_load_2d_pair_hint(uint32_t dst, const CUtensorMap* map,
+                                                      uint32_t bar, int c0, int c1, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::"
+        "bytes.L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "l"(pol)
+        : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -604,6 +614,8 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         // ---------------- TMA producer: nkb FP16 stages + 1 augment stage per tile
         // (whole warp walks the schedule; one elected lane issues)
         {
+            uint64_t pol_evl;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_evl));
             int s = 0;
             uint32_t ph = 0;
             for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
@@ -636,7 +648,13 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                 mbar_expect_tx(fb, (a_hi ? 2 : 1) * A_BYTES +
                                                        (b_hi ? 2 : 1) * B_HALF_BYTES);
                             if (a_mine)
-                                tma_load_2d<2>(sA + s * A_BYTES, &tmap_x, fb, kx, my_a);
+                            {
+                                if (a.diag_flags & FASTED_JOIN_DIAG_AEVL)
+                                    tma_load_2d_pair_hint(sA + s * A_BYTES, &tmap_x, fb, kx, my_a,
+                                                          pol_evl);
+                                else
+                                    tma_load_2d<2>(sA + s * A_BYTES, &tmap_x, fb, kx, my_a);
+                            }
                             if (rank == 0 || b_hi)
                                 tma_load_2d<2>(sB + s * C::B_BYTES, &tmap_x, fb, kx,
                                                (int)(col0 + 128 * rank));
