@@ -6,22 +6,27 @@
 //   kind::tf32 step (K=8) that adds
 //       sigma_i + rho_j = -s_i/2 + (-s_j/2 + eps^2/2)
 //   from two tiny per-point "augment" rows (norms split into 3 exact tf32
-//   parts, prepared per call by aug_prepare_kernel).  The accumulator then
-//   holds D_ij = (eps^2 - d2_ij) / 2, so the epilogue's common path is a
-//   sign test: d2 <= eps^2  <=>  D >= 0.  Epilogue warps drain their whole
-//   TMEM slice with back-to-back tcgen05.ld and one wait, release the
-//   accumulator to the MMA warp, then AND-reduce the sign bits (16 LOP3 per
-//   32 pairs); only a chunk holding a hit (or the diagonal) finds its
-//   candidate columns with REDUX and writes {i, j, d2 = eps^2 - 2D} records
-//   (PairWriter, one atomic per 256 records per warp).
+//   parts, prepared per call by aug_prepare_kernel from the tensor core's
+//   own Gram diagonal).  The accumulator then holds D_ij = (eps^2 - d2_ij)/2,
+//   so the epilogue's common path is a sign test: d2 <= eps^2 <=> D >= 0.
+//   Epilogue warps drain their whole TMEM slice with back-to-back
+//   tcgen05.ld and one wait, release the accumulator to the MMA warp, then
+//   AND-reduce the sign bits of the whole slice with one vote; only a chunk
+//   holding a hit (or the diagonal) builds per-lane hit masks and writes
+//   {i, j, d2 = eps^2 - 2D} records (StagedWriter: shared-memory staging,
+//   bulk async stores, one atomic per 256 records per warp).
 //
-// Two variants of the same kernel (template CG):
-//   CG = 2 (default): CTA pair (cluster of 2, tcgen05 cta_group::2).  A
-//          256 x 256 tile per pair; each CTA stages its 128 rows of A and its
-//          128-row half of B, the leader CTA issues M=256 N=256 MMAs that read
-//          both CTAs' shared memory.  Per SM this halves the B-operand shared
-//          memory reads and the L2->SM traffic of the 1-CTA form.
-//   CG = 1: one CTA, 128 x 256 tile (kept for A/B measurements).
+// Three kernels share that math and epilogue (tc_variant picks one):
+//   join_tc_kernel<CG>   both operands streamed.  CG = 2: CTA pair
+//                        (cta_group::2), a 256 x 256 tile per pair, each CTA
+//                        stages its 128 rows of A and its 128-row half of B,
+//                        the leader issues M=256 N=256 MMAs -- the form for
+//                        large low-output joins at d_pad > 256.  CG = 1: one
+//                        CTA, 128 x 256 tiles (the Gram pre-pass, A/B runs).
+//   join_tc_mc_kernel    clusters of two single-CTA MMAs sharing B by TMA
+//                        multicast (d_pad > 256 otherwise).
+//   join_tc_res_kernel   CTA pair with the A panel resident in shared memory
+//                        for a row tile x column segment (d_pad <= 256).
 //
 // The distance matrix never reaches HBM.  Replaces the reference's tile
 // sweep (tiling.py:307-344): compute_block_tile (tiling.py:199-285),
@@ -32,16 +37,17 @@
 // around eps^2 (tests/test_gpu.py).  Self pairs (i == j) are forced to
 // distance 0, which is exactly what the reference produces.
 //
-// Warp roles (320 threads -> up to 200 registers per thread, enough for a
-// warp's 32 x 128 accumulator slice):
-//   warp 0      : TMEM allocator / deallocator, then TMA producer (one lane)
-//   warp 1      : MMA issuer (one lane; leader CTA only for CG = 2)
+// Warp roles (320 threads; the register file allows 168 per thread, enough
+// for a warp's 32 x 128 accumulator slice):
+//   warp 0      : TMEM allocator / deallocator, then TMA producer
+//   warp 1      : MMA issuer (leader CTA only for a CTA pair)
 //   warps 2..9  : epilogue; warp w reads TMEM lanes 32*(w%4).. and column
 //                 half (w-2)/4 of the 256-column accumulator.
+// The producer and MMA loops run on the whole warp with elected issue.
 // TMEM: 2 accumulators x 256 columns (double buffered across tiles).
 // Tiles walk a grouped raster: GROUP row tiles sweep every column tile
-// together, so each 256-row B panel is read from HBM once per group and the
-// group's A panels stay L2 resident.
+// together, so each B panel is read from HBM once per group and the group's
+// A panels stay L2 resident.
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 

@@ -521,3 +521,23 @@ def test_c4_full_size_tc_vs_exact(oracle):
         sel = (ref.i > rb * 128) & (ref.i <= rb * 128 + 128)
         assert np.array_equal(oi, ref.i[sel]) and np.array_equal(oj, ref.j[sel])
         assert np.array_equal(od.view(np.uint32), ref.dist_sq[sel].view(np.uint32))
+
+
+def test_cta_pair_low_output_form_matches_single_cta():
+    """The large-join form at d_pad > 256 (CTA pair, 16K-row raster, picked
+    by the FASTED_JOIN_LOW_OUTPUT hint on >= 2^36 examined pairs) gives the
+    single-CTA kernel's bits: per element both accumulate the same K-ordered
+    MMA chain.  Also checks the selection rule itself."""
+    L = _lib.load()
+    name = lambda d, r, c, f: L.fasted_join_kernel_name(d, r, c, f).decode()
+    big = 1 << 19
+    assert "join_tc_kernel<2>" in name(512, big, big, _lib.JOIN_LOW_OUTPUT)
+    assert "mc" in name(512, big, big, 0)
+    assert "mc" in name(512, 60032, 60032, _lib.JOIN_LOW_OUTPUT)
+    assert "res" in name(128, big, big, _lib.JOIN_LOW_OUTPUT)
+    hd = F.to_half(F.generate_synthetic(3000, 520, seed=77))
+    pair = _tc_variant(hd, 8.5, FASTED_CTA_GROUP=2)
+    one = _tc_variant(hd, 8.5, FASTED_CTA_GROUP=1)
+    assert len(one[0]) > 3000
+    for x, y in zip(one, pair):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
