@@ -10,11 +10,16 @@
 //   4. per-row ordering by j (j values of a row are distinct):
 //        - rows <= SHORT_MAX records: one warp per row, rank by comparison
 //          against the row staged in shared memory;
-//        - rows <= MID_MAX: one CTA per row, bitonic sort of (j << 32 | d)
-//          keys in shared memory (O(len log^2 len)) -- the high-selectivity
-//          case (S ~ 1000-4000 at 5M x 384);
-//        - longer rows: a bitmap of the row's j range is set, prefix
-//          popcounts give every record's rank in O(n_cols/32 + len).
+//        - rows <= MID_MAX (then <= BIG_MAX): one CTA per row, bitonic sort
+//          of (j << 32 | d) keys in shared memory (O(len log^2 len)) -- the
+//          high-selectivity case (S ~ 1000-4000 at 5M x 384, where central
+//          points of uniform data have several times the mean neighbour
+//          count);
+//        - longer rows: one CTA per row splits the row into ~len/4096
+//          column buckets (shared-memory counts, scatter in place), then
+//          bitonic-sorts each bucket in shared memory; a row whose buckets
+//          overflow (adversarially clustered j) falls back to a bitmap of the
+//          column range with prefix popcounts, O(n_cols/32 + len).
 //          (This was the path for every row > 1024 before: at S = 4096 it
 //          cleared and scanned a 625 KB bitmap per row, 3.1 s for 2.56e9
 //          records; profiles/round1/c5_sweep_session2.jsonl.)
@@ -28,6 +33,7 @@ constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 constexpr int SHORT_MAX = 256;
 constexpr int SHORT_WARPS = 4;
 constexpr int MID_MAX = 8192;                  // keys per CTA bitonic sort (64 KB smem)
+constexpr int BIG_MAX = 16384;                 // second tier: 128 KB smem, one CTA per SM
 constexpr int MID_THREADS = 512;
 constexpr int LONG_BLOCKS = 32;
 constexpr int LONG_THREADS = 512;
@@ -41,6 +47,10 @@ struct SortWs {
     uint32_t* long_count;        // 1
     uint32_t* mid_rows;          // n_rows
     uint32_t* mid_count;         // 1
+    uint32_t* big_rows;          // n_rows
+    uint32_t* big_count;         // 1
+    uint32_t* fb_rows;           // n_rows (long rows whose buckets overflow: bitmap path)
+    uint32_t* fb_count;          // 1
     uint32_t* bitmap;            // LONG_BLOCKS * 2 * words
 };
 
@@ -65,6 +75,10 @@ static size_t carve(void* base, int64_t n_rows, int64_t n_cols, SortWs* ws) {
     w.long_count = reinterpret_cast<uint32_t*>(take(4));
     w.mid_rows = reinterpret_cast<uint32_t*>(take(n_rows * 4));
     w.mid_count = reinterpret_cast<uint32_t*>(take(4));
+    w.big_rows = reinterpret_cast<uint32_t*>(take(n_rows * 4));
+    w.big_count = reinterpret_cast<uint32_t*>(take(4));
+    w.fb_rows = reinterpret_cast<uint32_t*>(take(n_rows * 4));
+    w.fb_count = reinterpret_cast<uint32_t*>(take(4));
     w.bitmap = reinterpret_cast<uint32_t*>(take((size_t)LONG_BLOCKS * 2 * words * 4));
     if (ws) *ws = w;
     return off;
@@ -189,7 +203,8 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
                   int64_t row_begin, uint32_t* __restrict__ oi, uint32_t* __restrict__ oj,
                   float* __restrict__ od, uint32_t* __restrict__ long_rows,
                   uint32_t* __restrict__ long_count, uint32_t* __restrict__ mid_rows,
-                  uint32_t* __restrict__ mid_count) {
+                  uint32_t* __restrict__ mid_count, uint32_t* __restrict__ big_rows,
+                  uint32_t* __restrict__ big_count) {
     __shared__ uint32_t keys[SHORT_WARPS][SHORT_MAX];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int64_t r = (int64_t)blockIdx.x * SHORT_WARPS + w; r < n_rows;
@@ -200,6 +215,7 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
         if (len > SHORT_MAX) {
             if (lane == 0) {
                 if (len <= MID_MAX) mid_rows[atomicAdd(mid_count, 1u)] = (uint32_t)r;
+                else if (len <= BIG_MAX) big_rows[atomicAdd(big_count, 1u)] = (uint32_t)r;
                 else long_rows[atomicAdd(long_count, 1u)] = (uint32_t)r;
             }
             continue;
@@ -221,12 +237,13 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
 // One CTA per mid-length row: bitonic sort of 64-bit (j << 32 | d bits)
 // keys in shared memory (padding with all-ones keys to the next power of 2);
 // j is unique within a row, so key order is j order.
+template <int KEYS>
 __global__ void __launch_bounds__(MID_THREADS)
 mid_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
                 const unsigned long long* __restrict__ offsets, int64_t row_begin,
                 const uint32_t* __restrict__ mid_rows, const uint32_t* __restrict__ mid_count,
                 uint32_t* __restrict__ oi, uint32_t* __restrict__ oj, float* __restrict__ od) {
-    extern __shared__ unsigned long long key[];   // MID_MAX entries (dynamic: 64 KB)
+    extern __shared__ unsigned long long key[];   // KEYS entries (dynamic shared memory)
     const uint32_t nm = *mid_count;
     for (uint32_t mi = blockIdx.x; mi < nm; mi += gridDim.x) {
         const int64_t r = mid_rows[mi];
@@ -262,6 +279,99 @@ mid_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
             od[s0 + e] = __uint_as_float((uint32_t)v);
         }
         __syncthreads();
+    }
+}
+
+// Bitonic sort of n (power of 2) keys in shared memory, block-wide.
+__device__ __forceinline__ void block_bitonic(unsigned long long* key, uint32_t n) {
+    for (uint32_t k = 2; k <= n; k <<= 1) {
+        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+            for (uint32_t t = threadIdx.x; t < (n >> 1); t += blockDim.x) {
+                const uint32_t i = ((t & ~(jj - 1)) << 1) | (t & (jj - 1));
+                const uint32_t l = i + jj;
+                const unsigned long long a = key[i], b = key[l];
+                if ((a > b) == ((i & k) == 0)) {
+                    key[i] = b;
+                    key[l] = a;
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+constexpr int BUCKETS_MAX = 1024;
+
+// One CTA per long row (> BIG_MAX records): column buckets, then a
+// shared-memory bitonic sort per bucket.  The row's final slots in
+// out_j/out_d double as the scatter scratch.
+__global__ void __launch_bounds__(MID_THREADS)
+bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
+                   const unsigned long long* __restrict__ offsets, int64_t row_begin,
+                   int64_t n_cols, const uint32_t* __restrict__ long_rows,
+                   const uint32_t* __restrict__ long_count, uint32_t* __restrict__ fb_rows,
+                   uint32_t* __restrict__ fb_count, uint32_t* __restrict__ oi,
+                   uint32_t* __restrict__ oj, float* __restrict__ od) {
+    extern __shared__ unsigned long long key[];   // BIG_MAX entries
+    __shared__ uint32_t cnt[BUCKETS_MAX], boff[BUCKETS_MAX + 1], cur[BUCKETS_MAX];
+    __shared__ uint32_t overflow;
+    const uint32_t nl = *long_count;
+    for (uint32_t li = blockIdx.x; li < nl; li += gridDim.x) {
+        const int64_t r = long_rows[li];
+        const unsigned long long s0 = offsets[r];
+        const uint32_t len = (uint32_t)(offsets[r + 1] - s0);
+        uint32_t nb = 2;
+        while (nb < BUCKETS_MAX && (uint64_t)nb * 4096u < len) nb <<= 1;
+        const uint64_t bw = ((uint64_t)n_cols + nb - 1) / nb;   // columns per bucket
+        for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
+        if (threadIdx.x == 0) overflow = 0;
+        __syncthreads();
+        for (uint32_t e = threadIdx.x; e < len; e += blockDim.x)
+            atomicAdd(&cnt[(uint32_t)((tj[s0 + e] - 1) / bw)], 1u);
+        __syncthreads();
+        if (threadIdx.x == 0) {   // nb <= 1024: a serial scan is cheap next to the row
+            uint32_t run = 0;
+            for (uint32_t b = 0; b < nb; b++) {
+                boff[b] = run;
+                cur[b] = run;
+                if (cnt[b] > (uint32_t)BIG_MAX) overflow = 1;
+                run += cnt[b];
+            }
+            boff[nb] = run;
+        }
+        __syncthreads();
+        if (overflow) {
+            if (threadIdx.x == 0) fb_rows[atomicAdd(fb_count, 1u)] = (uint32_t)r;
+            __syncthreads();
+            continue;
+        }
+        for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
+            const uint32_t j = tj[s0 + e];
+            const uint32_t pos = atomicAdd(&cur[(uint32_t)((j - 1) / bw)], 1u);
+            oj[s0 + pos] = j;
+            od[s0 + pos] = td[s0 + e];
+        }
+        __syncthreads();   // the block's own global writes are visible to it after this
+        const uint32_t row1 = (uint32_t)(row_begin + r + 1);
+        for (uint32_t b = 0; b < nb; b++) {
+            const uint32_t b0 = boff[b], bl = boff[b + 1] - b0;
+            if (bl == 0) continue;
+            uint32_t n = 1;
+            while (n < bl) n <<= 1;
+            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
+                key[e] = e < bl ? ((unsigned long long)oj[s0 + b0 + e] << 32) |
+                                      (unsigned long long)__float_as_uint(od[s0 + b0 + e])
+                                : ~0ull;
+            __syncthreads();
+            block_bitonic(key, n);
+            for (uint32_t e = threadIdx.x; e < bl; e += blockDim.x) {
+                const unsigned long long v = key[e];
+                oi[s0 + b0 + e] = row1;
+                oj[s0 + b0 + e] = (uint32_t)(v >> 32);
+                od[s0 + b0 + e] = __uint_as_float((uint32_t)v);
+            }
+            __syncthreads();
+        }
     }
 }
 
@@ -355,6 +465,8 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
     cudaMemsetAsync(ws.cursor, 0, n_rows * 4, s);
     cudaMemsetAsync(ws.long_count, 0, 4, s);
     cudaMemsetAsync(ws.mid_count, 0, 4, s);
+    cudaMemsetAsync(ws.big_count, 0, 4, s);
+    cudaMemsetAsync(ws.fb_count, 0, 4, s);
     const int sms = sm_count_current();
     const unsigned rec_grid = (unsigned)((count + 255) / 256 < (uint64_t)sms * 16
                                              ? (count + 255) / 256
@@ -376,23 +488,40 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
     short_rows_kernel<<<(unsigned)(sgrid < (int64_t)sms * 64 ? sgrid : (int64_t)sms * 64),
                         SHORT_WARPS * 32, 0, s>>>(tmp_j, tmp_d, ws.offsets, n_rows, row_begin,
                                                   out_i, out_j, out_d, ws.long_rows,
-                                                  ws.long_count, ws.mid_rows, ws.mid_count);
+                                                  ws.long_count, ws.mid_rows, ws.mid_count,
+                                                  ws.big_rows, ws.big_count);
     FASTED_CHECK_LAUNCH("short_rows_kernel");
     static bool mid_attr = false;
     if (!mid_attr) {
-        cudaError_t e = cudaFuncSetAttribute(mid_rows_kernel,
+        cudaError_t e = cudaFuncSetAttribute(mid_rows_kernel<MID_MAX>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              MID_MAX * 8);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(mid_rows_kernel<BIG_MAX>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, BIG_MAX * 8);
         if (e != cudaSuccess) return cuda_status(e, "mid_rows_kernel attribute");
         mid_attr = true;
     }
-    mid_rows_kernel<<<(unsigned)(sms * 3), MID_THREADS, MID_MAX * 8, s>>>(tmp_j, tmp_d, ws.offsets,
-                                                                row_begin, ws.mid_rows,
-                                                                ws.mid_count, out_i, out_j,
-                                                                out_d);
+    mid_rows_kernel<MID_MAX><<<(unsigned)(sms * 3), MID_THREADS, MID_MAX * 8, s>>>(
+        tmp_j, tmp_d, ws.offsets, row_begin, ws.mid_rows, ws.mid_count, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("mid_rows_kernel");
+    mid_rows_kernel<BIG_MAX><<<(unsigned)sms, MID_THREADS, BIG_MAX * 8, s>>>(
+        tmp_j, tmp_d, ws.offsets, row_begin, ws.big_rows, ws.big_count, out_i, out_j, out_d);
+    FASTED_CHECK_LAUNCH("mid_rows_kernel");
+    static bool bucket_attr = false;
+    if (!bucket_attr) {
+        cudaError_t e = cudaFuncSetAttribute(bucket_rows_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             BIG_MAX * 8);
+        if (e != cudaSuccess) return cuda_status(e, "bucket_rows_kernel attribute");
+        bucket_attr = true;
+    }
+    bucket_rows_kernel<<<(unsigned)sms, MID_THREADS, BIG_MAX * 8, s>>>(
+        tmp_j, tmp_d, ws.offsets, row_begin, n_cols, ws.long_rows, ws.long_count, ws.fb_rows,
+        ws.fb_count, out_i, out_j, out_d);
+    FASTED_CHECK_LAUNCH("bucket_rows_kernel");
     long_rows_kernel<<<LONG_BLOCKS, LONG_THREADS, 0, s>>>(tmp_j, tmp_d, ws.offsets, row_begin,
-                                                          n_cols, ws.long_rows, ws.long_count,
+                                                          n_cols, ws.fb_rows, ws.fb_count,
                                                           ws.bitmap, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("long_rows_kernel");
     return FASTED_OK;

@@ -541,3 +541,36 @@ def test_cta_pair_low_output_form_matches_single_cta():
     assert len(one[0]) > 3000
     for x, y in zip(one, pair):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
+def test_sort_long_rows_bucket_and_fallback_paths():
+    """Rows above 16384 records: spread j -> column buckets + shared-memory
+    bitonic per bucket; j clustered in one bucket -> the bitmap fallback.
+    Both must give the reference's lexsort order."""
+    rng = np.random.default_rng(5)
+    n_cols = 4_000_000
+    rows = []
+    rows.append(rng.choice(n_cols, 30000, replace=False) + 1)          # spread: bucket path
+    rows.append(rng.choice(25000, 20000, replace=False) + 1)           # clustered: fallback
+    rows.append(rng.choice(n_cols, 3000, replace=False) + 1)           # mid path
+    i = np.concatenate([np.full(len(r), k + 1) for k, r in enumerate(rows)]).astype(np.int32)
+    j = np.concatenate(rows).astype(np.int32)
+    d = rng.random(len(i)).astype(np.float32)
+    perm = rng.permutation(len(i))
+    rec = np.zeros((len(i), 4), np.int32)
+    rec[:, 0], rec[:, 1], rec[:, 2] = i[perm], j[perm], d[perm].view(np.int32)
+    L = _lib.load()
+    trec = torch.from_numpy(rec).cuda()
+    n = len(i)
+    oi, oj, tj = (torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3))
+    od, td = (torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(2))
+    wsb = L.fasted_sort_workspace_bytes(len(rows), n_cols)
+    ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
+    _lib.check(L.fasted_sort_pairs(trec.data_ptr(), n, 0, len(rows), n_cols, oi.data_ptr(),
+                                   oj.data_ptr(), od.data_ptr(), tj.data_ptr(), td.data_ptr(),
+                                   ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream),
+               "sort")
+    order = np.lexsort((j, i))
+    assert np.array_equal(oi.cpu().numpy(), i[order])
+    assert np.array_equal(oj.cpu().numpy(), j[order])
+    assert np.array_equal(od.cpu().numpy(), d[order])
