@@ -579,10 +579,20 @@ def self_join_devices(hd, eps_sq: float, devices, exact: bool = False, row_range
         # the pinned host buffers ARE the result arrays (no concatenation copy)
         i, j, d = results[0][0].arrays()
     else:
+        # devices' shards in rank order = canonical order; one copy per device
+        # part and array, in parallel (numpy releases the GIL for the memcpy)
         arrs = [r[0].arrays() for r in results]
-        i = np.concatenate([a[0] for a in arrs])
-        j = np.concatenate([a[1] for a in arrs])
-        d = np.concatenate([a[2] for a in arrs])
+        offs = np.cumsum([0] + [len(a[0]) for a in arrs])
+        i = np.empty(offs[-1], np.uint32)
+        j = np.empty(offs[-1], np.uint32)
+        d = np.empty(offs[-1], np.float32)
+
+        def place(job):
+            g, k = job
+            (i, j, d)[k][offs[g]:offs[g + 1]] = arrs[g][k]
+
+        with ThreadPoolExecutor(max_workers=min(16, 3 * len(arrs))) as ex:
+            list(ex.map(place, [(g, k) for g in range(len(arrs)) for k in range(3)]))
     rep = JoinReport(
         kernel_seconds=max(r[1][0] for r in results) / 1e3,
         merge_seconds=max(r[3] - r[1][0] / 1e3 for r in results),
