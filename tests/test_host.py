@@ -242,3 +242,17 @@ def test_device_calibration_validates_before_device_use():
         F.calibrate_epsilon_device(hd, 1.0, sample_blocks=0)
     with pytest.raises(F.CalibrationError):
         F.calibrate_epsilon_device(hd, 10.0)
+
+
+def test_python_flag_constants_match_header():
+    """_lib's flag and status constants are the values include/fasted.h defines."""
+    src = open(os.path.join(ROOT, "include", "fasted.h")).read()
+    vals = {k: int(v) for k, v in re.findall(r"\b(FASTED_[A-Z_0-9]+)\s*=\s*(\d+)", src)}
+    assert vals["FASTED_JOIN_TC"] == _lib.JOIN_TC
+    assert vals["FASTED_JOIN_EXACT"] == _lib.JOIN_EXACT
+    assert vals["FASTED_JOIN_COUNT"] == _lib.JOIN_COUNT
+    assert vals["FASTED_JOIN_SYMMETRIC"] == _lib.JOIN_SYMMETRIC
+    assert vals["FASTED_JOIN_LOW_OUTPUT"] == _lib.JOIN_LOW_OUTPUT
+    assert vals["FASTED_ERR_ARGUMENT"] == _lib.ERR_ARGUMENT
+    rec = re.search(r"#define FASTED_RECORD_CHUNK (\d+)", src)
+    assert int(rec.group(1)) == engine.RECORD_CHUNK
