@@ -1664,11 +1664,14 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
             cudaFreeAsync(aug, s);
             return st;
         }
-        // 8 epilogue warps (NEPI = 16, each draining 64 columns, measured
-        // slower at 1M x 128: 263 vs 248 ms, its 96-register cap spills)
+        // 16 epilogue warps, each draining 64 columns (FASTED_RES_EPI=8: 8
+        // warps of 128 columns).  Measured at 1M x 128, alternating runs on
+        // one box: 253.8-253.9 ms with 16 vs 269-319 ms with 8 -- the shorter
+        // per-warp chain per tile also removes the run-to-run spread
+        // (profiles/round1/tune_c3_epi_ab_session2.txt).
         if (cg == 2)
             e = tbn == 128 ? launch_res<2, 128, 8>(mx, mxb, ma, mbb, a, s)
-                : env_int("FASTED_RES_EPI", 8) == 16 ? launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s)
+                : env_int("FASTED_RES_EPI", 16) == 16 ? launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s)
                            : launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
         else
             e = tbn == 128 ? launch_res<1, 128, 8>(mx, mxb, ma, mbb, a, s)

@@ -353,7 +353,7 @@ def test_resident_kernel_bit_identical_to_streaming(n, d, eps, seg):
     for cg in (2, 1):
         ref = _tc_variant(hd, eps, FASTED_RESIDENT=0, FASTED_CTA_GROUP=cg)
         assert len(ref[0]) > n
-        for bn, epi in ((256, 8), (128, 8)):
+        for bn, epi in ((256, 16), (256, 8), (128, 8)):
             res = _tc_variant(hd, eps, FASTED_RESIDENT=1, FASTED_CTA_GROUP=cg,
                               FASTED_SEG_TILES=seg, FASTED_RES_BN=bn, FASTED_RES_EPI=epi)
             for x, y in zip(ref, res):
