@@ -546,8 +546,8 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
     if (NCH > 2 && nchunks > 3) epi_chunk(a, wr, r3, jb + 96, i, iw, row_ok);
 }
 
-template <int CG, bool DIAG>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int CG, bool DIAG, int NEPI = NUM_EPI_WARPS>
+__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI) * 32, 1)
 join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                const __grid_constant__ CUtensorMap tmap_aug_a,
                const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
@@ -586,7 +586,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(tfull_bar(b), 1);
-            mbar_init(tempty_bar(b), NUM_EPI_WARPS * CG);
+            mbar_init(tempty_bar(b), NEPI * CG);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x))
@@ -754,8 +754,11 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         const int q = warp & 3;          // TMEM lane quarter this warp may access
         const int h = (warp - FIRST_EPI_WARP) >> 2;   // column half of the accumulator
         const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-        StagedWriter<WSTAGE> wr;
-        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WSTAGE * 16);
+        // staging: 16 KB for the epilogue warps (64 records per buffer with 8
+        // warps, 32 with 16)
+        constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;
+        StagedWriter<WST> wr;
+        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -785,7 +788,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 if (h == 0 && i < a.row_end) a.gram_diag[i] = __uint_as_float(pick32(r0, lane));
                 continue;
             }
-            epilogue_tile<CG, BN>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf, aph, q, h,
+            epilogue_tile<CG, BN, NEPI / 4>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf, aph, q, h,
                               lane, leader, tfull_bar(buf));
         }
         writer_finish(wr, a);
@@ -842,7 +845,8 @@ constexpr int MC_STAGES = 4;
 constexpr int MC_SMEM_BYTES =
     MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + WSTAGE_BYTES + 1024;
 
-__global__ void __launch_bounds__(THREADS, 1)
+template <int NEPI>
+__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI) * 32, 1)
 join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                   const __grid_constant__ CUtensorMap tmap_aug_a,
                   const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
@@ -878,7 +882,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(tfull_bar(b), 1);
-            mbar_init(tempty_bar(b), NUM_EPI_WARPS);
+            mbar_init(tempty_bar(b), NEPI);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x))
@@ -988,8 +992,9 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         // ---------------- epilogue
         const int q = warp & 3;
         const int h = (warp - FIRST_EPI_WARP) >> 2;
-        StagedWriter<WSTAGE> wr;
-        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WSTAGE * 16);
+        constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;   // 16 KB of staging either way
+        StagedWriter<WST> wr;
+        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -1001,7 +1006,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 continue;
             }
             const int buf = lt & 1;
-            epilogue_tile<1, BN>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf,
+            epilogue_tile<1, BN, NEPI / 4>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf,
                                  (uint32_t)(lt >> 1) & 1u, q, h, lane, true, tfull_bar(buf));
         }
         writer_finish(wr, a);
@@ -1402,12 +1407,12 @@ static int env_int(const char* name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 
-template <int CG, bool DIAG = false>
+template <int CG, bool DIAG = false, int NEPI = tc::NUM_EPI_WARPS>
 static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
                                   const CUtensorMap& mb, const JoinArgs& a, const tc::Sched& sch,
                                   cudaStream_t s) {
     using namespace tc;
-    auto kern = join_tc_kernel<CG, DIAG>;
+    auto kern = join_tc_kernel<CG, DIAG, NEPI>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1421,7 +1426,7 @@ static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
     if (work <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * CG));
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI) * 32);
     cfg.dynamicSmemBytes = Cfg<CG>::SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1435,10 +1440,11 @@ static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
 }
 
 // B-multicast launch: clusters of two CTAs over super-tiles of 256 rows.
+template <int NEPI>
 static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const CUtensorMap& mb,
                              const JoinArgs& a, cudaStream_t s) {
     using namespace tc;
-    auto kern = join_tc_mc_kernel;
+    auto kern = join_tc_mc_kernel<NEPI>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1461,7 +1467,7 @@ static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const
     if (work <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * 2));
-    cfg.blockDim = dim3(THREADS);
+    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI) * 32);
     cfg.dynamicSmemBytes = MC_SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1683,7 +1689,12 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     }
     // Large d: B-multicast clusters unless FASTED_MC=0 (or a CTA group is forced).
     if (variant == TC_MULTICAST) {
-        e = launch_mc(mx, ma, mb, a, s);
+        // 16 epilogue warps of 64 columns (FASTED_MC_EPI=8: 8 of 128).  Measured,
+        // alternating runs: 60K x 512 2.63-2.67 vs 2.94-3.55 ms; 1M x 960
+        // 1406-1431 vs 1506-1515 ms; 5M x 384 shard at S ~ 4000 2535 vs 3140 ms
+        // (profiles/round1/tune_mepi_session2.txt)
+        e = env_int("FASTED_MC_EPI", 16) == 8 ? launch_mc<8>(mx, ma, mb, a, s)
+                                              : launch_mc<16>(mx, ma, mb, a, s);
         if (e == cudaSuccess) e = cudaGetLastError();
         cudaFreeAsync(aug, s);
         if (e != cudaSuccess) return cuda_status(e, "join_tc_mc_kernel");
@@ -1703,7 +1714,12 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     if (sch.group < 1) sch.group = 1;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.total = (int64_t)sch.row_tiles * sch.col_tiles;
-    e = cg == 2 ? launch_variant<2>(mx, ma, mb, a, sch, s) : launch_variant<1>(mx, ma, mb, a, sch, s);
+    // FASTED_STREAM_EPI=16: 16 epilogue warps of 64 columns (CTA pair only)
+    if (cg == 2)
+        e = env_int("FASTED_STREAM_EPI", 8) == 16 ? launch_variant<2, false, 16>(mx, ma, mb, a, sch, s)
+                                                  : launch_variant<2>(mx, ma, mb, a, sch, s);
+    else
+        e = launch_variant<1>(mx, ma, mb, a, sch, s);
     if (e == cudaSuccess) e = cudaGetLastError();
     cudaFreeAsync(aug, s);
     if (e != cudaSuccess) return cuda_status(e, "join_tc_kernel");

@@ -375,10 +375,11 @@ def test_multicast_kernel_bit_identical_to_single_cta(n, d, eps):
     row-tile counts (a masked partner tile) and ragged shard ranges."""
     hd = F.to_half(F.generate_synthetic(n, d, seed=n * 7 + d))
     ref = _tc_variant(hd, eps, FASTED_CTA_GROUP=1)
-    mc = _tc_variant(hd, eps, FASTED_MC=1, FASTED_CTA_GROUP=0)
     assert len(ref[0]) > n
-    for x, y in zip(ref, mc):
-        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    for mepi in (8, 16):
+        mc = _tc_variant(hd, eps, FASTED_MC=1, FASTED_CTA_GROUP=0, FASTED_MC_EPI=mepi)
+        for x, y in zip(ref, mc):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), mepi
     n_dev = -(-hd.n_padded // 128) * 128
     rows, cols = (128, min(n_dev, 1152)), (256, n_dev)
     ref = _tc_variant(hd, eps, rows, cols, FASTED_CTA_GROUP=1)
@@ -536,11 +537,12 @@ def test_cta_pair_low_output_form_matches_single_cta():
     assert "mc" in name(512, 60032, 60032, _lib.JOIN_LOW_OUTPUT)
     assert "res" in name(128, big, big, _lib.JOIN_LOW_OUTPUT)
     hd = F.to_half(F.generate_synthetic(3000, 520, seed=77))
-    pair = _tc_variant(hd, 8.5, FASTED_CTA_GROUP=2)
     one = _tc_variant(hd, 8.5, FASTED_CTA_GROUP=1)
     assert len(one[0]) > 3000
-    for x, y in zip(one, pair):
-        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    for sepi in (8, 16):
+        pair = _tc_variant(hd, 8.5, FASTED_CTA_GROUP=2, FASTED_STREAM_EPI=sepi)
+        for x, y in zip(one, pair):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), sepi
 
 
 def test_sort_long_rows_bucket_and_fallback_paths():
