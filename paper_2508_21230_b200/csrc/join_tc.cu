@@ -1714,10 +1714,12 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     if (sch.group < 1) sch.group = 1;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.total = (int64_t)sch.row_tiles * sch.col_tiles;
-    // FASTED_STREAM_EPI=16: 16 epilogue warps of 64 columns (CTA pair only)
+    // CTA pair: 16 epilogue warps of 64 columns (FASTED_STREAM_EPI=8: 8 of
+    // 128).  1M x 960: 1466-1472 vs 1450-1491 TFLOPS (even); 5M x 384 shard
+    // at S <= 64: 1917-1946 vs 2060-2253 ms (profiles/round1/tune_sepi_session2.txt)
     if (cg == 2)
-        e = env_int("FASTED_STREAM_EPI", 8) == 16 ? launch_variant<2, false, 16>(mx, ma, mb, a, sch, s)
-                                                  : launch_variant<2>(mx, ma, mb, a, sch, s);
+        e = env_int("FASTED_STREAM_EPI", 16) == 8 ? launch_variant<2>(mx, ma, mb, a, sch, s)
+                                                  : launch_variant<2, false, 16>(mx, ma, mb, a, sch, s);
     else
         e = launch_variant<1>(mx, ma, mb, a, sch, s);
     if (e == cudaSuccess) e = cudaGetLastError();

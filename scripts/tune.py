@@ -65,7 +65,7 @@ for cfg in configs:
     os.environ["FASTED_RES_BN"] = kv.get("BN", "256")
     os.environ["FASTED_MC"] = kv.get("MC", "1")
     os.environ["FASTED_RES_EPI"] = kv.get("EPI", "16")
-    os.environ["FASTED_STREAM_EPI"] = kv.get("SEPI", "8")
+    os.environ["FASTED_STREAM_EPI"] = kv.get("SEPI", "16")
     os.environ["FASTED_MC_EPI"] = kv.get("MEPI", "16")
     os.environ["FASTED_DYN"] = kv.get("DYN", "1")
     flags = int(kv.get("F", "0"))
