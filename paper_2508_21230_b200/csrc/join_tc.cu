@@ -37,12 +37,13 @@
 // around eps^2 (tests/test_gpu.py).  Self pairs (i == j) are forced to
 // distance 0, which is exactly what the reference produces.
 //
-// Warp roles (320 threads; the register file allows 168 per thread, enough
-// for a warp's 32 x 128 accumulator slice):
+// Warp roles (2 + NEPI warps; the product forms use NEPI = 16 -- 96
+// registers per thread, a warp's 32 x 64 accumulator slice; NEPI = 8 gives
+// 168 registers and 32 x 128 slices):
 //   warp 0      : TMEM allocator / deallocator, then TMA producer
 //   warp 1      : MMA issuer (leader CTA only for a CTA pair)
-//   warps 2..9  : epilogue; warp w reads TMEM lanes 32*(w%4).. and column
-//                 half (w-2)/4 of the 256-column accumulator.
+//   warps 2..   : epilogue; warp w reads TMEM lanes 32*(w%4).. and column
+//                 group (w-2)/4 of the 256-column accumulator.
 // The producer and MMA loops run on the whole warp with elected issue.
 // TMEM: 2 accumulators x 256 columns (double buffered across tiles).
 // Tiles walk a grouped raster: GROUP row tiles sweep every column tile
