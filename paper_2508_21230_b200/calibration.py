@@ -27,7 +27,6 @@ def _count_fn(hd, sample_blocks: int, seed: int, device):
     if device is None:
         device = torch.cuda.current_device()
     dd = engine.upload(hd, device)
-    nblk = dd.n_dev // engine.BLOCK
     valid_blk = -(-hd.n_logical // engine.BLOCK)
     k = min(sample_blocks, valid_blk)
     rng = np.random.default_rng(seed)
@@ -47,7 +46,6 @@ def _count_fn(hd, sample_blocks: int, seed: int, device):
         return tot
 
     max_norm = float(np.max(hd.norms[:hd.n_logical])) if hd.n_logical else 0.0
-    del nblk
     return count, m, max_norm
 
 
