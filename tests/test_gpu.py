@@ -576,3 +576,17 @@ def test_sort_long_rows_bucket_and_fallback_paths():
     assert np.array_equal(oi.cpu().numpy(), i[order])
     assert np.array_equal(oj.cpu().numpy(), j[order])
     assert np.array_equal(od.cpu().numpy(), d[order])
+
+
+@pytest.mark.parametrize("n,d,eps", [(5, 3, 0.7), (130, 2000, 25.5), (257, 4100, 36.8)])
+def test_tc_extreme_shapes_band_parity(oracle, n, d, eps):
+    """Tiny n (one partial row block) and large d (k loop of 32-65 blocks,
+    ragged last block zero-filled by TMA) on every kernel form."""
+    hd = F.to_half(F.generate_synthetic(n, d, seed=d))
+    oi, oj, od = oracle.join(hd.values, hd.norms, n, eps)
+    for env in ({}, {"FASTED_CTA_GROUP": "1"}, {"FASTED_CTA_GROUP": "2"}):
+        got = _tc_variant(hd, eps, **env)
+        rs = F.make_result_set(got[0], got[1], got[2], n, eps)
+        rep = _band_ok(oracle, hd, rs, oi, oj, od, eps)
+        assert rep.ok, (env, rep)
+        assert len(rs) >= n
