@@ -256,3 +256,32 @@ def test_python_flag_constants_match_header():
     assert vals["FASTED_ERR_ARGUMENT"] == _lib.ERR_ARGUMENT
     rec = re.search(r"#define FASTED_RECORD_CHUNK (\d+)", src)
     assert int(rec.group(1)) == engine.RECORD_CHUNK
+
+
+def test_plan_row_chunks():
+    """Contiguous 128-aligned chunks covering the range; count from the
+    record budget, at least min_chunks, at most one per row block."""
+    ch = engine.plan_row_chunks((0, 1000064), 49e6, 20e6, 1)
+    assert len(ch) == 3 and ch[0][0] == 0 and ch[-1][1] == 1000064
+    assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
+    assert all(c[0] % 128 == 0 and c[1] % 128 == 0 for c in ch)
+    assert len(engine.plan_row_chunks((0, 1000064), 1e3, 1e9, 4)) == 4
+    assert engine.plan_row_chunks((256, 512), 1e9, 1, 1) == [(256, 384), (384, 512)]
+    assert engine.plan_row_chunks((128, 128), 10, 1, 4) == [(128, 128)]
+
+
+def test_kernel_selection_rule_is_host_side():
+    """fasted_join_kernel_name applies the launch's selection rule without a
+    GPU: resident pair for d_pad <= 256, the CTA pair for large low-output
+    joins, multicast clusters otherwise, the exact kernel for mode exact."""
+    L = _lib.load()
+
+    def name(d, r, c, f):
+        return L.fasted_join_kernel_name(d, r, c, f).decode()
+
+    big = 1 << 19
+    assert name(128, big, big, 0) == "fasted::tc::join_tc_res_kernel<2>"
+    assert name(960, big, big, _lib.JOIN_LOW_OUTPUT) == "fasted::tc::join_tc_kernel<2>"
+    assert name(960, big, big, 0) == "fasted::tc::join_tc_mc_kernel"
+    assert name(512, 60032, 60032, _lib.JOIN_LOW_OUTPUT) == "fasted::tc::join_tc_mc_kernel"
+    assert name(960, big, big, _lib.JOIN_EXACT) == "fasted::join_exact_kernel"
