@@ -1053,7 +1053,10 @@ struct ResSched {
     int64_t units;            // row_tiles * nsegs
 };
 
-constexpr int RES_WSTAGE = 32;   // records per staging buffer (resident kernel: tight smem)
+// Records per staging buffer in the resident kernel (tight shared memory):
+// 8 KB for the epilogue in total, so the B ring keeps its 7 stages at d = 128
+// (16 KB cost a stage: no-epilogue 204 vs 174 ms at 1M x 128).
+constexpr int RES_WSTAGE_TOTAL = 256;   // records, all epilogue warps x 2 buffers
 
 template <int CG, int TBN>
 struct ResCfg {
@@ -1300,9 +1303,10 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         // ---------------- epilogue
         const int q = warp & 3;                       // TMEM lane quarter
         const int h = (warp - FIRST_EPI_WARP) >> 2;   // column group (NEPI / 4 of them)
-        StagedWriter<RES_WSTAGE> wr;
+        constexpr int RWS = RES_WSTAGE_TOTAL / (2 * NEPI) * 2;   // 16 (NEPI 16) / 32 (NEPI 8)
+        StagedWriter<RWS> wr;
         writer_init(wr, bars + C::BAR_REGION +
-                            (uint32_t)(warp - FIRST_EPI_WARP) * 2 * RES_WSTAGE * 16);
+                            (uint32_t)(warp - FIRST_EPI_WARP) * 2 * RWS * 16);
         int lt = 0;
         for (int64_t u = unit0; u < sch.units; u += ustep) {
             int rt, ct0, ct1;
@@ -1501,7 +1505,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     ResSched sch;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.a_buf_bytes = (uint32_t)((sch.nkb * A_BYTES + BM * AUG_ROW_BYTES + 1023) & ~1023);
-    const int wstage = NEPI * 2 * RES_WSTAGE * 16;
+    const int wstage = NEPI * 2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16;
     const int budget = SMEM_MAX - 1024 - C::BAR_REGION - wstage;
     sch.na = 2 * (int)sch.a_buf_bytes <= 80 * 1024 ? 2 : 1;
     sch.stages = (budget - sch.na * (int)sch.a_buf_bytes) / C::STAGE_BYTES;
