@@ -28,6 +28,25 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 int sm_count_current();
 
+// cudaFuncSetAttribute applies per device context: a launcher keeps one of
+// these per kernel and sets the attribute once for each device it runs on
+// (one host thread per GPU in self_join(devices=[...])).
+struct PerDeviceOnce {
+    static constexpr int MAX_DEVICES = 64;
+    volatile bool done[MAX_DEVICES] = {};
+    template <typename F>
+    cudaError_t run(F&& f) {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) return e;
+        if (dev < 0 || dev >= MAX_DEVICES) return f();
+        if (done[dev]) return cudaSuccess;
+        e = f();
+        if (e == cudaSuccess) done[dev] = true;
+        return e;
+    }
+};
+
 // ---------------------------------------------------------------- device side
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }

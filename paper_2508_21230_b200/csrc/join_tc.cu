@@ -1418,12 +1418,13 @@ static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
                                   cudaStream_t s) {
     using namespace tc;
     auto kern = join_tc_kernel<CG, DIAG, NEPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Cfg<CG>::SMEM_BYTES);
+    static PerDeviceOnce attr_once;
+    {
+        cudaError_t e = attr_once.run([&] {
+            return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        Cfg<CG>::SMEM_BYTES);
+        });
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const int sms = sm_count_current();
     const int64_t units = sms / CG;   // CTAs (or CTA pairs) resident at once
@@ -1450,12 +1451,13 @@ static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const
                              const JoinArgs& a, cudaStream_t s) {
     using namespace tc;
     auto kern = join_tc_mc_kernel<NEPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             MC_SMEM_BYTES);
+    static PerDeviceOnce attr_once;
+    {
+        cudaError_t e = attr_once.run([&] {
+            return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        MC_SMEM_BYTES);
+        });
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     Sched sch;
     sch.diag = 0;
@@ -1495,12 +1497,13 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     using C = ResCfg<CG, TBN>;
     constexpr int SMEM_MAX = 227 * 1024;
     auto kern = join_tc_res_kernel<CG, TBN, NEPI>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             SMEM_MAX);
+    static PerDeviceOnce attr_once;
+    {
+        cudaError_t e = attr_once.run([&] {
+            return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SMEM_MAX);
+        });
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     ResSched sch;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);

@@ -491,16 +491,18 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
                                                   ws.long_count, ws.mid_rows, ws.mid_count,
                                                   ws.big_rows, ws.big_count);
     FASTED_CHECK_LAUNCH("short_rows_kernel");
-    static bool mid_attr = false;
-    if (!mid_attr) {
-        cudaError_t e = cudaFuncSetAttribute(mid_rows_kernel<MID_MAX>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             MID_MAX * 8);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(mid_rows_kernel<BIG_MAX>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, BIG_MAX * 8);
+    static PerDeviceOnce mid_once;
+    {
+        cudaError_t e = mid_once.run([&] {
+            cudaError_t r = cudaFuncSetAttribute(mid_rows_kernel<MID_MAX>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 MID_MAX * 8);
+            if (r == cudaSuccess)
+                r = cudaFuncSetAttribute(mid_rows_kernel<BIG_MAX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, BIG_MAX * 8);
+            return r;
+        });
         if (e != cudaSuccess) return cuda_status(e, "mid_rows_kernel attribute");
-        mid_attr = true;
     }
     mid_rows_kernel<MID_MAX><<<(unsigned)(sms * 3), MID_THREADS, MID_MAX * 8, s>>>(
         tmp_j, tmp_d, ws.offsets, row_begin, ws.mid_rows, ws.mid_count, out_i, out_j, out_d);
@@ -508,13 +510,13 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
     mid_rows_kernel<BIG_MAX><<<(unsigned)sms, MID_THREADS, BIG_MAX * 8, s>>>(
         tmp_j, tmp_d, ws.offsets, row_begin, ws.big_rows, ws.big_count, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("mid_rows_kernel");
-    static bool bucket_attr = false;
-    if (!bucket_attr) {
-        cudaError_t e = cudaFuncSetAttribute(bucket_rows_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             BIG_MAX * 8);
+    static PerDeviceOnce bucket_once;
+    {
+        cudaError_t e = bucket_once.run([&] {
+            return cudaFuncSetAttribute(bucket_rows_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, BIG_MAX * 8);
+        });
         if (e != cudaSuccess) return cuda_status(e, "bucket_rows_kernel attribute");
-        bucket_attr = true;
     }
     bucket_rows_kernel<<<(unsigned)sms, MID_THREADS, BIG_MAX * 8, s>>>(
         tmp_j, tmp_d, ws.offsets, row_begin, n_cols, ws.long_rows, ws.long_count, ws.fb_rows,
