@@ -205,6 +205,15 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) 
                  : "memory");
 }
 
+// Release-semantics remote arrive: orders this thread's earlier TMEM stores
+// (after tcgen05.wait::st) and shared-memory writes before the arrive.
+__device__ __forceinline__ void mbar_arrive_remote_release(uint32_t bar, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+                 : "memory");
+}
+
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                  : "memory");
@@ -492,8 +501,8 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
                                               int64_t col0, int buf, uint32_t aph, int q, int h,
                                               int lane, bool leader, uint32_t tfull) {
     constexpr int HALF = TBN / NSPLIT;   // columns per warp
-    constexpr int NCH = HALF / 32;       // 32-column chunks per warp (4 or 2)
-    static_assert(NCH == 2 || NCH == 4, "a warp covers 64 or 128 columns");
+    constexpr int NCH = HALF / 32;       // 32-column chunks per warp (1, 2 or 4)
+    static_assert(NCH == 1 || NCH == 2 || NCH == 4, "a warp covers 32, 64 or 128 columns");
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     const int64_t iw = row0 + q * 32;
     const int64_t i = iw + lane;
@@ -507,18 +516,18 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
     mbar_wait2(tfull, aph, (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
     tc_fence_after();
     uint32_t r0[32], r1[32], r2[32], r3[32];
-    if ((a.diag_flags & FASTED_JOIN_DIAG_LDX64) && nchunks == NCH) {
+    if (NCH > 1 && (a.diag_flags & FASTED_JOIN_DIAG_LDX64) && nchunks == NCH) {
         tmem_ld64(tcol, r0, r1);
         if (NCH > 2) tmem_ld64(tcol + 64u, r2, r3);
     } else {
         if (nchunks > 0) tmem_ld32(tcol, r0);
-        if (nchunks > 1) tmem_ld32(tcol + 32u, r1);
+        if (NCH > 1 && nchunks > 1) tmem_ld32(tcol + 32u, r1);
         if (NCH > 2 && nchunks > 2) tmem_ld32(tcol + 64u, r2);
         if (NCH > 2 && nchunks > 3) tmem_ld32(tcol + 96u, r3);
     }
     if (nchunks > 0) {
         tmem_ld_wait(r0);
-        tmem_ld_wait(r1);
+        if (NCH > 1) tmem_ld_wait(r1);
         if (NCH > 2) {
             tmem_ld_wait(r2);
             tmem_ld_wait(r3);
@@ -537,12 +546,13 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
     // a dependent AND chain per 32-column chunk (measured at 1M x 128: the
     // per-chunk form cost 50 ms of a 231 ms join).
     if (nchunks == NCH && !((jb < iw + 32) && (iw < jb + HALF))) {
-        uint32_t all = and_tree32(r0) & and_tree32(r1);
+        uint32_t all = and_tree32(r0);
+        if (NCH > 1) all &= and_tree32(r1);
         if (NCH > 2) all &= and_tree32(r2) & and_tree32(r3);
         if (!__any_sync(0xffffffffu, (int)all >= 0)) return;
     }
     if (nchunks > 0) epi_chunk(a, wr, r0, jb, i, iw, row_ok);
-    if (nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok);
+    if (NCH > 1 && nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok);
     if (NCH > 2 && nchunks > 2) epi_chunk(a, wr, r2, jb + 64, i, iw, row_ok);
     if (NCH > 2 && nchunks > 3) epi_chunk(a, wr, r3, jb + 96, i, iw, row_ok);
 }
@@ -1338,6 +1348,292 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
     }
 }
 
+// ---------------------------------------------------------------------------
+// TMEM-A variant (d_pad <= 128, CTA pair).  The resident kernel at d = 128 is
+// epilogue bound: a 256 x 256 tile is ~1150 MMA cycles and, with only two
+// 256-column accumulators, a tile whose epilogue runs late (hits to write)
+// stalls the MMA.  Narrower tiles with more accumulators need N = 128 MMAs,
+// which re-read A from shared memory twice as often (measured slower).  Here
+// A lives in TMEM instead (tcgen05.mma A-from-TMEM): each CTA's 128-row A
+// panel (d_pad / 2 columns, two FP16 per 32-bit column, one row per lane) is
+// written by four loader warps with tcgen05.st, double buffered per unit, and
+// the 512 TMEM columns hold 2 A panels + THREE 128-column accumulators.
+// B streams through shared memory as in the resident kernel; the tf32
+// augment step keeps both operands in shared memory.
+constexpr int TS_TBN = 128;
+constexpr int TS_NACC = 3;
+constexpr int TS_NEPI = 16;
+constexpr int TS_LOAD_WARP0 = FIRST_EPI_WARP + TS_NEPI;           // 4 A-loader warps
+constexpr int TS_THREADS = (TS_LOAD_WARP0 + 4) * 32;
+constexpr int TS_A_COLS = 64;                                      // d_pad <= 128
+constexpr int TS_ACC0 = 2 * TS_A_COLS;                             // first accumulator column
+constexpr int TS_NB = TS_TBN / 2;                                  // B rows per CTA
+constexpr int TS_STAGE_BYTES = TS_NB * BK * 2 + TS_NB * AUG_ROW_BYTES;   // 10 KB
+constexpr int TS_AUGA_BYTES = BM * AUG_ROW_BYTES;                  // 4 KB
+constexpr int TS_MAX_STAGES = 16;
+constexpr int TS_BARS = 2 * TS_MAX_STAGES + 2 * TS_NACC + 6 + 1;
+constexpr int TS_BAR_REGION = ((TS_BARS * 8 + 4 + 127) / 128) * 128;
+constexpr int TS_WSTAGE = 16;                                      // records per staging buffer
+constexpr uint32_t TS_IDESC_F16 =
+    (1u << 4) | ((uint32_t)(TS_TBN >> 3) << 17) | ((uint32_t)(256 >> 4) << 24);
+constexpr uint32_t TS_IDESC_TF32 = TS_IDESC_F16 | (2u << 7) | (2u << 10);
+static_assert(TS_STAGE_BYTES % 1024 == 0, "stages must stay 1024-aligned");
+
+__device__ __forceinline__ void mma_f16_ts2(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc,
+                                            uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "r"(tmem_a), "l"(bdesc), "r"(TS_IDESC_F16), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+        "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+        "%28, %29, %30, %31, %32};" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+        "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+        "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+        "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+
+__global__ void __launch_bounds__(TS_THREADS, 1)
+join_tc_ts_kernel(const uint4* __restrict__ X, const __grid_constant__ CUtensorMap tmap_xb,
+                  const __grid_constant__ CUtensorMap tmap_aug_a,
+                  const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
+                  const ResSched sch) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    const int S = sch.stages;
+    const uint32_t sAug = base;                                   // 2 x aug A (4 KB each)
+    const uint32_t sB = base + 2 * 4096;
+    const uint32_t bars = sB + (uint32_t)S * TS_STAGE_BYTES;
+    auto full_bar = [&](int st) { return bars + 8u * st; };
+    auto empty_bar = [&](int st) { return bars + 8u * (S + st); };
+    auto tfull_bar = [&](int b) { return bars + 8u * (2 * S + b); };
+    auto tempty_bar = [&](int b) { return bars + 8u * (2 * S + TS_NACC + b); };
+    auto afull_bar = [&](int b) { return bars + 8u * (2 * S + 2 * TS_NACC + b); };       // TMEM A
+    auto augfull_bar = [&](int b) { return bars + 8u * (2 * S + 2 * TS_NACC + 2 + b); }; // TMA aug A
+    auto aempty_bar = [&](int b) { return bars + 8u * (2 * S + 2 * TS_NACC + 4 + b); };
+    const uint32_t slot = bars + 8u * (2 * S + 2 * TS_NACC + 6);
+    volatile uint32_t* slot_ptr = reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - raw));
+    const uint32_t wst_base = bars + TS_BAR_REGION;
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const bool leader = rank == 0;
+    const int64_t unit0 = (int64_t)(blockIdx.x >> 1);
+    const int64_t ustep = (int64_t)(gridDim.x >> 1);
+    constexpr int TILE_M = 2 * BM;
+
+    if (threadIdx.x == 0) {
+        for (int st = 0; st < S; st++) {
+            mbar_init(full_bar(st), 1);
+            mbar_init(empty_bar(st), 1);
+        }
+        for (int b = 0; b < TS_NACC; b++) {
+            mbar_init(tfull_bar(b), 1);
+            mbar_init(tempty_bar(b), TS_NEPI * 2);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(afull_bar(b), 4 * 2);      // the A-loader warps of both CTAs
+            mbar_init(augfull_bar(b), 1);
+            mbar_init(aempty_bar(b), 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_xb))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_a))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_b))
+                     : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *slot_ptr;
+    const int nks = (int)(a.d_pad / UK);   // K=16 steps over the resident A
+
+    if (warp == 0) {
+        // ---------------- TMA producer: aug A per unit, nkb B stages per tile
+        int st = 0;
+        uint32_t ph = 0;
+        int ua = 0;
+        for (int64_t u = unit0; u < sch.units; u += ustep, ++ua) {
+            int rt, ct0, ct1;
+            res_unit_sym<TILE_M, TS_TBN>(sch, a, u, rt, ct0, ct1);
+            const int64_t row0 = a.row_begin + (int64_t)rt * TILE_M;
+            const bool a_hi = row0 + 128 < a.row_end;
+            const int my_a = (int)(row0 + 128 * rank);
+            const int ab = ua & 1;
+            mbar_wait(aempty_bar(ab), ((uint32_t)(ua >> 1) & 1u) ^ 1u);
+            if (elect_one()) {
+                if (leader) mbar_expect_tx(augfull_bar(ab), (a_hi ? 2u : 1u) * TS_AUGA_BYTES);
+                if (leader || a_hi)
+                    tma_load_2d<2>(sAug + (uint32_t)ab * 4096u, &tmap_aug_a, augfull_bar(ab), 0,
+                                   my_a);
+            }
+            __syncwarp();
+            for (int ct = ct0; ct < ct1; ct++) {
+                const int64_t col0 = a.col_begin + (int64_t)ct * TS_TBN;
+                const int cb = (int)(col0 + TS_NB * rank);
+                const bool mine = cb < a.col_end;
+                const bool peer = col0 + TS_NB < a.col_end;
+                for (int kb = 0; kb < sch.nkb; kb++) {
+                    const bool last = kb == sch.nkb - 1;
+                    mbar_wait(empty_bar(st), ph ^ 1u);
+                    const uint32_t fb = full_bar(st);
+                    const uint32_t sa = sB + (uint32_t)st * TS_STAGE_BYTES;
+                    if (elect_one()) {
+                        const uint32_t box = TS_NB * (BK * 2 + (last ? AUG_ROW_BYTES : 0));
+                        if (leader) mbar_expect_tx(fb, (1u + (peer ? 1u : 0u)) * box);
+                        if (mine) {
+                            tma_load_2d<2>(sa, &tmap_xb, fb, kb * BK, cb);
+                            if (last)
+                                tma_load_2d<2>(sa + TS_NB * BK * 2, &tmap_aug_b, fb, 0, cb);
+                        }
+                    }
+                    __syncwarp();
+                    if (++st == S) {
+                        st = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (leader CTA)
+        if (leader) {
+            int st = 0;
+            uint32_t ph = 0;
+            int lt = 0, ua = 0;
+            for (int64_t u = unit0; u < sch.units; u += ustep, ++ua) {
+                int rt, ct0, ct1;
+                res_unit_sym<TILE_M, TS_TBN>(sch, a, u, rt, ct0, ct1);
+                const int ab = ua & 1;
+                const uint32_t aph = (uint32_t)(ua >> 1) & 1u;
+                mbar_wait(afull_bar(ab), aph);
+                mbar_wait(augfull_bar(ab), aph);
+                tc_fence_after();
+                const uint32_t atm = tmem_base + (uint32_t)(ab * TS_A_COLS);
+                for (int ct = ct0; ct < ct1; ct++, ++lt) {
+                    const int buf = lt % TS_NACC;
+                    mbar_wait(tempty_bar(buf), ((uint32_t)(lt / TS_NACC) & 1u) ^ 1u);
+                    tc_fence_after();
+                    const uint32_t dtm = tmem_base + (uint32_t)(TS_ACC0 + buf * TS_TBN);
+                    for (int kb = 0; kb < sch.nkb; kb++) {
+                        mbar_wait(full_bar(st), ph);
+                        tc_fence_after();
+                        const uint32_t sa = sB + (uint32_t)st * TS_STAGE_BYTES;
+                        const uint64_t bd = sw128_desc(sa);
+                        if (elect_one()) {
+#pragma unroll
+                            for (int kk = 0; kk < BK / UK; kk++) {
+                                const int k16 = kb * (BK / UK) + kk;
+                                if (k16 < nks)
+                                    mma_f16_ts2(dtm, atm + (uint32_t)(k16 * (UK / 2)),
+                                                bd + (uint64_t)((kk * UK * 2) >> 4),
+                                                k16 != 0 ? 1u : 0u);
+                            }
+                            if (kb == sch.nkb - 1)
+                                mma_tf32<2>(dtm, sw32_desc(sAug + (uint32_t)ab * 4096u),
+                                            sw32_desc(sa + TS_NB * BK * 2), TS_IDESC_TF32);
+                            mma_commit<2>(empty_bar(st));
+                        }
+                        __syncwarp();
+                        if (++st == S) {
+                            st = 0;
+                            ph ^= 1u;
+                        }
+                    }
+                    if (elect_one()) mma_commit<2>(tfull_bar(buf));
+                    __syncwarp();
+                }
+                if (elect_one()) mma_commit<2>(aempty_bar(ab));
+                __syncwarp();
+            }
+        }
+    } else if (warp >= TS_LOAD_WARP0) {
+        // ---------------- A loaders: this CTA's 128 rows into TMEM, one row per lane
+        const int q = warp & 3;
+        int ua = 0;
+        for (int64_t u = unit0; u < sch.units; u += ustep, ++ua) {
+            int rt, ct0, ct1;
+            res_unit_sym<TILE_M, TS_TBN>(sch, a, u, rt, ct0, ct1);
+            const int64_t row = a.row_begin + (int64_t)rt * TILE_M + 128 * rank + 32 * q + lane;
+            const int ab = ua & 1;
+            mbar_wait(aempty_bar(ab), ((uint32_t)(ua >> 1) & 1u) ^ 1u);
+            const int words = (int)(a.d_pad / 2);        // FP16 pairs in the row
+            const uint4* src = X + row * (a.d_pad / 8);
+            const uint32_t tdst =
+                tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(ab * TS_A_COLS);
+#pragma unroll
+            for (int half = 0; half < 2; half++) {   // 32 columns (64 FP16) at a time
+                uint32_t v[32];
+#pragma unroll
+                for (int c = 0; c < 8; c++) {
+                    const int w0 = half * 32 + 4 * c;
+                    const uint4 w = (row < a.n_pad && w0 < words) ? __ldg(src + half * 8 + c)
+                                                                  : make_uint4(0u, 0u, 0u, 0u);
+                    v[4 * c] = w.x;
+                    v[4 * c + 1] = w.y;
+                    v[4 * c + 2] = w.z;
+                    v[4 * c + 3] = w.w;
+                }
+                tmem_st32(tdst + (uint32_t)(half * 32), v);
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader) mbar_arrive(afull_bar(ab));
+                else mbar_arrive_remote_release(afull_bar(ab), 0);
+            }
+        }
+    } else {
+        // ---------------- epilogue: 16 warps, 32 x 32 each of a 128-column accumulator
+        const int q = warp & 3;
+        const int h = (warp - FIRST_EPI_WARP) >> 2;
+        StagedWriter<TS_WSTAGE> wr;
+        writer_init(wr, wst_base + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * TS_WSTAGE * 16);
+        int lt = 0;
+        for (int64_t u = unit0; u < sch.units; u += ustep) {
+            int rt, ct0, ct1;
+            res_unit_sym<TILE_M, TS_TBN>(sch, a, u, rt, ct0, ct1);
+            const int64_t row0 = a.row_begin + (int64_t)rt * TILE_M + 128 * rank;
+            for (int ct = ct0; ct < ct1; ct++, ++lt) {
+                const int buf = lt % TS_NACC;
+                epilogue_tile<2, TS_TBN, 4>(a, wr, tmem_base + TS_ACC0, tempty_bar(buf), row0,
+                                            a.col_begin + (int64_t)ct * TS_TBN, buf,
+                                            (uint32_t)(lt / TS_NACC) & 1u, q, h, lane, leader,
+                                            tfull_bar(buf));
+            }
+        }
+        writer_finish(wr, a);
+    }
+
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS)
+                     : "memory");
+}
+
 // Exact split of an FP32 value into three TF32 values (10-bit mantissas,
 // low 13 bits zero) whose sum is the input: 3 x 11 significant bits >= 24.
 __device__ __forceinline__ void split_tf32(float x, float& h1, float& h2, float& h3) {
@@ -1579,6 +1875,53 @@ const char* join_tc_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, bool 
     }
 }
 
+// TMEM-A launch (d_pad <= 128, CTA pair).
+static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUtensorMap& ma,
+                             const CUtensorMap& mbb, const JoinArgs& a, cudaStream_t s) {
+    using namespace tc;
+    constexpr int SMEM_MAX = 227 * 1024;
+    auto kern = join_tc_ts_kernel;
+    static PerDeviceOnce attr_once;
+    {
+        cudaError_t e = attr_once.run([&] {
+            return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SMEM_MAX);
+        });
+        if (e != cudaSuccess) return e;
+    }
+    ResSched sch;
+    sch.nkb = (int)((a.d_pad + BK - 1) / BK);
+    sch.na = 2;
+    sch.a_buf_bytes = 0;
+    const int wst = TS_NEPI * 2 * TS_WSTAGE * 16;
+    const int fixed = 2 * 4096 + TS_BAR_REGION + wst + 1024;
+    sch.stages = (SMEM_MAX - fixed) / TS_STAGE_BYTES;
+    if (sch.stages > TS_MAX_STAGES) sch.stages = TS_MAX_STAGES;
+    sch.row_tiles = (int)((a.row_end - a.row_begin + 2 * BM - 1) / (2 * BM));
+    sch.col_tiles = (int)((a.col_end - a.col_begin + TS_TBN - 1) / TS_TBN);
+    int seg = env_int("FASTED_SEG_TILES", 16384 / TS_TBN);
+    if (seg < 1) seg = 1;
+    sch.nsegs = (sch.col_tiles + seg - 1) / seg;
+    sch.units = (int64_t)sch.row_tiles * sch.nsegs;
+    const int smem = fixed + sch.stages * TS_STAGE_BYTES;
+    const int64_t slots = sm_count_current() / 2;
+    const int64_t work = sch.units < slots ? sch.units : slots;
+    if (work <= 0) return cudaSuccess;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(work * 2));
+    cfg.blockDim = dim3(TS_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint4*>(X), mxb, ma, mbb, a, sch);
+}
+
 int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     using namespace tc;
     if ((a.d_pad % 8) != 0 || (reinterpret_cast<uintptr_t>(X) & 15u) != 0) {
@@ -1666,7 +2009,8 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     // FASTED_RES_BN = 256 (default: two accumulators) or 128 (four; measured
     // slower: 372 vs 283 ms at 1M x 128, the N=128 MMAs re-read A per 64 cycles).
     if (variant == TC_RESIDENT) {
-        const int tbn = env_int("FASTED_RES_BN", 256) == 128 ? 128 : 256;
+        const bool ts = cg == 2 && a.d_pad <= 128 && env_int("FASTED_TS", 0) != 0;
+        const int tbn = ts ? 128 : env_int("FASTED_RES_BN", 256) == 128 ? 128 : 256;
         const int nb = tbn / cg, bbox = nb < 128 ? nb : 128;
         CUtensorMap mxb, mbb;
         st = encode_2d(&mxb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, X, a.d_pad, a.n_pad, a.d_pad * 2,
@@ -1683,7 +2027,9 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         // one box: 253.8-253.9 ms with 16 vs 269-319 ms with 8 -- the shorter
         // per-warp chain per tile also removes the run-to-run spread
         // (profiles/round1/tune_c3_epi_ab_session2.txt).
-        if (cg == 2)
+        if (ts)
+            e = launch_ts(X, mxb, ma, mbb, a, s);
+        else if (cg == 2)
             e = tbn == 128 ? launch_res<2, 128, 8>(mx, mxb, ma, mbb, a, s)
                 : env_int("FASTED_RES_EPI", 16) == 16 ? launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s)
                            : launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);

@@ -67,6 +67,7 @@ for cfg in configs:
     os.environ["FASTED_RES_EPI"] = kv.get("EPI", "16")
     os.environ["FASTED_STREAM_EPI"] = kv.get("SEPI", "16")
     os.environ["FASTED_MC_EPI"] = kv.get("MEPI", "16")
+    os.environ["FASTED_TS"] = kv.get("TS", "0")
     os.environ["FASTED_DYN"] = kv.get("DYN", "1")
     flags = int(kv.get("F", "0"))
     engine.join_raw(dd, es, flags, (0, dd.n_dev), (0, dd.n_dev), rec, cap, cnt, stream.cuda_stream)

@@ -590,3 +590,36 @@ def test_tc_extreme_shapes_band_parity(oracle, n, d, eps):
         rep = _band_ok(oracle, hd, rs, oi, oj, od, eps)
         assert rep.ok, (env, rep)
         assert len(rs) >= n
+
+
+@pytest.mark.parametrize("n,d,eps", [(3000, 128, 3.7), (2999, 100, 3.3), (1100, 16, 1.0),
+                                     (5000, 64, 2.6), (777, 120, 3.5)])
+def test_tmem_a_kernel_bit_identical(n, d, eps):
+    """The TMEM-A kernel (A panel in tensor memory, three 128-column
+    accumulators) issues the same per-element K-ordered MMA chain as the
+    resident kernel: identical bits, also on a ragged shard range and under
+    the symmetric schedule."""
+    hd = F.to_half(F.generate_synthetic(n, d, seed=n + 5 * d))
+    ref = _tc_variant(hd, eps, FASTED_TS=0)
+    assert len(ref[0]) > n
+    ts = _tc_variant(hd, eps, FASTED_TS=1)
+    for x, y in zip(ref, ts):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    n_dev = -(-hd.n_padded // 128) * 128
+    rows, cols = (128, min(n_dev, 1152)), (256, n_dev)
+    ref = _tc_variant(hd, eps, rows, cols, FASTED_TS=0)
+    ts = _tc_variant(hd, eps, rows, cols, FASTED_TS=1, FASTED_SEG_TILES=3)
+    for x, y in zip(ref, ts):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    old = os.environ.get("FASTED_TS")
+    os.environ["FASTED_TS"] = "1"
+    try:
+        sym = F.self_join(hd, eps, symmetric=True)
+    finally:
+        if old is None:
+            os.environ.pop("FASTED_TS", None)
+        else:
+            os.environ["FASTED_TS"] = old
+    full = F.self_join(hd, eps)
+    key = lambda r: set(zip(r.i.tolist(), r.j.tolist()))
+    assert len(key(sym) ^ key(full)) <= max(2, len(full) // 10000)
