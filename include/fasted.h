@@ -29,6 +29,8 @@
  *                      is compute_block_tile itself
  *   fasted_sort_pairs: tiling.make_result_set     tiling.py:116-122
  *                      (and the merge, tiling.py:346-351)
+ *   fasted_fp64_rows : oracle.brute_force_fp64    oracle.py:43-64 (sampled rows,
+ *                      for analysis.overlap_accuracy at scale)
  */
 #ifndef FASTED_H_
 #define FASTED_H_

@@ -623,3 +623,26 @@ def test_tmem_a_kernel_bit_identical(n, d, eps):
     full = F.self_join(hd, eps)
     key = lambda r: set(zip(r.i.tolist(), r.j.tolist()))
     assert len(key(sym) ^ key(full)) <= max(2, len(full) // 10000)
+
+
+@pytest.mark.slow
+def test_c5_rows_at_full_column_range(oracle):
+    """C5 (5M x 384) at S ~ 1000: two sampled row blocks against all 5M
+    columns -- the exact kernel equals the C oracle bit for bit, and the
+    product path meets the band contract against it."""
+    n, d, eps = 5_000_000, 384, 7.1352369182727085
+    hd = F.to_half(F.generate_synthetic(n, d, seed=12345))
+    dd = engine.upload(hd, 0)
+    es = float(oracle.eps_sq_of(eps))
+    for rb in (0, 23456):
+        rows = (rb * 128, rb * 128 + 128)
+        ex = engine.to_host(engine.join_device(dd, es, rows=rows, exact=True))
+        tc = engine.to_host(engine.join_device(dd, es, rows=rows))
+        oi, oj, od = oracle.join(hd.values, hd.norms, n, eps, rows=rows)
+        assert np.array_equal(oi, ex[0]) and np.array_equal(oj, ex[1])
+        assert np.array_equal(od.view(np.uint32), ex[2].view(np.uint32))
+        assert len(ex[0]) > 128 * 500
+        rep = F.band_compare(tc[0], tc[1], tc[2], ex[0], ex[1], ex[2], es,
+                             lambda i, j: oracle.pair_d2(hd.values, hd.norms, i, j))
+        print("C5 row block", rb, rep)
+        assert rep.ok, rep
