@@ -75,7 +75,14 @@ enum {
     /* 4096: retired (column-scan hit search) */
     FASTED_JOIN_DIAG_SPIN = 8192,    /* accumulator waits spin (no suspend hint)      */
     FASTED_JOIN_DIAG_LDX64 = 16384,  /* epilogue: 32x32b.x64 TMEM loads               */
-    FASTED_JOIN_DIAG_AEVL = 32768    /* CTA pair: A panel loads with L2 evict_last    */
+    FASTED_JOIN_DIAG_AEVL = 32768,   /* CTA pair: A panel loads with L2 evict_last    */
+    FASTED_JOIN_DIAG_TRACE = 65536,  /* resident kernel: per-tile clock64 timeline of
+                                        CTA 0 in the last 266240 bytes of out_records */
+    /* epilogue hit-search A/B (results stay valid): always per-lane masks /
+     * always transposed rows (default: rows for one candidate row in a
+     * 32 x 32 chunk, masks for two or more) */
+    FASTED_JOIN_DIAG_RARE_LM = 131072,
+    FASTED_JOIN_DIAG_RARE_ROWS = 262144
 };
 
 int fasted_abi_version(void);

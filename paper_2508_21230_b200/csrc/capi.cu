@@ -137,11 +137,23 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     a.diag_flags = flags & (FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA |
                             FASTED_JOIN_DIAG_LOADONLY | FASTED_JOIN_DIAG_NOSLOW |
                             FASTED_JOIN_DIAG_SPIN | FASTED_JOIN_DIAG_LDX64 |
-                            FASTED_JOIN_DIAG_AEVL);
+                            FASTED_JOIN_DIAG_AEVL | FASTED_JOIN_DIAG_TRACE |
+                            FASTED_JOIN_DIAG_RARE_LM | FASTED_JOIN_DIAG_RARE_ROWS);
     a.out = reinterpret_cast<uint4*>(out_records);
     a.capacity = count_only ? 0ull : (unsigned long long)capacity;
     a.count = count;
     a.gram_diag = nullptr;
+    a.trace = nullptr;
+    if (flags & FASTED_JOIN_DIAG_TRACE) {
+        const unsigned long long trace_recs = TRACE_WORDS / 2;
+        if (count_only || a.capacity < trace_recs) {
+            set_error("fasted_join: FASTED_JOIN_DIAG_TRACE needs a record buffer with room for "
+                      "the timeline");
+            return FASTED_ERR_ARGUMENT;
+        }
+        a.capacity -= trace_recs;
+        a.trace = reinterpret_cast<unsigned long long*>(a.out + a.capacity);
+    }
     const __half* X = reinterpret_cast<const __half*>(values16);
     return kind == FASTED_JOIN_EXACT ? launch_join_exact(X, a, s) : launch_join_tc(X, a, s);
 }

@@ -18,7 +18,18 @@ struct JoinArgs {
     unsigned long long capacity;       // record slots available in out
     unsigned long long* count;         // [0] exact pair total, [1] chunks taken
     float* gram_diag;                  // diagonal pre-pass output (tcgen05 kernel), else null
+    unsigned long long* trace;         // FASTED_JOIN_DIAG_TRACE timeline (CTA 0), else null
 };
+
+// FASTED_JOIN_DIAG_TRACE layout (resident kernel, CTA 0, first TRACE_TILES
+// accumulator tiles, SM clock64): [t][2] MMA warp {tempty passed, tfull
+// committed}, then [t][w][8] per epilogue warp {tfull passed, TMEM loads
+// landed, tempty arrived, tile done, slice vote done, rare chunk: hit masks
+// built, rare chunk: records appended, 1 if a rare chunk ran}.
+constexpr int TRACE_TILES = 256;
+constexpr int TRACE_EPI_WARPS = 16;
+constexpr unsigned long long TRACE_WORDS =
+    (unsigned long long)TRACE_TILES * (2 + 8 * TRACE_EPI_WARPS);
 
 // ((-2 a) + s_i) + s_j in FP32 round-to-nearest, clamped at 0
 // (mma.py:143-157).  -2a is exact, so the first step is one RN FMA.
@@ -108,10 +119,17 @@ struct StagedWriter {
     uint32_t sbuf;              // shared address of this warp's 2 x STAGE x 16 bytes
     unsigned long long total;   // pairs found by this warp
     uint64_t policy;            // L2 evict_first cache policy for the record stream
+    uint32_t stash;             // shared address of this warp's 128-byte row stash
 };
 
+// Per-warp row stash of the tcgen05 epilogues (epi_chunk's transposed hit
+// search): one lane's 32 accumulator words.
+constexpr int EPI_STASH_BYTES = 128;
+
 template <int STAGE>
-__device__ __forceinline__ void writer_init(StagedWriter<STAGE>& w, uint32_t sbuf) {
+__device__ __forceinline__ void writer_init(StagedWriter<STAGE>& w, uint32_t sbuf,
+                                            uint32_t stash = 0) {
+    w.stash = stash;
     w.base = ~0ull;
     w.flushed = 0;
     w.fill = 0;
@@ -123,6 +141,12 @@ __device__ __forceinline__ void writer_init(StagedWriter<STAGE>& w, uint32_t sbu
     // default policy the join re-read 861 GB from HBM per 75K-row slice
     // against 40 GB count-only, L2 hit rate 61% vs 97%).
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(w.policy));
+}
+
+__device__ __forceinline__ uint32_t ld_shared_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
 }
 
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {

@@ -75,12 +75,15 @@ constexpr int BAR_BYTES = 256;
 // records of 16 bytes.
 constexpr int WSTAGE = 64;
 constexpr int WSTAGE_BYTES = NUM_EPI_WARPS * 2 * WSTAGE * 16;   // 16 KB
+// epi_chunk row stashes, up to 16 epilogue warps x 128 bytes, after the staging
+constexpr int STASH_BYTES = 16 * EPI_STASH_BYTES;
 
 template <int CG>
 struct Cfg {
     static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of B
     static constexpr int STAGES = CG == 2 ? 6 : 4;
-    static constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + BAR_BYTES + WSTAGE_BYTES + 1024;
+    static constexpr int SMEM_BYTES =
+        STAGES * (A_BYTES + B_BYTES) + BAR_BYTES + WSTAGE_BYTES + STASH_BYTES + 1024;
     static constexpr int TILE_M = BM * CG;                // rows per tile
     // Instruction descriptors: D=F32 (bits 4-5 = 1); A/B format at bits
     // 7-9 / 10-12 (F16 = 0, TF32 = 2); both K-major; N>>3 at 17-22; M>>4 at
@@ -203,6 +206,19 @@ __device__ __forceinline__ void mbar_arrive_remote(uint32_t bar, uint32_t rank) 
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(bar), "r"(rank));
     asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
                  : "memory");
+}
+
+// Relaxed arrive on a barrier address already mapped into the cluster
+// window (mapa hoisted out of the per-tile loop).
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t remote) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(addr), "r"(rank));
+    return remote;
 }
 
 // Release-semantics remote arrive: orders this thread's earlier TMEM stores
@@ -423,30 +439,62 @@ __device__ __forceinline__ uint32_t pick32(const uint32_t (&r)[32], uint32_t e) 
     return (e & 1u) ? t[1] : t[0];
 }
 
-// AND of 32 words as a balanced tree: the sign bit of the result is clear
-// iff some word's sign bit is clear (some D >= 0, i.e. a hit).
+// SM clock read ordered after `dep` is available (FASTED_JOIN_DIAG_TRACE:
+// makes the stamp wait for the TMEM loads that produce it).
+__device__ __forceinline__ unsigned long long clock_after(uint32_t dep) {
+    unsigned long long t;
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0x7fc00001;\n\t"
+                 "@p mov.u64 %0, %%clock64;\n\t@!p mov.u64 %0, 0;\n\t}"
+                 : "=l"(t)
+                 : "r"(dep)
+                 : "memory");
+    return t;
+}
+
+// AND of 32 words: the sign bit of the result is clear iff some word's sign
+// bit is clear (some D >= 0, i.e. a hit).  A depth-4 tree of 3-input LOP3s
+// in inline PTX (from plain C the compiler reassociates a tree into a
+// 32-deep dependent chain; measured equal at 1M x 128 -- the per-tile cost
+// is issue slots, not this latency -- kept for the shorter chain).
+__device__ __forceinline__ uint32_t and3(uint32_t a, uint32_t b, uint32_t c) {
+    uint32_t d;
+    asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 __device__ __forceinline__ uint32_t and_tree32(const uint32_t (&r)[32]) {
-    uint32_t t[16];
+    uint32_t t[11];
 #pragma unroll
-    for (int k = 0; k < 16; k++) t[k] = r[2 * k] & r[2 * k + 1];
-#pragma unroll
-    for (int k = 0; k < 8; k++) t[k] = t[2 * k] & t[2 * k + 1];
-#pragma unroll
-    for (int k = 0; k < 4; k++) t[k] = t[2 * k] & t[2 * k + 1];
-    return (t[0] & t[1]) & (t[2] & t[3]);
+    for (int k = 0; k < 10; k++) t[k] = and3(r[3 * k], r[3 * k + 1], r[3 * k + 2]);
+    t[10] = and3(r[30], r[31], 0xffffffffu);
+    const uint32_t u0 = and3(t[0], t[1], t[2]), u1 = and3(t[3], t[4], t[5]);
+    const uint32_t u2 = and3(t[6], t[7], t[8]), u3 = and3(t[9], t[10], 0xffffffffu);
+    return and3(and3(u0, u1, u2), u3, 0xffffffffu);
 }
 
 // Epilogue of one 32-column chunk (columns jb.., row i = this lane).
 // r[e] = D_{i, jb+e} = (eps^2 - d2) / 2 as FP32 bits.
+//
+// Hit search, transposed: a lane whose row has a candidate (some D >= 0)
+// publishes its 32 words to the warp's shared-memory stash and every lane e
+// tests column e of that row, so one ballot yields the row's hits and each
+// hitting lane holds its own value -- no per-lane 32-bit hit mask, no
+// select tree.  Rows with a candidate are rare (~2 per 32 x 64 slice at
+// S ~ 64), and this path's dependent chain is a few tens of instructions
+// against ~200 for the per-lane mask form it replaced (measured with
+// FASTED_JOIN_DIAG_TRACE at 1M x 128: a warp with a hit came back to the next
+// tile ~2900 cycles late, stalling the MMA warp on the accumulator).
 template <typename W>
 __device__ __forceinline__ void epi_chunk(const JoinArgs& a, W& wr, const uint32_t (&r)[32],
-                                          int64_t jb, int64_t i, int64_t iw, bool row_ok) {
-    // common path: is any D >= 0 (sign bit clear)?  A balanced AND tree
-    // (depth ~5, not a 16-deep chain).
+                                          int64_t jb, int64_t i, int64_t iw, bool row_ok,
+                                          unsigned long long* tr = nullptr) {
+    // common path: is any D >= 0 (sign bit clear)?  A balanced AND tree.
     const uint32_t acc = and_tree32(r);
     const bool diag = (jb < iw + 32) && (iw < jb + 32);   // warp-uniform
-    if (!__any_sync(0xffffffffu, (int)acc >= 0) && !diag) return;
+    const uint32_t rows = __ballot_sync(0xffffffffu, (int)acc >= 0 && row_ok);
+    if (rows == 0u && !diag) return;
     if (a.diag_flags & FASTED_JOIN_DIAG_NOSLOW) return;
+    const uint32_t lane = threadIdx.x & 31u;
     // rare path.  Self pairs first: distance exactly 0 (the reference's
     // a_ii and s_i are the same chain), one append for the whole warp.
     if (diag) {
@@ -454,12 +502,14 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, W& wr, const uint32
         const uint32_t b = __ballot_sync(0xffffffffu, self);
         if (b) writer_append(wr, a, b, self, (uint32_t)(i + 1), (uint32_t)(i + 1), 0.0f);
     }
-    {
-        // Per lane: build the hit mask (sign bits clear), drop the self
-        // column and columns past n_logical; the warp appends one record per
-        // hitting lane per round -- usually one round, hits being sparse.
-        // (A column-scan form -- 32 REDUX.AND per chunk -- measured no faster
-        // at 1M x 128 and doubled the rare-path code; it was removed.)
+    if (tr && lane == 0) tr[5] = clock64();
+    // One candidate row: the transposed search.  Two or more: per-lane hit
+    // masks, all rows at once (serialising rows measured 20% slower at
+    // 60K x 512, where a 32 x 32 chunk holds ~1 pair; A/B flags force either).
+    const bool multi = (rows & (rows - 1u)) != 0u;
+    if (((a.diag_flags & FASTED_JOIN_DIAG_RARE_LM) || multi) &&
+        !(a.diag_flags & FASTED_JOIN_DIAG_RARE_ROWS)) {
+        // per-lane hit masks: all candidate rows at once
         uint32_t lm = 0;
 #pragma unroll
         for (int e = 0; e < 32; e++) lm |= ((~r[e]) >> 31) << e;
@@ -467,8 +517,7 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, W& wr, const uint32
         if (valid < 32) lm &= valid <= 0 ? 0u : ((1u << (uint32_t)valid) - 1u);
         if (i >= jb && i < jb + 32) lm &= ~(1u << (uint32_t)(i - jb));
         if (a.symmetric) {
-            // upper triangle only (j > i); the mirrored record covers (j, i)
-            const int64_t off = i - jb;   // columns jb .. i are not above the diagonal
+            const int64_t off = i - jb;
             if (off >= 31) lm = 0u;
             else if (off >= 0) lm &= ~((2u << (uint32_t)off) - 1u);
         }
@@ -485,7 +534,35 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, W& wr, const uint32
             if (a.symmetric)
                 writer_append(wr, a, b, mine, (uint32_t)(jb + e + 1), (uint32_t)(i + 1), d2);
         }
+        if (tr && lane == 0) tr[6] = clock64();
+        return;
     }
+    const int64_t j = jb + lane;
+    const bool col_ok = j < a.n_logical;
+    uint32_t rest = rows;
+    while (rest != 0u) {
+        const uint32_t src = (uint32_t)(__ffs(rest) - 1);
+        rest &= rest - 1u;
+        if (lane == src) {
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                st_shared_v4(wr.stash + 16u * k,
+                             make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
+        }
+        __syncwarp();
+        const uint32_t v = ld_shared_u32(wr.stash + 4u * lane);
+        __syncwarp();   // the stash is rewritten for the next row
+        const int64_t is = iw + src;
+        // drop the self column and columns past n_logical; symmetric: keep
+        // the upper triangle only (j > i), the mirrored record covers (j, i)
+        const bool hit = (int)v >= 0 && col_ok && j != is && (!a.symmetric || j > is);
+        const uint32_t b = __ballot_sync(0xffffffffu, hit);
+        if (b == 0u) continue;
+        const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
+        writer_append(wr, a, b, hit, (uint32_t)(is + 1), (uint32_t)(j + 1), d2);
+        if (a.symmetric) writer_append(wr, a, b, hit, (uint32_t)(j + 1), (uint32_t)(is + 1), d2);
+    }
+    if (tr && lane == 0) tr[6] = clock64();
 }
 
 // One epilogue warp's share of one finished accumulator of TBN columns:
@@ -553,6 +630,70 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
     }
     if (nchunks > 0) epi_chunk(a, wr, r0, jb, i, iw, row_ok);
     if (NCH > 1 && nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok);
+    if (NCH > 2 && nchunks > 2) epi_chunk(a, wr, r2, jb + 64, i, iw, row_ok);
+    if (NCH > 2 && nchunks > 3) epi_chunk(a, wr, r3, jb + 96, i, iw, row_ok);
+}
+
+// The resident kernel's per-tile epilogue, lean form.  Everything that is
+// fixed for a work unit (row validity, which tiles are full, which one holds
+// the diagonal, the accumulator-release address) is computed once per unit
+// by the caller, so the common tile -- full slice, off the diagonal, no hit --
+// is: wait tfull, two TMEM loads, release the accumulator, a 64-word AND
+// tree, one vote.  Measured with FASTED_JOIN_DIAG_TRACE at 1M x 128 (one
+// row slice): the general epilogue_tile spent ~200 instructions per
+// warp-tile, 16 warps x 200 issue slots against a ~1150-cycle tile, and the
+// warps that found a hit (15% of warp-tiles) then took ~2900 cycles to get
+// back to the next tile, stalling the MMA warp on the accumulator.
+template <int CG, int TBN, int NSPLIT, bool TRACE, typename W>
+__device__ __forceinline__ void res_epi_tile(const JoinArgs& a, W& wr, uint32_t tcol,
+                                             uint32_t tfull, uint32_t aph, uint32_t tempty,
+                                             bool local_release, bool spin, int dflags,
+                                             int nchunks, bool fast, int64_t jb, int64_t i,
+                                             int64_t iw, bool row_ok, int lane,
+                                             unsigned long long* tr) {
+    constexpr int HALF = TBN / NSPLIT;
+    constexpr int NCH = HALF / 32;
+    static_assert(NCH == 1 || NCH == 2 || NCH == 4, "a warp covers 32, 64 or 128 columns");
+    mbar_wait2(tfull, aph, spin);
+    tc_fence_after();
+    if (TRACE && tr && lane == 0) tr[0] = clock64();
+    uint32_t r0[32], r1[32], r2[32], r3[32];
+    if (nchunks > 0) tmem_ld32(tcol, r0);
+    if (NCH > 1 && nchunks > 1) tmem_ld32(tcol + 32u, r1);
+    if (NCH > 2 && nchunks > 2) tmem_ld32(tcol + 64u, r2);
+    if (NCH > 2 && nchunks > 3) tmem_ld32(tcol + 96u, r3);
+    if (nchunks > 0) {
+        tmem_ld_wait(r0);
+        if (NCH > 1) tmem_ld_wait(r1);
+        if (NCH > 2) {
+            tmem_ld_wait(r2);
+            tmem_ld_wait(r3);
+        }
+    }
+    if (TRACE && tr && lane == 0)
+        tr[1] = clock_after(r0[0] ^ r0[31] ^ (NCH > 1 ? r1[31] : 0u));
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+        if (local_release) mbar_arrive_relaxed(tempty);
+        else mbar_arrive_cluster(tempty);
+        if (TRACE && tr) tr[2] = clock64();
+    }
+    if (dflags & FASTED_JOIN_DIAG_LOADONLY) return;
+    if (fast) {
+        uint32_t all = and_tree32(r0);
+        if (NCH > 1) all &= and_tree32(r1);
+        if (NCH > 2) all &= and_tree32(r2) & and_tree32(r3);
+        const bool any = __any_sync(0xffffffffu, (int)all >= 0);
+        if (TRACE && tr && lane == 0) {
+            tr[4] = clock64();
+            tr[7] = any ? 1ull : 0ull;
+        }
+        if (!any) return;
+    }
+    unsigned long long* const trc = TRACE ? tr : nullptr;
+    if (nchunks > 0) epi_chunk(a, wr, r0, jb, i, iw, row_ok, trc);
+    if (NCH > 1 && nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok, trc);
     if (NCH > 2 && nchunks > 2) epi_chunk(a, wr, r2, jb + 64, i, iw, row_ok);
     if (NCH > 2 && nchunks > 3) epi_chunk(a, wr, r3, jb + 96, i, iw, row_ok);
 }
@@ -769,7 +910,9 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         // warps, 32 with 16)
         constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;
         StagedWriter<WST> wr;
-        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
+        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16,
+                    bars + BAR_BYTES + WSTAGE_BYTES +
+                        (uint32_t)(warp - FIRST_EPI_WARP) * EPI_STASH_BYTES);
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -854,7 +997,7 @@ __device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
 
 constexpr int MC_STAGES = 4;
 constexpr int MC_SMEM_BYTES =
-    MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + WSTAGE_BYTES + 1024;
+    MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + WSTAGE_BYTES + STASH_BYTES + 1024;
 
 template <int NEPI>
 __global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI) * 32, 1)
@@ -1005,7 +1148,9 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         const int h = (warp - FIRST_EPI_WARP) >> 2;
         constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;   // 16 KB of staging either way
         StagedWriter<WST> wr;
-        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
+        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16,
+                    bars + BAR_BYTES + WSTAGE_BYTES +
+                        (uint32_t)(warp - FIRST_EPI_WARP) * EPI_STASH_BYTES);
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -1108,7 +1253,7 @@ __device__ __forceinline__ void res_unit_sym(const ResSched& s, const JoinArgs& 
     }
 }
 
-template <int CG, int TBN, int NEPI>
+template <int CG, int TBN, int NEPI, bool TRACE = false>
 __global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI) * 32, 1)
 join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                    const __grid_constant__ CUtensorMap tmap_xb,
@@ -1274,6 +1419,11 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                     mbar_wait2(tempty_bar(buf), ((uint32_t)(lt / NACC) & 1u) ^ 1u,
                                (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
                     tc_fence_after();
+                    unsigned long long* tr =
+                        (TRACE && a.trace && blockIdx.x == 0 && lt < TRACE_TILES)
+                            ? a.trace + 2 * lt
+                            : nullptr;
+                    if (TRACE && tr && lane == 0) tr[0] = clock64();
                     const uint32_t dtm = tmem_base + (uint32_t)(buf * TBN);
                     for (int kb = 0; kb < sch.nkb; kb++) {
                         mbar_wait(full_bar(s), ph);
@@ -1303,6 +1453,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                     }
                     if (elect_one()) mma_commit<CG>(tfull_bar(buf));
                     __syncwarp();
+                    if (TRACE && tr && lane == 0) tr[1] = clock64();
                 }
                 if (elect_one()) mma_commit<CG>(aempty_bar(ab));
                 __syncwarp();
@@ -1311,23 +1462,65 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         __syncwarp();
     } else {
         // ---------------- epilogue
+        constexpr int NSPLIT = NEPI / 4;
+        constexpr int HALF = TBN / NSPLIT;            // columns per warp
+        constexpr int NCH = HALF / 32;
         const int q = warp & 3;                       // TMEM lane quarter
         const int h = (warp - FIRST_EPI_WARP) >> 2;   // column group (NEPI / 4 of them)
         constexpr int RWS = RES_WSTAGE_TOTAL / (2 * NEPI) * 2;   // 16 (NEPI 16) / 32 (NEPI 8)
         StagedWriter<RWS> wr;
-        writer_init(wr, bars + C::BAR_REGION +
-                            (uint32_t)(warp - FIRST_EPI_WARP) * 2 * RWS * 16);
+        writer_init(wr, bars + C::BAR_REGION + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * RWS * 16,
+                    bars + C::BAR_REGION + (uint32_t)(NEPI * 2 * RWS * 16) +
+                        (uint32_t)(warp - FIRST_EPI_WARP) * EPI_STASH_BYTES);
+        static_assert(NACC == 2, "lean epilogue assumes two accumulators");
+        const uint32_t tcol0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * HALF);
+        const bool local_release = CG == 1 || leader;
+        const uint32_t release0 = local_release ? tempty_bar(0) : mapa_shared(tempty_bar(0), 0);
+        const uint32_t release1 = local_release ? tempty_bar(1) : mapa_shared(tempty_bar(1), 0);
+        const uint32_t tfull0 = tfull_bar(0);
+        const int dflags = a.diag_flags;
+        const bool spin = (dflags & FASTED_JOIN_DIAG_SPIN) != 0;
+        const bool noepi = (dflags & FASTED_JOIN_DIAG_NOEPI) != 0;
+        // 32-bit point indices (n_pad < 2^31; records hold 32-bit ids anyway);
+        // this warp's first column in tile 0 of the range
+        const int jbase = (int)a.col_begin + h * HALF;
+        const int col_end = (int)a.col_end;
         int lt = 0;
-        for (int64_t u = unit0; u < sch.units; u += ustep) {
+        uint32_t buf = 0, aph = 0;
+        for (int u = (int)unit0; u < (int)sch.units; u += (int)ustep) {
             int rt, ct0, ct1;
             res_unit_sym<C::TILE_M, TBN>(sch, a, u, rt, ct0, ct1);
-            const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M + 128 * rank;
+            const int row0 = (int)a.row_begin + rt * C::TILE_M + 128 * (int)rank;
+            const int iw = row0 + q * 32;
+            const int i = iw + lane;
+            const bool row_ok = i < a.n_logical && i < a.row_end;
+            const bool rows_in = row0 < a.row_end && !noepi;
+            // tiles whose slice [jb, jb + HALF) lies inside [.., col_end)
+            const int room = col_end - jbase - HALF;
+            int ct_full = (room < 0 || !rows_in) ? 0 : room / TBN + 1;
+            // the one tile (if any) whose slice meets rows [iw, iw + 32):
+            // jb in (iw - HALF, iw + 32), jb = jbase + ct * TBN
+            const int x = iw + 31 - jbase;
+            const int ct_diag = (x >= 0 && (x / TBN) * TBN > x - 31 - HALF) ? x / TBN : -1;
             for (int ct = ct0; ct < ct1; ct++, ++lt) {
-                const int buf = lt % NACC;
-                epilogue_tile<CG, TBN, NEPI / 4>(a, wr, tmem_base, tempty_bar(buf), row0,
-                                       a.col_begin + (int64_t)ct * TBN, buf,
-                                       (uint32_t)(lt / NACC) & 1u, q, h, lane, leader,
-                                       tfull_bar(buf));
+                const int jb = jbase + ct * TBN;
+                int nchunks = NCH;
+                if (ct >= ct_full) {
+                    const int left = col_end - jb;
+                    nchunks = (!rows_in || left <= 0) ? 0
+                              : (left >= HALF ? NCH : left / 32);
+                }
+                const bool fast = ct < ct_full && ct != ct_diag;
+                unsigned long long* tr = nullptr;
+                if (TRACE && a.trace && blockIdx.x == 0 && lt < TRACE_TILES)
+                    tr = a.trace + 2 * TRACE_TILES +
+                         8 * (lt * TRACE_EPI_WARPS + (warp - FIRST_EPI_WARP));
+                res_epi_tile<CG, TBN, NSPLIT, TRACE>(
+                    a, wr, tcol0 + buf * TBN, tfull0 + 8u * buf, aph, buf ? release1 : release0,
+                    local_release, spin, dflags, nchunks, fast, jb, i, iw, row_ok, lane, tr);
+                if (TRACE && tr && lane == 0) tr[3] = clock64();
+                buf ^= 1u;
+                aph ^= buf ^ 1u;   // phase flips after buffer 1
             }
         }
         writer_finish(wr, a);
@@ -1608,7 +1801,9 @@ join_tc_ts_kernel(const uint4* __restrict__ X, const __grid_constant__ CUtensorM
         const int q = warp & 3;
         const int h = (warp - FIRST_EPI_WARP) >> 2;
         StagedWriter<TS_WSTAGE> wr;
-        writer_init(wr, wst_base + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * TS_WSTAGE * 16);
+        writer_init(wr, wst_base + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * TS_WSTAGE * 16,
+                    wst_base + (uint32_t)(TS_NEPI * 2 * TS_WSTAGE * 16) +
+                        (uint32_t)(warp - FIRST_EPI_WARP) * EPI_STASH_BYTES);
         int lt = 0;
         for (int64_t u = unit0; u < sch.units; u += ustep) {
             int rt, ct0, ct1;
@@ -1792,8 +1987,17 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     using namespace tc;
     using C = ResCfg<CG, TBN>;
     constexpr int SMEM_MAX = 227 * 1024;
-    auto kern = join_tc_res_kernel<CG, TBN, NEPI>;
-    static PerDeviceOnce attr_once;
+    constexpr bool CAN_TRACE = CG == 2 && TBN == 256 && NEPI == 16;
+    auto kern = (CAN_TRACE && a.trace) ? join_tc_res_kernel<CG, TBN, NEPI, CAN_TRACE>
+                                       : join_tc_res_kernel<CG, TBN, NEPI, false>;
+    static PerDeviceOnce attr_once, attr_once_trace;
+    if (CAN_TRACE && a.trace) {
+        cudaError_t e = attr_once_trace.run([&] {
+            return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        SMEM_MAX);
+        });
+        if (e != cudaSuccess) return e;
+    } else
     {
         cudaError_t e = attr_once.run([&] {
             return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1804,7 +2008,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     ResSched sch;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.a_buf_bytes = (uint32_t)((sch.nkb * A_BYTES + BM * AUG_ROW_BYTES + 1023) & ~1023);
-    const int wstage = NEPI * 2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16;
+    const int wstage = NEPI * 2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16 + NEPI * EPI_STASH_BYTES;
     const int budget = SMEM_MAX - 1024 - C::BAR_REGION - wstage;
     sch.na = 2 * (int)sch.a_buf_bytes <= 80 * 1024 ? 2 : 1;
     sch.stages = (budget - sch.na * (int)sch.a_buf_bytes) / C::STAGE_BYTES;
@@ -1893,7 +2097,7 @@ static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUte
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.na = 2;
     sch.a_buf_bytes = 0;
-    const int wst = TS_NEPI * 2 * TS_WSTAGE * 16;
+    const int wst = TS_NEPI * 2 * TS_WSTAGE * 16 + TS_NEPI * EPI_STASH_BYTES;
     const int fixed = 2 * 4096 + TS_BAR_REGION + wst + 1024;
     sch.stages = (SMEM_MAX - fixed) / TS_STAGE_BYTES;
     if (sch.stages > TS_MAX_STAGES) sch.stages = TS_MAX_STAGES;
@@ -2005,12 +2209,13 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         cudaFreeAsync(aug, s);
         return cuda_status(e, "aug_prepare_kernel");
     }
-    // Resident-A form for d_pad <= 256 (FASTED_RESIDENT=0 selects streaming);
-    // FASTED_RES_BN = 256 (default: two accumulators) or 128 (four; measured
-    // slower: 372 vs 283 ms at 1M x 128, the N=128 MMAs re-read A per 64 cycles).
+    // Resident-A form for d_pad <= 256 (FASTED_RESIDENT=0 selects streaming),
+    // 256-column tiles, two accumulators.  (128-column tiles with four
+    // accumulators measured slower, 372 vs 283 ms at 1M x 128 -- the N=128
+    // MMAs re-read A every 64 cycles -- and were removed.)
     if (variant == TC_RESIDENT) {
         const bool ts = cg == 2 && a.d_pad <= 128 && env_int("FASTED_TS", 0) != 0;
-        const int tbn = ts ? 128 : env_int("FASTED_RES_BN", 256) == 128 ? 128 : 256;
+        const int tbn = ts ? 128 : 256;
         const int nb = tbn / cg, bbox = nb < 128 ? nb : 128;
         CUtensorMap mxb, mbb;
         st = encode_2d(&mxb, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, X, a.d_pad, a.n_pad, a.d_pad * 2,
@@ -2030,12 +2235,10 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         if (ts)
             e = launch_ts(X, mxb, ma, mbb, a, s);
         else if (cg == 2)
-            e = tbn == 128 ? launch_res<2, 128, 8>(mx, mxb, ma, mbb, a, s)
-                : env_int("FASTED_RES_EPI", 16) == 16 ? launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s)
-                           : launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
+            e = env_int("FASTED_RES_EPI", 16) == 16 ? launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s)
+                                                     : launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
         else
-            e = tbn == 128 ? launch_res<1, 128, 8>(mx, mxb, ma, mbb, a, s)
-                           : launch_res<1, 256, 8>(mx, mxb, ma, mbb, a, s);
+            e = launch_res<1, 256, 8>(mx, mxb, ma, mbb, a, s);
         if (e == cudaSuccess) e = cudaGetLastError();
         cudaFreeAsync(aug, s);
         if (e != cudaSuccess) return cuda_status(e, "join_tc_res_kernel");

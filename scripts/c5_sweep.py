@@ -27,6 +27,9 @@ import paper_2508_21230_b200 as F  # noqa: E402
 from bench import SEED, ClockSampler, load_peaks  # noqa: E402
 from paper_2508_21230_b200 import _lib, engine  # noqa: E402
 
+if os.environ.get("FASTED_LIB"):   # A/B against another build of the library
+    _lib.LIB_PATH = os.path.abspath(os.environ["FASTED_LIB"])
+
 # eps per target selectivity (reference CLI calibrate, sample 4096)
 SWEEP = [("S0 (self pairs only)", 0.0), ("S16", 6.896041752764515), ("S64", 6.97276473038035),
          ("S256", 7.049487707996186), ("S1024", 7.1352369182727085),
@@ -39,7 +42,10 @@ def main():
     ap.add_argument("--shard", default="0/8")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--only", default="")
+    ap.add_argument("--extra-flags", default="0",
+                    help="comma list of diagnostic flag sets to A/B (each row runs once per set)")
     args = ap.parse_args()
+    extras = [int(x) for x in args.extra_flags.split(",")]
     rank, world = (int(x) for x in args.shard.split("/"))
     t0 = time.time()
     hd = F.to_half(F.generate_synthetic(N, D, seed=SEED))
@@ -60,7 +66,7 @@ def main():
     peak_burst, peak_sus, _ = load_peaks()
     cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
     flops = 2.0 * nrows * N * D
-    for label, eps in SWEEP:
+    for (label, eps), extra in [(le, x) for le in SWEEP for x in extras]:
         if args.only and args.only not in label:
             continue
         es = float(np.float32(np.float32(eps) * np.float32(eps)))
@@ -77,8 +83,8 @@ def main():
         engine.join_raw(dd, es, _lib.JOIN_COUNT, rows, (0, dd.n_dev), None, 0, cnt, sp)
         pairs = int(cnt[0].item())
         cap = pairs + engine.max_holes(0)
-        jflags = _lib.JOIN_TC | (_lib.JOIN_LOW_OUTPUT
-                                 if pairs <= engine.LOW_OUTPUT_PER_ROW * nrows else 0)
+        jflags = _lib.JOIN_TC | extra | (_lib.JOIN_LOW_OUTPUT
+                                         if pairs <= engine.LOW_OUTPUT_PER_ROW * nrows else 0)
         count_ms = []
         with ClockSampler(0) as clk_c:
             for _ in range(args.reps):
@@ -100,6 +106,7 @@ def main():
         rec_bytes = slots * engine.RECORD_BYTES
         line = {
             "workload": f"C5 Tiny-shaped synthetic {N}x{D}, {label}", "epsilon": eps,
+            "extra_flags": extra,
             "eps_sq": es, "shard": f"rows {rows[0]}..{rows[1]} ({nrows} points) = rank "
                                    f"{rank} of {world}, x all {N} columns",
             "pairs": pairs, "selectivity": (pairs - nrows) / nrows,

@@ -17,6 +17,9 @@ import paper_2508_21230_b200 as F  # noqa: E402
 from bench import SEED, WORKLOADS  # noqa: E402
 from paper_2508_21230_b200 import _lib, engine  # noqa: E402
 
+if os.environ.get("FASTED_LIB"):   # A/B against another build of the library
+    _lib.LIB_PATH = os.path.abspath(os.environ["FASTED_LIB"])
+
 wl, reps = sys.argv[1], int(sys.argv[2])
 configs = sys.argv[3:] or ["CG=2,G=8192"]
 name, n, d, eps = WORKLOADS[wl]
@@ -62,7 +65,6 @@ for cfg in configs:
         os.environ["FASTED_SEG_TILES"] = kv["SEG"]
     else:
         os.environ.pop("FASTED_SEG_TILES", None)
-    os.environ["FASTED_RES_BN"] = kv.get("BN", "256")
     os.environ["FASTED_MC"] = kv.get("MC", "1")
     os.environ["FASTED_RES_EPI"] = kv.get("EPI", "16")
     os.environ["FASTED_STREAM_EPI"] = kv.get("SEPI", "16")

@@ -353,18 +353,21 @@ def test_resident_kernel_bit_identical_to_streaming(n, d, eps, seg):
     for cg in (2, 1):
         ref = _tc_variant(hd, eps, FASTED_RESIDENT=0, FASTED_CTA_GROUP=cg)
         assert len(ref[0]) > n
-        for bn, epi in ((256, 16), (256, 8), (128, 8)):
+        for epi in (16, 8):
             res = _tc_variant(hd, eps, FASTED_RESIDENT=1, FASTED_CTA_GROUP=cg,
-                              FASTED_SEG_TILES=seg, FASTED_RES_BN=bn, FASTED_RES_EPI=epi)
+                              FASTED_SEG_TILES=seg, FASTED_RES_EPI=epi)
             for x, y in zip(ref, res):
-                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (cg, bn, epi, n, d)
-    # a ragged row range x column range (the multi-GPU shard shape)
+                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (cg, epi, n, d)
+    # ragged row ranges x column ranges (the multi-GPU shard shape): the
+    # diagonal falls at different offsets inside the 256-column tiles
     n_dev = -(-hd.n_padded // 128) * 128
-    rows, cols = (128, min(n_dev, 1152)), (256, n_dev)
-    ref = _tc_variant(hd, eps, rows, cols, FASTED_RESIDENT=0)
-    res = _tc_variant(hd, eps, rows, cols, FASTED_RESIDENT=1, FASTED_SEG_TILES=seg)
-    for x, y in zip(ref, res):
-        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+    for rows, cols in (((128, min(n_dev, 1152)), (256, n_dev)),
+                       ((min(n_dev, 384), min(n_dev, 1408)), (128, n_dev)),
+                       ((0, n_dev), (min(n_dev, 640), n_dev))):
+        ref = _tc_variant(hd, eps, rows, cols, FASTED_RESIDENT=0)
+        res = _tc_variant(hd, eps, rows, cols, FASTED_RESIDENT=1, FASTED_SEG_TILES=seg)
+        for x, y in zip(ref, res):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (rows, cols)
 
 
 @pytest.mark.parametrize("n,d,eps", [(3000, 512, 8.6), (2999, 300, 6.8), (1100, 960, 12.0),
