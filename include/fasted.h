@@ -67,6 +67,11 @@ enum {
      * kernel form (results are identical): at d_pad > 256 on large joins the
      * CTA-pair form, faster at low selectivity under the 1 kW power cap. */
     FASTED_JOIN_LOW_OUTPUT = 8,
+    /* OR-able: do not zero `count`; the launch appends to the records and
+     * totals an earlier launch left in out_records / count (same buffer,
+     * same capacity), e.g. one row range swept in column segments while the
+     * dataset is still arriving (engine.stream_join). */
+    FASTED_JOIN_APPEND = 16,
     /* Diagnostics for power/throughput attribution (results are NOT valid): */
     FASTED_JOIN_DIAG_NOEPI = 256,    /* tcgen05 kernel: skip the epilogue entirely     */
     FASTED_JOIN_DIAG_NOMMA = 512,    /* tcgen05 kernel: skip the MMAs (TMA + epilogue) */
@@ -122,7 +127,11 @@ int fasted_norms(const uint16_t* values16, int64_t n_pad, int64_t d_pad, float* 
  * UNSPECIFIED order.  Each warp fills private runs of FASTED_RECORD_CHUNK
  * slots, so the record array may contain unused slots, marked i == 0
  * (fasted_sort_pairs drops them).
- * `count` is DEVICE memory for two uint64 (zeroed by this call):
+ * The tcgen05 path reads only the rows of [row_begin, row_end) and
+ * [col_begin, col_end) (plus the padding of their last tiles, whose results
+ * are masked), so a launch may run while other rows are still being copied.
+ * `count` is DEVICE memory for two uint64 (zeroed by this call unless
+ * FASTED_JOIN_APPEND):
  *   count[0] = exact number of qualifying pairs,
  *   count[1] = chunks taken; slots used = count[1] * FASTED_RECORD_CHUNK.
  * Slots >= capacity are not written; if slots used > capacity the caller

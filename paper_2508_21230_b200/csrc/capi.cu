@@ -118,8 +118,10 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
         return FASTED_ERR_ARGUMENT;
     }
     cudaStream_t s = as_stream(stream);
-    cudaError_t e = cudaMemsetAsync(count, 0, 2 * sizeof(unsigned long long), s);
-    if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(count)");
+    if (!(flags & FASTED_JOIN_APPEND)) {
+        cudaError_t e = cudaMemsetAsync(count, 0, 2 * sizeof(unsigned long long), s);
+        if (e != cudaSuccess) return cuda_status(e, "cudaMemsetAsync(count)");
+    }
     if (row_end == row_begin || col_end == col_begin) return FASTED_OK;
     JoinArgs a;
     a.norms = norms;

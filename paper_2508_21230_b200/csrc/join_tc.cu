@@ -1846,10 +1846,11 @@ __device__ __forceinline__ void split_tf32(float x, float& h1, float& h2, float&
 // Augment rows: A_i = [sigma_i parts, 1, 1, 1, 0, 0], B_j = [1, 1, 1,
 // rho_j parts, 0, 0] with sigma = -s/2 and rho = -s/2 + eps^2/2, so that
 // A_i . B_j = (eps^2 - s_i - s_j) / 2.
-__global__ void aug_prepare_kernel(const float* __restrict__ norms, int64_t n_pad, float eps_sq,
-                                   float4* __restrict__ aug_a, float4* __restrict__ aug_b) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n_pad) return;
+__global__ void aug_prepare_kernel(const float* __restrict__ norms, int64_t begin, int64_t end,
+                                   float eps_sq, float4* __restrict__ aug_a,
+                                   float4* __restrict__ aug_b) {
+    const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= end) return;
     const float sigma = -0.5f * norms[i];
     const float rho = __fadd_rn(sigma, 0.5f * eps_sq);
     float a1, a2, a3, b1, b2, b3;
@@ -2177,37 +2178,53 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         cudaFreeAsync(aug, s);
         return st;
     }
-    if (tc_norms) {
-        JoinArgs ad = a;
-        ad.row_begin = 0;
-        ad.row_end = a.n_pad;
-        ad.col_begin = 0;
-        ad.col_end = a.n_pad;
-        ad.count_only = 1;
-        ad.capacity = 0;
-        ad.diag_flags = 0;
-        ad.symmetric = 0;
-        ad.gram_diag = gram;
-        Sched sd;
-        sd.row_tiles = (int)(a.n_pad / BM);
-        sd.col_tiles = 1;
-        sd.group = 1;
-        sd.nkb = (int)((a.d_pad + BK - 1) / BK);
-        sd.total = sd.row_tiles;
-        sd.diag = 1;
-        e = launch_variant<1, true>(mx, ma, mb, ad, sd, s);
-        if (e == cudaSuccess) e = cudaGetLastError();
+    // Both steps cover only the rows the join reads: [row_begin, row_end) and
+    // [col_begin, col_end) (one range when they meet), so a launch needs just
+    // those rows resident (FASTED_JOIN_APPEND column segments run while the
+    // rest of the dataset is still being copied).
+    int64_t rg[2][2] = {{a.row_begin, a.row_end}, {a.col_begin, a.col_end}};
+    int nrg = 2;
+    if (rg[1][0] <= rg[0][1] && rg[0][0] <= rg[1][1]) {
+        rg[0][0] = rg[0][0] < rg[1][0] ? rg[0][0] : rg[1][0];
+        rg[0][1] = rg[0][1] > rg[1][1] ? rg[0][1] : rg[1][1];
+        nrg = 1;
+    }
+    for (int g = 0; g < nrg; g++) {
+        const int64_t lo = rg[g][0], hi = rg[g][1];
+        if (hi <= lo) continue;
+        if (tc_norms) {
+            JoinArgs ad = a;
+            ad.row_begin = lo;
+            ad.row_end = hi;
+            ad.col_begin = lo;
+            ad.col_end = hi;
+            ad.count_only = 1;
+            ad.capacity = 0;
+            ad.diag_flags = 0;
+            ad.symmetric = 0;
+            ad.trace = nullptr;
+            ad.gram_diag = gram;
+            Sched sd;
+            sd.row_tiles = (int)((hi - lo + BM - 1) / BM);
+            sd.col_tiles = 1;
+            sd.group = 1;
+            sd.nkb = (int)((a.d_pad + BK - 1) / BK);
+            sd.total = sd.row_tiles;
+            sd.diag = 1;
+            e = launch_variant<1, true>(mx, ma, mb, ad, sd, s);
+            if (e == cudaSuccess) e = cudaGetLastError();
+            if (e != cudaSuccess) {
+                cudaFreeAsync(aug, s);
+                return cuda_status(e, "join_tc_kernel (Gram diagonal)");
+            }
+        }
+        aug_prepare_kernel<<<(unsigned)((hi - lo + 255) / 256), 256, 0, s>>>(
+            tc_norms ? gram : a.norms, lo, hi, a.eps_sq, aug_a, aug_b);
+        e = cudaGetLastError();
         if (e != cudaSuccess) {
             cudaFreeAsync(aug, s);
-            return cuda_status(e, "join_tc_kernel (Gram diagonal)");
+            return cuda_status(e, "aug_prepare_kernel");
         }
-    }
-    aug_prepare_kernel<<<(unsigned)((a.n_pad + 255) / 256), 256, 0, s>>>(
-        tc_norms ? gram : a.norms, a.n_pad, a.eps_sq, aug_a, aug_b);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) {
-        cudaFreeAsync(aug, s);
-        return cuda_status(e, "aug_prepare_kernel");
     }
     // Resident-A form for d_pad <= 256 (FASTED_RESIDENT=0 selects streaming),
     // 256-column tiles, two accumulators.  (128-column tiles with four

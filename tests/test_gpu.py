@@ -419,6 +419,62 @@ def test_stream_join_pipeline_matches_single_shot(budget, monkeypatch):
     engine._count_memo.clear()
 
 
+@pytest.mark.parametrize("exact", [False, True])
+def test_append_flag_sweeps_columns_in_segments(exact):
+    """FASTED_JOIN_APPEND: one row range swept in column segments, each
+    launch appending to the same record buffer and counts, sorts to exactly
+    the single-launch result (tcgen05 and exact kernels)."""
+    hd = F.to_half(F.generate_synthetic(5000, 200, seed=5))
+    dd = engine.upload(hd, 0)
+    es = float(np.float32(np.float32(5.4) ** 2))
+    rows = (0, dd.n_dev)
+    ref = engine.to_host(engine.join_device(dd, es, rows=rows, exact=exact))
+    flags = _lib.JOIN_EXACT if exact else _lib.JOIN_TC
+    cap = len(ref[0]) + engine.max_holes(0)
+    rec = torch.empty((cap, 4), dtype=torch.int32, device="cuda")
+    cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+    s = torch.cuda.current_stream()
+    bounds = [0, 1280, 1408, 3840, dd.n_dev]
+    for k, (c0, c1) in enumerate(zip(bounds[:-1], bounds[1:])):
+        engine.join_raw(dd, es, flags | (_lib.JOIN_APPEND if k else 0), rows, (c0, c1), rec,
+                        cap, cnt, s.cuda_stream)
+    count, used = (int(v) for v in cnt.tolist())
+    assert count == len(ref[0])
+    oi, oj, od, _ = engine._sort_records(dd, rec, used * engine.RECORD_CHUNK, count, rows, s)
+    got = (oi.cpu().numpy().view(np.uint32), oj.cpu().numpy().view(np.uint32), od.cpu().numpy())
+    for x, y in zip(ref, got):
+        assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
+
+
+def test_segmented_upload_pipeline_matches_resident(monkeypatch):
+    """upload_segmented + stream_join: the first row chunk sweeps its columns
+    segment by segment as the copy lands (FASTED_JOIN_APPEND), later chunks
+    run on the resident dataset -- exactly the result of a join on a fully
+    resident copy."""
+    hd = F.to_half(F.generate_synthetic(9000, 256, seed=8), pin_host=True)
+    es = float(np.float32(np.float32(6.0) ** 2))
+    dd0 = engine.upload(hd, 0)
+    ref = engine.to_host(engine.join_device(dd0, es))
+    monkeypatch.setattr(engine, "SEGMENT_MIN_BYTES", 0)
+    monkeypatch.setattr(engine, "PIPELINE_MIN_RECORDS", 0)     # 4 row chunks
+    if hasattr(hd, "device_cache"):
+        hd.device_cache.clear()
+    for segments in (8, 3):
+        engine._count_memo.clear()
+        dd = engine.upload_segmented(hd, 0, segments=segments)
+        assert dd.ready is not None and len(dd.ready) == segments
+        segs = engine.column_segments(dd, (0, dd.n_dev), dd.n_dev // 4 // 128 * 128)
+        assert len(segs) == 2 and segs[0][0] == 0 and segs[-1][1] == dd.n_dev
+        assert segs[0][1] < dd.n_dev and segs[1][2] == dd.n_dev
+        host = engine.HostPairs(1)
+        kms, sms, reruns, nch = engine.stream_join(dd, es, (0, dd.n_dev), False, host)
+        assert nch > 1 and dd.ready is None
+        got = host.arrays()
+        for x, y in zip(ref, got):
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), segments
+    engine._count_memo.clear()
+
+
 def test_device_calibration_hits_target_on_full_data(golden_meta):
     """GPU count-only bisection (16 row blocks x all columns): the full
     join at the calibrated epsilon lands within a few percent of the target

@@ -253,6 +253,7 @@ def test_python_flag_constants_match_header():
     assert vals["FASTED_JOIN_COUNT"] == _lib.JOIN_COUNT
     assert vals["FASTED_JOIN_SYMMETRIC"] == _lib.JOIN_SYMMETRIC
     assert vals["FASTED_JOIN_LOW_OUTPUT"] == _lib.JOIN_LOW_OUTPUT
+    assert vals["FASTED_JOIN_APPEND"] == _lib.JOIN_APPEND
     assert vals["FASTED_ERR_ARGUMENT"] == _lib.ERR_ARGUMENT
     rec = re.search(r"#define FASTED_RECORD_CHUNK (\d+)", src)
     assert int(rec.group(1)) == engine.RECORD_CHUNK
