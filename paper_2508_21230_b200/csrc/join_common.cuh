@@ -112,6 +112,7 @@ __device__ __forceinline__ void writer_finish(PairWriter& w, const JoinArgs& a) 
 template <int STAGE>
 struct StagedWriter {
     static_assert(WRITER_CHUNK % STAGE == 0, "chunk must hold whole staging buffers");
+    static constexpr uint32_t kStage = STAGE;
     unsigned long long base;    // first slot of the current chunk (~0: none open)
     uint32_t flushed;           // staging buffers shipped into the current chunk
     uint32_t fill;              // records in the current staging buffer
@@ -119,17 +120,15 @@ struct StagedWriter {
     uint32_t sbuf;              // shared address of this warp's 2 x STAGE x 16 bytes
     unsigned long long total;   // pairs found by this warp
     uint64_t policy;            // L2 evict_first cache policy for the record stream
-    uint32_t stash;             // shared address of this warp's 128-byte row stash
 };
 
-// Per-warp row stash of the tcgen05 epilogues (epi_chunk's transposed hit
-// search): one lane's 32 accumulator words.
+// Per-warp row stash of the resident kernel's epilogue (epi_chunk_res's
+// transposed hit search: one lane's 32 accumulator words), placed right after
+// the warp's two staging buffers.
 constexpr int EPI_STASH_BYTES = 128;
 
 template <int STAGE>
-__device__ __forceinline__ void writer_init(StagedWriter<STAGE>& w, uint32_t sbuf,
-                                            uint32_t stash = 0) {
-    w.stash = stash;
+__device__ __forceinline__ void writer_init(StagedWriter<STAGE>& w, uint32_t sbuf) {
     w.base = ~0ull;
     w.flushed = 0;
     w.fill = 0;

@@ -75,15 +75,12 @@ constexpr int BAR_BYTES = 256;
 // records of 16 bytes.
 constexpr int WSTAGE = 64;
 constexpr int WSTAGE_BYTES = NUM_EPI_WARPS * 2 * WSTAGE * 16;   // 16 KB
-// epi_chunk row stashes, up to 16 epilogue warps x 128 bytes, after the staging
-constexpr int STASH_BYTES = 16 * EPI_STASH_BYTES;
 
 template <int CG>
 struct Cfg {
     static constexpr int B_BYTES = (BN / CG) * BK * 2;   // this CTA's share of B
     static constexpr int STAGES = CG == 2 ? 6 : 4;
-    static constexpr int SMEM_BYTES =
-        STAGES * (A_BYTES + B_BYTES) + BAR_BYTES + WSTAGE_BYTES + STASH_BYTES + 1024;
+    static constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + BAR_BYTES + WSTAGE_BYTES + 1024;
     static constexpr int TILE_M = BM * CG;                // rows per tile
     // Instruction descriptors: D=F32 (bits 4-5 = 1); A/B format at bits
     // 7-9 / 10-12 (F16 = 0, TF32 = 2); both K-major; N>>3 at 17-22; M>>4 at
@@ -451,30 +448,72 @@ __device__ __forceinline__ unsigned long long clock_after(uint32_t dep) {
     return t;
 }
 
-// AND of 32 words: the sign bit of the result is clear iff some word's sign
-// bit is clear (some D >= 0, i.e. a hit).  A depth-4 tree of 3-input LOP3s
-// in inline PTX (from plain C the compiler reassociates a tree into a
-// 32-deep dependent chain; measured equal at 1M x 128 -- the per-tile cost
-// is issue slots, not this latency -- kept for the shorter chain).
-__device__ __forceinline__ uint32_t and3(uint32_t a, uint32_t b, uint32_t c) {
-    uint32_t d;
-    asm("lop3.b32 %0, %1, %2, %3, 0x80;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-    return d;
-}
-
+// AND of 32 words as a balanced tree: the sign bit of the result is clear
+// iff some word's sign bit is clear (some D >= 0, i.e. a hit).
 __device__ __forceinline__ uint32_t and_tree32(const uint32_t (&r)[32]) {
-    uint32_t t[11];
+    uint32_t t[16];
 #pragma unroll
-    for (int k = 0; k < 10; k++) t[k] = and3(r[3 * k], r[3 * k + 1], r[3 * k + 2]);
-    t[10] = and3(r[30], r[31], 0xffffffffu);
-    const uint32_t u0 = and3(t[0], t[1], t[2]), u1 = and3(t[3], t[4], t[5]);
-    const uint32_t u2 = and3(t[6], t[7], t[8]), u3 = and3(t[9], t[10], 0xffffffffu);
-    return and3(and3(u0, u1, u2), u3, 0xffffffffu);
+    for (int k = 0; k < 16; k++) t[k] = r[2 * k] & r[2 * k + 1];
+#pragma unroll
+    for (int k = 0; k < 8; k++) t[k] = t[2 * k] & t[2 * k + 1];
+#pragma unroll
+    for (int k = 0; k < 4; k++) t[k] = t[2 * k] & t[2 * k + 1];
+    return (t[0] & t[1]) & (t[2] & t[3]);
 }
 
 // Epilogue of one 32-column chunk (columns jb.., row i = this lane).
 // r[e] = D_{i, jb+e} = (eps^2 - d2) / 2 as FP32 bits.
-//
+template <typename W>
+__device__ __forceinline__ void epi_chunk(const JoinArgs& a, W& wr, const uint32_t (&r)[32],
+                                          int64_t jb, int64_t i, int64_t iw, bool row_ok) {
+    // common path: is any D >= 0 (sign bit clear)?  A balanced AND tree
+    // (depth ~5, not a 16-deep chain).
+    const uint32_t acc = and_tree32(r);
+    const bool diag = (jb < iw + 32) && (iw < jb + 32);   // warp-uniform
+    if (!__any_sync(0xffffffffu, (int)acc >= 0) && !diag) return;
+    if (a.diag_flags & FASTED_JOIN_DIAG_NOSLOW) return;
+    // rare path.  Self pairs first: distance exactly 0 (the reference's
+    // a_ii and s_i are the same chain), one append for the whole warp.
+    if (diag) {
+        const bool self = (i >= jb) && (i < jb + 32) && row_ok;
+        const uint32_t b = __ballot_sync(0xffffffffu, self);
+        if (b) writer_append(wr, a, b, self, (uint32_t)(i + 1), (uint32_t)(i + 1), 0.0f);
+    }
+    {
+        // Per lane: build the hit mask (sign bits clear), drop the self
+        // column and columns past n_logical; the warp appends one record per
+        // hitting lane per round -- usually one round, hits being sparse.
+        // (A column-scan form -- 32 REDUX.AND per chunk -- measured no faster
+        // at 1M x 128 and doubled the rare-path code; it was removed.)
+        uint32_t lm = 0;
+#pragma unroll
+        for (int e = 0; e < 32; e++) lm |= ((~r[e]) >> 31) << e;
+        const int64_t valid = a.n_logical - jb;
+        if (valid < 32) lm &= valid <= 0 ? 0u : ((1u << (uint32_t)valid) - 1u);
+        if (i >= jb && i < jb + 32) lm &= ~(1u << (uint32_t)(i - jb));
+        if (a.symmetric) {
+            // upper triangle only (j > i); the mirrored record covers (j, i)
+            const int64_t off = i - jb;   // columns jb .. i are not above the diagonal
+            if (off >= 31) lm = 0u;
+            else if (off >= 0) lm &= ~((2u << (uint32_t)off) - 1u);
+        }
+        if (!row_ok) lm = 0u;
+        while (true) {
+            const bool mine = lm != 0u;
+            const uint32_t b = __ballot_sync(0xffffffffu, mine);
+            if (b == 0u) break;
+            const uint32_t e = mine ? (uint32_t)(__ffs(lm) - 1) : 0u;
+            lm &= lm - 1u;
+            const uint32_t v = pick32(r, e);
+            const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
+            writer_append(wr, a, b, mine, (uint32_t)(i + 1), (uint32_t)(jb + e + 1), d2);
+            if (a.symmetric)
+                writer_append(wr, a, b, mine, (uint32_t)(jb + e + 1), (uint32_t)(i + 1), d2);
+        }
+    }
+}
+
+// The resident kernel's chunk epilogue: epi_chunk with a hybrid hit search.
 // Hit search, transposed: a lane whose row has a candidate (some D >= 0)
 // publishes its 32 words to the warp's shared-memory stash and every lane e
 // tests column e of that row, so one ballot yields the row's hits and each
@@ -484,10 +523,14 @@ __device__ __forceinline__ uint32_t and_tree32(const uint32_t (&r)[32]) {
 // against ~200 for the per-lane mask form it replaced (measured with
 // FASTED_JOIN_DIAG_TRACE at 1M x 128: a warp with a hit came back to the next
 // tile ~2900 cycles late, stalling the MMA warp on the accumulator).
+// The stash is the 128 bytes after the warp's two staging buffers.  (The
+// streaming and multicast kernels keep epi_chunk: at d > 256 the hybrid
+// measured 6% slower at 5M x 384, S ~ 4096, and at 60K x 512.)
 template <typename W>
-__device__ __forceinline__ void epi_chunk(const JoinArgs& a, W& wr, const uint32_t (&r)[32],
-                                          int64_t jb, int64_t i, int64_t iw, bool row_ok,
-                                          unsigned long long* tr = nullptr) {
+__device__ __forceinline__ void epi_chunk_res(const JoinArgs& a, W& wr, const uint32_t (&r)[32],
+                                              int64_t jb, int64_t i, int64_t iw, bool row_ok,
+                                              unsigned long long* tr = nullptr) {
+    const uint32_t stash = wr.sbuf + 2u * W::kStage * 16u;
     // common path: is any D >= 0 (sign bit clear)?  A balanced AND tree.
     const uint32_t acc = and_tree32(r);
     const bool diag = (jb < iw + 32) && (iw < jb + 32);   // warp-uniform
@@ -546,11 +589,11 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, W& wr, const uint32
         if (lane == src) {
 #pragma unroll
             for (int k = 0; k < 8; k++)
-                st_shared_v4(wr.stash + 16u * k,
+                st_shared_v4(stash + 16u * k,
                              make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
         }
         __syncwarp();
-        const uint32_t v = ld_shared_u32(wr.stash + 4u * lane);
+        const uint32_t v = ld_shared_u32(stash + 4u * lane);
         __syncwarp();   // the stash is rewritten for the next row
         const int64_t is = iw + src;
         // drop the self column and columns past n_logical; symmetric: keep
@@ -692,10 +735,10 @@ __device__ __forceinline__ void res_epi_tile(const JoinArgs& a, W& wr, uint32_t 
         if (!any) return;
     }
     unsigned long long* const trc = TRACE ? tr : nullptr;
-    if (nchunks > 0) epi_chunk(a, wr, r0, jb, i, iw, row_ok, trc);
-    if (NCH > 1 && nchunks > 1) epi_chunk(a, wr, r1, jb + 32, i, iw, row_ok, trc);
-    if (NCH > 2 && nchunks > 2) epi_chunk(a, wr, r2, jb + 64, i, iw, row_ok);
-    if (NCH > 2 && nchunks > 3) epi_chunk(a, wr, r3, jb + 96, i, iw, row_ok);
+    if (nchunks > 0) epi_chunk_res(a, wr, r0, jb, i, iw, row_ok, trc);
+    if (NCH > 1 && nchunks > 1) epi_chunk_res(a, wr, r1, jb + 32, i, iw, row_ok, trc);
+    if (NCH > 2 && nchunks > 2) epi_chunk_res(a, wr, r2, jb + 64, i, iw, row_ok);
+    if (NCH > 2 && nchunks > 3) epi_chunk_res(a, wr, r3, jb + 96, i, iw, row_ok);
 }
 
 template <int CG, bool DIAG, int NEPI = NUM_EPI_WARPS>
@@ -910,9 +953,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         // warps, 32 with 16)
         constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;
         StagedWriter<WST> wr;
-        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16,
-                    bars + BAR_BYTES + WSTAGE_BYTES +
-                        (uint32_t)(warp - FIRST_EPI_WARP) * EPI_STASH_BYTES);
+        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -997,7 +1038,7 @@ __device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
 
 constexpr int MC_STAGES = 4;
 constexpr int MC_SMEM_BYTES =
-    MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + WSTAGE_BYTES + STASH_BYTES + 1024;
+    MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + WSTAGE_BYTES + 1024;
 
 template <int NEPI>
 __global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI) * 32, 1)
@@ -1148,9 +1189,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         const int h = (warp - FIRST_EPI_WARP) >> 2;
         constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;   // 16 KB of staging either way
         StagedWriter<WST> wr;
-        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16,
-                    bars + BAR_BYTES + WSTAGE_BYTES +
-                        (uint32_t)(warp - FIRST_EPI_WARP) * EPI_STASH_BYTES);
+        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -1469,9 +1508,9 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         const int h = (warp - FIRST_EPI_WARP) >> 2;   // column group (NEPI / 4 of them)
         constexpr int RWS = RES_WSTAGE_TOTAL / (2 * NEPI) * 2;   // 16 (NEPI 16) / 32 (NEPI 8)
         StagedWriter<RWS> wr;
-        writer_init(wr, bars + C::BAR_REGION + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * RWS * 16,
-                    bars + C::BAR_REGION + (uint32_t)(NEPI * 2 * RWS * 16) +
-                        (uint32_t)(warp - FIRST_EPI_WARP) * EPI_STASH_BYTES);
+        // per warp: two staging buffers, then the 128-byte row stash
+        writer_init(wr, bars + C::BAR_REGION +
+                            (uint32_t)(warp - FIRST_EPI_WARP) * (2 * RWS * 16 + EPI_STASH_BYTES));
         static_assert(NACC == 2, "lean epilogue assumes two accumulators");
         const uint32_t tcol0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * HALF);
         const bool local_release = CG == 1 || leader;
@@ -1801,9 +1840,7 @@ join_tc_ts_kernel(const uint4* __restrict__ X, const __grid_constant__ CUtensorM
         const int q = warp & 3;
         const int h = (warp - FIRST_EPI_WARP) >> 2;
         StagedWriter<TS_WSTAGE> wr;
-        writer_init(wr, wst_base + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * TS_WSTAGE * 16,
-                    wst_base + (uint32_t)(TS_NEPI * 2 * TS_WSTAGE * 16) +
-                        (uint32_t)(warp - FIRST_EPI_WARP) * EPI_STASH_BYTES);
+        writer_init(wr, wst_base + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * TS_WSTAGE * 16);
         int lt = 0;
         for (int64_t u = unit0; u < sch.units; u += ustep) {
             int rt, ct0, ct1;
@@ -2009,7 +2046,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     ResSched sch;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.a_buf_bytes = (uint32_t)((sch.nkb * A_BYTES + BM * AUG_ROW_BYTES + 1023) & ~1023);
-    const int wstage = NEPI * 2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16 + NEPI * EPI_STASH_BYTES;
+    const int wstage = NEPI * (2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16 + EPI_STASH_BYTES);
     const int budget = SMEM_MAX - 1024 - C::BAR_REGION - wstage;
     sch.na = 2 * (int)sch.a_buf_bytes <= 80 * 1024 ? 2 : 1;
     sch.stages = (budget - sch.na * (int)sch.a_buf_bytes) / C::STAGE_BYTES;
@@ -2098,7 +2135,7 @@ static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUte
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.na = 2;
     sch.a_buf_bytes = 0;
-    const int wst = TS_NEPI * 2 * TS_WSTAGE * 16 + TS_NEPI * EPI_STASH_BYTES;
+    const int wst = TS_NEPI * 2 * TS_WSTAGE * 16;
     const int fixed = 2 * 4096 + TS_BAR_REGION + wst + 1024;
     sch.stages = (SMEM_MAX - fixed) / TS_STAGE_BYTES;
     if (sch.stages > TS_MAX_STAGES) sch.stages = TS_MAX_STAGES;
