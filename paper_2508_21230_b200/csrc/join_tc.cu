@@ -1292,8 +1292,178 @@ __device__ __forceinline__ void res_unit_sym(const ResSched& s, const JoinArgs& 
     }
 }
 
-template <int CG, int TBN, int NEPI, bool TRACE = false>
-__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI) * 32, 1)
+// Hit warps (FASTED_RES_HIT, resident kernel).  The trace of the resident
+// kernel (above) shows the MMA waiting on the slowest of 32 epilogue warps,
+// and the slowest is one that found a candidate and ran the rare path.  With
+// NHIT hit warps the epilogue warps never run it: a lane whose row holds a
+// candidate copies its 32 words into a shared-memory queue slot and the warp
+// moves on; the hit warps pop slots in order, test the row transposed (lane e
+// = column e), and own the record writers.  One queue per hit warp, fed by a
+// fixed set of epilogue warps; an epilogue warp ends its stream with an END
+// entry.  Slot protocol: slots are taken in order from a shared tail
+// counter; a producer may fill slot idx once the hit warp's head counter
+// (atomically stored after each entry) shows entry idx - Q consumed -- a
+// parity wait alone would let a producer two laps ahead overwrite an
+// unconsumed slot -- and the slot's empty mbarrier completed; it publishes
+// the entry with the slot's full mbarrier.
+template <int NHIT>
+struct HitQ {
+    static constexpr int Q = 16;                    // slots per queue
+    static constexpr int HWS = 64;                  // records per staging buffer (hit warp)
+    static constexpr int WRITER_BYTES = NHIT * 2 * HWS * 16;
+    static constexpr int DATA_BYTES = NHIT * Q * 128;
+    static constexpr int META_BYTES = NHIT * Q * 16;
+    static constexpr int BARQ_BYTES = NHIT * Q * 16;   // full, empty barriers
+    static constexpr int BYTES = WRITER_BYTES + DATA_BYTES + META_BYTES + BARQ_BYTES + 16;
+    static __device__ __forceinline__ uint32_t data(uint32_t r, int q, uint32_t s) {
+        return r + WRITER_BYTES + ((uint32_t)q * Q + s) * 128u;
+    }
+    static __device__ __forceinline__ uint32_t meta(uint32_t r, int q, uint32_t s) {
+        return r + WRITER_BYTES + DATA_BYTES + ((uint32_t)q * Q + s) * 16u;
+    }
+    static __device__ __forceinline__ uint32_t full(uint32_t r, int q, uint32_t s) {
+        return r + WRITER_BYTES + DATA_BYTES + META_BYTES + ((uint32_t)q * Q + s) * 16u;
+    }
+    static __device__ __forceinline__ uint32_t tail(uint32_t r, int q) {
+        return r + WRITER_BYTES + DATA_BYTES + META_BYTES + BARQ_BYTES + 4u * q;
+    }
+    static __device__ __forceinline__ uint32_t head(uint32_t r, int q) {
+        return tail(r, q) + 8u;
+    }
+};
+
+// The head counter is accessed with atomics (acquire read, release write):
+// ordinary ld.acquire/st.release work too but read as races to racecheck.
+__device__ __forceinline__ uint32_t ld_acquire_shared(uint32_t addr) {
+    uint32_t v;
+    asm volatile("atom.acquire.cta.shared::cta.or.b32 %0, [%1], 0;" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_shared(uint32_t addr, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.release.cta.shared::cta.exch.b32 %0, [%1], %2;"
+                 : "=r"(old)
+                 : "r"(addr), "r"(v)
+                 : "memory");
+}
+enum { HIT_ROW = 0, HIT_SELF = 1, HIT_END = 2 };
+
+__device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+// One queue entry, written by one thread: wait until the slot's previous
+// lap was consumed, fill it, publish it (release arrive).
+template <int NHIT>
+__device__ __forceinline__ void hit_put(uint32_t reg, int q, uint32_t idx, uint32_t kind,
+                                        uint32_t i, uint32_t jb, uint32_t mask,
+                                        const uint32_t (&r)[32], bool with_data) {
+    using H = HitQ<NHIT>;
+    const uint32_t slot = idx % H::Q;
+    if (idx >= (uint32_t)H::Q) {
+        // at most one lap ahead of the hit warp (the head counter), then the
+        // slot's empty barrier for the previous lap (all 32 consumer lanes
+        // arrive after their reads; with the lap bounded its parity is
+        // unambiguous)
+        if (ld_acquire_shared(H::head(reg, q)) + H::Q <= idx) {
+            const uint64_t t0 = global_timer();
+            while (ld_acquire_shared(H::head(reg, q)) + H::Q <= idx) {
+                __nanosleep(64);
+                if (global_timer() - t0 > 20000000000ull) __trap();
+            }
+        }
+        mbar_wait(H::full(reg, q, slot) + 8u, ((idx / H::Q) & 1u) ^ 1u);
+    }
+    if (with_data) {
+        const uint32_t d = H::data(reg, q, slot);
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            st_shared_v4(d + 16u * k, make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
+    }
+    st_shared_v4(H::meta(reg, q, slot), make_uint4(kind, i, jb, mask));
+    mbar_arrive(H::full(reg, q, slot));
+}
+
+// Hand one 32-column chunk's candidate rows (and the diagonal's self pairs)
+// to hit warp q.  Warp-collective.
+template <int NHIT>
+__device__ __forceinline__ void hit_push(uint32_t reg, uint8_t* smem_raw, uint32_t raw, int q,
+                                         const uint32_t (&r)[32], int jb, int i, int iw,
+                                         bool row_ok, uint32_t lane) {
+    const bool diag = (jb < iw + 32) && (iw < jb + 32);
+    uint32_t rows, selfmask = 0u;
+    if (!diag) {
+        rows = __ballot_sync(0xffffffffu, (int)and_tree32(r) >= 0 && row_ok);
+    } else {
+        // every row meets its own column here: candidates other than the self column
+        uint32_t lm = 0;
+#pragma unroll
+        for (int e = 0; e < 32; e++) lm |= ((~r[e]) >> 31) << e;
+        const bool self = i >= jb && i < jb + 32 && row_ok;
+        if (self) lm &= ~(1u << (uint32_t)(i - jb));
+        rows = __ballot_sync(0xffffffffu, lm != 0u && row_ok);
+        selfmask = __ballot_sync(0xffffffffu, self);
+    }
+    const uint32_t k = (uint32_t)__popc(rows) + (selfmask ? 1u : 0u);
+    if (k == 0u) return;
+    uint32_t b0 = 0;
+    if (lane == 0)
+        b0 = atomicAdd(reinterpret_cast<unsigned*>(smem_raw + (HitQ<NHIT>::tail(reg, q) - raw)), k);
+    b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if ((rows >> lane) & 1u)
+        hit_put<NHIT>(reg, q, b0 + (uint32_t)__popc(rows & lanemask_lt()), HIT_ROW, (uint32_t)i,
+                      (uint32_t)jb, 0u, r, true);
+    if (selfmask && lane == 0)
+        hit_put<NHIT>(reg, q, b0 + (uint32_t)__popc(rows), HIT_SELF, (uint32_t)iw, (uint32_t)jb,
+                      selfmask, r, false);
+    __syncwarp();
+}
+
+// The resident epilogue tile with hit warps: drain, release, slice test, and
+// on a candidate only the hand-off.
+template <int CG, int TBN, int NSPLIT, int NHIT>
+__device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg, uint8_t* smem_raw,
+                                                 uint32_t raw, int hq, uint32_t tcol,
+                                                 uint32_t tfull, uint32_t aph, uint32_t tempty,
+                                                 bool local_release, bool spin, int dflags,
+                                                 int nchunks, bool fast, int jb, int i, int iw,
+                                                 bool row_ok, uint32_t lane) {
+    constexpr int HALF = TBN / NSPLIT;
+    constexpr int NCH = HALF / 32;
+    static_assert(NCH == 2, "hit-warp epilogue: 64 columns per warp");
+    mbar_wait2(tfull, aph, spin);
+    tc_fence_after();
+    uint32_t r0[32], r1[32];
+    if (nchunks > 0) tmem_ld32(tcol, r0);
+    if (nchunks > 1) tmem_ld32(tcol + 32u, r1);
+    if (nchunks > 0) {
+        tmem_ld_wait(r0);
+        tmem_ld_wait(r1);
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+        if (local_release) mbar_arrive_relaxed(tempty);
+        else mbar_arrive_cluster(tempty);
+    }
+    if (dflags & FASTED_JOIN_DIAG_LOADONLY) return;
+    if (fast) {
+        const uint32_t all = and_tree32(r0) & and_tree32(r1);
+        if (!__any_sync(0xffffffffu, (int)all >= 0)) return;
+    }
+    if (dflags & FASTED_JOIN_DIAG_NOSLOW) return;
+    if (nchunks > 0) hit_push<NHIT>(reg, smem_raw, raw, hq, r0, jb, i, iw, row_ok, lane);
+    if (nchunks > 1) hit_push<NHIT>(reg, smem_raw, raw, hq, r1, jb + 32, i, iw, row_ok, lane);
+}
+
+template <int CG, int TBN, int NEPI, bool TRACE = false, int NHIT = 0>
+__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI + NHIT) * 32, 1)
 join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                    const __grid_constant__ CUtensorMap tmap_xb,
                    const __grid_constant__ CUtensorMap tmap_aug_a,
@@ -1337,6 +1507,17 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         for (int b = 0; b < 2; b++) {
             mbar_init(afull_bar(b), 1);
             mbar_init(aempty_bar(b), 1);
+        }
+        if constexpr (NHIT > 0) {
+            const uint32_t reg = bars + C::BAR_REGION;
+            for (int q = 0; q < NHIT; q++) {
+                for (uint32_t sl = 0; sl < (uint32_t)HitQ<NHIT>::Q; sl++) {
+                    mbar_init(HitQ<NHIT>::full(reg, q, sl), 1);
+                    mbar_init(HitQ<NHIT>::full(reg, q, sl) + 8u, 32);   // empty
+                }
+                *reinterpret_cast<volatile uint32_t*>(smem_raw + (HitQ<NHIT>::tail(reg, q) - raw)) = 0u;
+                *reinterpret_cast<volatile uint32_t*>(smem_raw + (HitQ<NHIT>::head(reg, q) - raw)) = 0u;
+            }
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_xa))
@@ -1499,6 +1680,43 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
             }
         }
         __syncwarp();
+    } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
+        // ---------------- hit warp: pop queue hq in order, test rows, write records
+        using H = HitQ<NHIT>;
+        const int hq = warp - FIRST_EPI_WARP - NEPI;
+        const uint32_t reg = bars + C::BAR_REGION;
+        StagedWriter<H::HWS> wr;
+        writer_init(wr, reg + (uint32_t)hq * 2u * H::HWS * 16u);
+        const bool spin = (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0;
+        int ends = 0;
+        for (uint32_t idx = 0; ends < NEPI / NHIT; idx++) {
+            const uint32_t sl = idx % H::Q;
+            mbar_wait2(H::full(reg, hq, sl), (idx / H::Q) & 1u, spin);
+            const uint4 m = ld_shared_v4(H::meta(reg, hq, sl));
+            if (m.x == HIT_ROW) {
+                const uint32_t v = ld_shared_u32(H::data(reg, hq, sl) + 4u * (uint32_t)lane);
+                const int64_t is = (int64_t)m.y, j = (int64_t)m.z + lane;
+                const bool hit = (int)v >= 0 && j < a.n_logical && j != is &&
+                                 (!a.symmetric || j > is);
+                const uint32_t b = __ballot_sync(0xffffffffu, hit);
+                if (b) {
+                    const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
+                    writer_append(wr, a, b, hit, (uint32_t)(is + 1), (uint32_t)(j + 1), d2);
+                    if (a.symmetric)
+                        writer_append(wr, a, b, hit, (uint32_t)(j + 1), (uint32_t)(is + 1), d2);
+                }
+            } else if (m.x == HIT_SELF) {
+                const bool mine = (m.w >> lane) & 1u;
+                writer_append(wr, a, m.w, mine, m.y + (uint32_t)lane + 1u,
+                              m.y + (uint32_t)lane + 1u, 0.0f);
+            } else {
+                ends++;
+            }
+            mbar_arrive(H::full(reg, hq, sl) + 8u);   // this lane is done with the slot
+            __syncwarp();
+            if (lane == 0) st_release_shared(H::head(reg, hq), idx + 1u);
+        }
+        writer_finish(wr, a);
     } else {
         // ---------------- epilogue
         constexpr int NSPLIT = NEPI / 4;
@@ -1508,9 +1726,11 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         const int h = (warp - FIRST_EPI_WARP) >> 2;   // column group (NEPI / 4 of them)
         constexpr int RWS = RES_WSTAGE_TOTAL / (2 * NEPI) * 2;   // 16 (NEPI 16) / 32 (NEPI 8)
         StagedWriter<RWS> wr;
-        // per warp: two staging buffers, then the 128-byte row stash
-        writer_init(wr, bars + C::BAR_REGION +
-                            (uint32_t)(warp - FIRST_EPI_WARP) * (2 * RWS * 16 + EPI_STASH_BYTES));
+        // per warp: two staging buffers, then the 128-byte row stash (no
+        // writers here when hit warps write the records)
+        if constexpr (NHIT == 0)
+            writer_init(wr, bars + C::BAR_REGION +
+                                (uint32_t)(warp - FIRST_EPI_WARP) * (2 * RWS * 16 + EPI_STASH_BYTES));
         static_assert(NACC == 2, "lean epilogue assumes two accumulators");
         const uint32_t tcol0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * HALF);
         const bool local_release = CG == 1 || leader;
@@ -1554,15 +1774,36 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                 if (TRACE && a.trace && blockIdx.x == 0 && lt < TRACE_TILES)
                     tr = a.trace + 2 * TRACE_TILES +
                          8 * (lt * TRACE_EPI_WARPS + (warp - FIRST_EPI_WARP));
-                res_epi_tile<CG, TBN, NSPLIT, TRACE>(
-                    a, wr, tcol0 + buf * TBN, tfull0 + 8u * buf, aph, buf ? release1 : release0,
-                    local_release, spin, dflags, nchunks, fast, jb, i, iw, row_ok, lane, tr);
+                if constexpr (NHIT > 0)
+                    res_epi_tile_hit<CG, TBN, NSPLIT, NHIT>(
+                        a, bars + C::BAR_REGION, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT,
+                        tcol0 + buf * TBN, tfull0 + 8u * buf, aph, buf ? release1 : release0,
+                        local_release, spin, dflags, nchunks, fast, jb, i, iw, row_ok,
+                        (uint32_t)lane);
+                else
+                    res_epi_tile<CG, TBN, NSPLIT, TRACE>(
+                        a, wr, tcol0 + buf * TBN, tfull0 + 8u * buf, aph,
+                        buf ? release1 : release0, local_release, spin, dflags, nchunks, fast, jb,
+                        i, iw, row_ok, lane, tr);
                 if (TRACE && tr && lane == 0) tr[3] = clock64();
                 buf ^= 1u;
                 aph ^= buf ^ 1u;   // phase flips after buffer 1
             }
         }
-        writer_finish(wr, a);
+        if constexpr (NHIT > 0) {
+            // end of this warp's stream in its hit warp's queue
+            const uint32_t reg = bars + C::BAR_REGION;
+            const int hq = (warp - FIRST_EPI_WARP) % NHIT;
+            if (lane == 0) {
+                const uint32_t idx = atomicAdd(
+                    reinterpret_cast<unsigned*>(smem_raw + (HitQ<NHIT>::tail(reg, hq) - raw)), 1u);
+                uint32_t none[32];
+                hit_put<NHIT>(reg, hq, idx, HIT_END, 0u, 0u, 0u, none, false);
+            }
+            __syncwarp();
+        } else {
+            writer_finish(wr, a);
+        }
     }
 
     tc_fence_before();
@@ -2018,16 +2259,16 @@ static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const
 
 // Resident-A launch: shared memory split between the A buffer(s) and as many
 // B stages as fit.
-template <int CG, int TBN, int NEPI>
+template <int CG, int TBN, int NEPI, int NHIT = 0>
 static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
                               const CUtensorMap& ma, const CUtensorMap& mb, const JoinArgs& a,
                               cudaStream_t s) {
     using namespace tc;
     using C = ResCfg<CG, TBN>;
     constexpr int SMEM_MAX = 227 * 1024;
-    constexpr bool CAN_TRACE = CG == 2 && TBN == 256 && NEPI == 16;
-    auto kern = (CAN_TRACE && a.trace) ? join_tc_res_kernel<CG, TBN, NEPI, CAN_TRACE>
-                                       : join_tc_res_kernel<CG, TBN, NEPI, false>;
+    constexpr bool CAN_TRACE = CG == 2 && TBN == 256 && NEPI == 16 && NHIT == 0;
+    auto kern = (CAN_TRACE && a.trace) ? join_tc_res_kernel<CG, TBN, NEPI, CAN_TRACE, 0>
+                                       : join_tc_res_kernel<CG, TBN, NEPI, false, NHIT>;
     static PerDeviceOnce attr_once, attr_once_trace;
     if (CAN_TRACE && a.trace) {
         cudaError_t e = attr_once_trace.run([&] {
@@ -2046,7 +2287,9 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     ResSched sch;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.a_buf_bytes = (uint32_t)((sch.nkb * A_BYTES + BM * AUG_ROW_BYTES + 1023) & ~1023);
-    const int wstage = NEPI * (2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16 + EPI_STASH_BYTES);
+    const int wstage = NHIT > 0 ? HitQ<NHIT>::BYTES
+                                : NEPI * (2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16 +
+                                          EPI_STASH_BYTES);
     const int budget = SMEM_MAX - 1024 - C::BAR_REGION - wstage;
     sch.na = 2 * (int)sch.a_buf_bytes <= 80 * 1024 ? 2 : 1;
     sch.stages = (budget - sch.na * (int)sch.a_buf_bytes) / C::STAGE_BYTES;
@@ -2067,7 +2310,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     if (work <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * CG));
-    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI) * 32);
+    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI + NHIT) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -2281,16 +2524,20 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
             cudaFreeAsync(aug, s);
             return st;
         }
-        // 16 epilogue warps, each draining 64 columns (FASTED_RES_EPI=8: 8
-        // warps of 128 columns).  Measured at 1M x 128, alternating runs on
+        // 16 epilogue warps, each draining 64 columns, plus two hit warps
+        // that own the rare path and the record writers (FASTED_RES_HIT=0:
+        // the epilogue warps run it themselves; measured at 1M x 128,
+        // alternating: 212-224 vs 245-249 ms); FASTED_RES_EPI=8: 8 warps of
+        // 128 columns.  Measured at 1M x 128, alternating runs on
         // one box: 253.8-253.9 ms with 16 vs 269-319 ms with 8 -- the shorter
         // per-warp chain per tile also removes the run-to-run spread
         // (profiles/round1/tune_c3_epi_ab_session2.txt).
         if (ts)
             e = launch_ts(X, mxb, ma, mbb, a, s);
         else if (cg == 2)
-            e = env_int("FASTED_RES_EPI", 16) == 16 ? launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s)
-                                                     : launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
+            e = env_int("FASTED_RES_EPI", 16) != 16 ? launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s)
+                : env_int("FASTED_RES_HIT", 2) == 2 ? launch_res<2, 256, 16, 2>(mx, mxb, ma, mbb, a, s)
+                                                     : launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s);
         else
             e = launch_res<1, 256, 8>(mx, mxb, ma, mbb, a, s);
         if (e == cudaSuccess) e = cudaGetLastError();

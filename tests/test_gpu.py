@@ -353,11 +353,11 @@ def test_resident_kernel_bit_identical_to_streaming(n, d, eps, seg):
     for cg in (2, 1):
         ref = _tc_variant(hd, eps, FASTED_RESIDENT=0, FASTED_CTA_GROUP=cg)
         assert len(ref[0]) > n
-        for epi in (16, 8):
+        for epi, hit in ((16, 0), (8, 0), (16, 2)):
             res = _tc_variant(hd, eps, FASTED_RESIDENT=1, FASTED_CTA_GROUP=cg,
-                              FASTED_SEG_TILES=seg, FASTED_RES_EPI=epi)
+                              FASTED_SEG_TILES=seg, FASTED_RES_EPI=epi, FASTED_RES_HIT=hit)
             for x, y in zip(ref, res):
-                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (cg, epi, n, d)
+                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (cg, epi, hit, n, d)
     # ragged row ranges x column ranges (the multi-GPU shard shape): the
     # diagonal falls at different offsets inside the 256-column tiles
     n_dev = -(-hd.n_padded // 128) * 128
@@ -365,9 +365,34 @@ def test_resident_kernel_bit_identical_to_streaming(n, d, eps, seg):
                        ((min(n_dev, 384), min(n_dev, 1408)), (128, n_dev)),
                        ((0, n_dev), (min(n_dev, 640), n_dev))):
         ref = _tc_variant(hd, eps, rows, cols, FASTED_RESIDENT=0)
-        res = _tc_variant(hd, eps, rows, cols, FASTED_RESIDENT=1, FASTED_SEG_TILES=seg)
-        for x, y in zip(ref, res):
-            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (rows, cols)
+        for hit in (0, 2):
+            res = _tc_variant(hd, eps, rows, cols, FASTED_RESIDENT=1, FASTED_SEG_TILES=seg,
+                              FASTED_RES_HIT=hit)
+            for x, y in zip(ref, res):
+                assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (rows, cols, hit)
+
+
+@pytest.mark.parametrize("n,d,eps", [(3000, 128, 3.7), (2999, 100, 3.3), (4000, 64, 2.9)])
+def test_resident_hit_warps_symmetric_and_count(n, d, eps, monkeypatch):
+    """Hit warps (FASTED_RES_HIT=2): the symmetric schedule and the
+    count-only join give what the epilogue-warp form gives."""
+    hd = F.to_half(F.generate_synthetic(n, d, seed=n * 3 + d))
+    es = float(np.float32(np.float32(eps) ** 2))
+    dd = engine.upload(hd, 0)
+    out = {}
+    for hit in ("0", "2"):
+        monkeypatch.setenv("FASTED_RES_HIT", hit)
+        engine._count_memo.clear()
+        rs = F.self_join(hd, eps, symmetric=True)
+        cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+        engine.join_raw(dd, es, _lib.JOIN_TC | _lib.JOIN_COUNT, (0, dd.n_dev), (0, dd.n_dev),
+                        None, 0, cnt, torch.cuda.current_stream().cuda_stream)
+        out[hit] = (rs, int(cnt[0]))
+    (ra, ca), (rb, cb) = out["0"], out["2"]
+    assert ca == cb == len(ra) == len(rb) > n
+    for x, y in zip((ra.i, ra.j, ra.dist_sq), (rb.i, rb.j, rb.dist_sq)):
+        assert np.array_equal(np.asarray(x).view(np.uint32), np.asarray(y).view(np.uint32))
+    engine._count_memo.clear()
 
 
 @pytest.mark.parametrize("n,d,eps", [(3000, 512, 8.6), (2999, 300, 6.8), (1100, 960, 12.0),
