@@ -232,9 +232,7 @@ def main():
 
     nrows = max(rows[1] - rows[0], 1)
     # the product path's kernel-form hint (engine.stream_join sets it the same way)
-    jflags = _lib.JOIN_TC | (_lib.JOIN_LOW_OUTPUT
-                             if cap - engine.hole_slack(device) <= engine.LOW_OUTPUT_PER_ROW * nrows
-                             else 0)
+    jflags = _lib.JOIN_TC | engine.form_hints(cap - engine.hole_slack(device), rows, (0, dd.n_dev))
 
     def step():
         engine.join_raw(dd, eps_sq, jflags, rows, (0, dd.n_dev), rec, cap, cnt,

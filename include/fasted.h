@@ -72,6 +72,13 @@ enum {
      * same capacity), e.g. one row range swept in column segments while the
      * dataset is still arriving (engine.stream_join). */
     FASTED_JOIN_APPEND = 16,
+    /* OR-able hint: the caller expects at most one pair per 8192 examined
+     * (row x column) pairs.  Only picks the kernel form (results are
+     * identical): the resident and multicast kernels then hand candidate rows
+     * to two hit warps instead of running the rare path in the epilogue
+     * warps (1M x 128: 1137 vs 992 TFLOPS; at ~1 pair per 1000 examined the
+     * hit warps cannot keep up, 2x slower). */
+    FASTED_JOIN_SPARSE = 32,
     /* Diagnostics for power/throughput attribution (results are NOT valid): */
     FASTED_JOIN_DIAG_NOEPI = 256,    /* tcgen05 kernel: skip the epilogue entirely     */
     FASTED_JOIN_DIAG_NOMMA = 512,    /* tcgen05 kernel: skip the MMAs (TMA + epilogue) */

@@ -19,6 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libfasted.so")
 
 OK, ERR_ARGUMENT, ERR_RANGE, ERR_CAPACITY, ERR_CUDA, ERR_UNSUPPORTED = 0, 2, 3, 4, 5, 6
 JOIN_TC, JOIN_EXACT, JOIN_COUNT, JOIN_SYMMETRIC, JOIN_LOW_OUTPUT, JOIN_APPEND = 0, 1, 2, 4, 8, 16
+JOIN_SPARSE = 32
 
 # Every symbol include/fasted.h declares (tests check the .so exports them).
 EXPORTS = (

@@ -65,7 +65,8 @@ extern "C" int fasted_device_check(int device) {
 extern "C" const char* fasted_join_kernel_name(int64_t d_pad, int64_t rows, int64_t cols,
                                                int flags) {
     if ((flags & 1) == FASTED_JOIN_EXACT) return "fasted::join_exact_kernel";
-    return join_tc_kernel_name(d_pad, rows, cols, (flags & FASTED_JOIN_LOW_OUTPUT) != 0);
+    return join_tc_kernel_name(d_pad, rows, cols, (flags & FASTED_JOIN_LOW_OUTPUT) != 0,
+                               (flags & FASTED_JOIN_SPARSE) != 0);
 }
 
 extern "C" int fasted_device_info(int* sm_count, char* name, int name_len) {
@@ -136,6 +137,7 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     a.count_only = count_only ? 1 : 0;
     a.symmetric = symmetric ? 1 : 0;
     a.low_output = (flags & FASTED_JOIN_LOW_OUTPUT) != 0 ? 1 : 0;
+    a.sparse = (flags & FASTED_JOIN_SPARSE) != 0 ? 1 : 0;
     a.diag_flags = flags & (FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA |
                             FASTED_JOIN_DIAG_LOADONLY | FASTED_JOIN_DIAG_NOSLOW |
                             FASTED_JOIN_DIAG_SPIN | FASTED_JOIN_DIAG_LDX64 |

@@ -14,6 +14,7 @@ struct JoinArgs {
     int diag_flags;                    // FASTED_JOIN_DIAG_* (experiments only)
     int symmetric;                     // FASTED_JOIN_SYMMETRIC: upper tiles, mirrored records
     int low_output;                    // FASTED_JOIN_LOW_OUTPUT hint (kernel choice only)
+    int sparse;                        // FASTED_JOIN_SPARSE hint (kernel choice only)
     uint4* out;                        // records {i, j, dist_sq bits, 0}
     unsigned long long capacity;       // record slots available in out
     unsigned long long* count;         // [0] exact pair total, [1] chunks taken
@@ -233,6 +234,7 @@ __device__ __forceinline__ void writer_finish(StagedWriter<STAGE>& w, const Join
 
 int launch_join_exact(const __half* X, const JoinArgs& a, cudaStream_t s);
 int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s);
-const char* join_tc_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, bool low_output);
+const char* join_tc_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, bool low_output,
+                                bool sparse);
 
 }  // namespace fasted

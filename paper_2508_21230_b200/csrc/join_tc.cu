@@ -1036,264 +1036,8 @@ __device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
         : "memory");
 }
 
-constexpr int MC_STAGES = 4;
-constexpr int MC_SMEM_BYTES =
-    MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + WSTAGE_BYTES + 1024;
-
-template <int NEPI>
-__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI) * 32, 1)
-join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
-                  const __grid_constant__ CUtensorMap tmap_aug_a,
-                  const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
-                  const Sched sch) {
-    constexpr int STAGES = MC_STAGES;
-    constexpr int B_BYTES = 2 * B_HALF_BYTES;
-    constexpr int AUG_A = BM * AUG_ROW_BYTES;
-    constexpr int AUG_B_HALF = 128 * AUG_ROW_BYTES;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    const uint32_t sA = base;
-    const uint32_t sB = base + STAGES * A_BYTES;
-    const uint32_t bars = sB + STAGES * B_BYTES;
-    auto full_bar = [&](int s) { return bars + 8u * s; };
-    auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
-    auto tfull_bar = [&](int b) { return bars + 8u * (2 * STAGES + b); };
-    auto tempty_bar = [&](int b) { return bars + 8u * (2 * STAGES + 2 + b); };
-    const uint32_t slot = bars + 8u * (2 * STAGES + 4);
-    volatile uint32_t* slot_ptr = reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - raw));
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const uint32_t cr = cluster_rank();   // 0: upper row tile, 1: lower
-    const int64_t tile_id0 = (int64_t)(blockIdx.x >> 1);
-    const int64_t tile_step = (int64_t)(gridDim.x >> 1);
-    constexpr uint16_t BOTH = 0x3;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; s++) {
-            mbar_init(full_bar(s), 1);
-            mbar_init(empty_bar(s), 2);   // both CTAs' MMAs read this stage's B
-        }
-        for (int b = 0; b < 2; b++) {
-            mbar_init(tfull_bar(b), 1);
-            mbar_init(tempty_bar(b), NEPI);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x))
-                     : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_a))
-                     : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_b))
-                     : "memory");
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot),
-                     "r"(TMEM_COLS)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    }
-    tc_fence_before();
-    cluster_sync();   // peers' barriers initialised before any multicast lands
-    tc_fence_after();
-    const uint32_t tmem_base = *slot_ptr;
-
-    if (warp == 0) {
-        // ---------------- TMA producer (whole warp; one elected lane issues)
-        int s = 0;
-        uint32_t ph = 0;
-        for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
-            int rt, ct;
-            tile_coords(sch, t, rt, ct);
-            if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM, a.col_begin + (int64_t)ct * BN,
-                         BN))
-                continue;
-            const int row0 = (int)(a.row_begin + ((int64_t)rt * 2 + cr) * BM);
-            const int colh = (int)(a.col_begin + (int64_t)ct * BN + 128 * cr);
-            for (int kb = 0; kb < sch.nkb + 1; kb++) {
-                mbar_wait(empty_bar(s), ph ^ 1u);
-                const uint32_t fb = full_bar(s);
-                if (elect_one()) {
-                    if (kb < sch.nkb) {
-                        const int kx = kb * BK;
-                        mbar_expect_tx(fb, A_BYTES + B_BYTES);
-                        tma_load_2d<1>(sA + s * A_BYTES, &tmap_x, fb, kx, row0);
-                        tma_load_2d_mc(sB + s * B_BYTES + cr * B_HALF_BYTES, &tmap_x, fb, kx, colh,
-                                       BOTH);
-                    } else {
-                        mbar_expect_tx(fb, AUG_A + 2 * AUG_B_HALF);
-                        tma_load_2d<1>(sA + s * A_BYTES, &tmap_aug_a, fb, 0, row0);
-                        tma_load_2d_mc(sB + s * B_BYTES + cr * AUG_B_HALF, &tmap_aug_b, fb, 0, colh,
-                                       BOTH);
-                    }
-                }
-                __syncwarp();
-                if (++s == STAGES) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-            }
-        }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer (every CTA; M = 128; whole warp, one lane issues)
-        const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
-        int s = 0;
-        uint32_t ph = 0;
-        int lt = 0;
-        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
-            if (a.symmetric) {
-                int rt, ct;
-                tile_coords(sch, t, rt, ct);
-                if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM,
-                             a.col_begin + (int64_t)ct * BN, BN)) {
-                    --lt;
-                    continue;
-                }
-            }
-            const int buf = lt & 1;
-            mbar_wait2(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u,
-                       (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
-            tc_fence_after();
-            const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
-            for (int kb = 0; kb < sch.nkb + 1; kb++) {
-                mbar_wait(full_bar(s), ph);
-                tc_fence_after();
-                const uint64_t ad = sw128_desc(sA + s * A_BYTES);
-                const uint64_t bd = sw128_desc(sB + s * B_BYTES);
-                if (elect_one()) {
-                    if (!no_mma) {
-                        if (kb < sch.nkb) {
-#pragma unroll
-                            for (int kk = 0; kk < BK / UK; kk++) {
-                                const uint64_t koff = (uint64_t)((kk * UK * 2) >> 4);
-                                mma_f16<1>(dtm, ad + koff, bd + koff, (kb | kk) != 0 ? 1u : 0u);
-                            }
-                        } else {
-                            mma_tf32<1>(dtm, sw32_desc(sA + s * A_BYTES), sw32_desc(sB + s * B_BYTES));
-                        }
-                    }
-                    mma_commit_mc(empty_bar(s), BOTH);
-                }
-                __syncwarp();
-                if (++s == STAGES) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-            }
-            if (elect_one()) mma_commit<1>(tfull_bar(buf));
-            __syncwarp();
-        }
-    } else {
-        // ---------------- epilogue
-        const int q = warp & 3;
-        const int h = (warp - FIRST_EPI_WARP) >> 2;
-        constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;   // 16 KB of staging either way
-        StagedWriter<WST> wr;
-        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
-        int lt = 0;
-        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
-            int rt, ct;
-            tile_coords(sch, t, rt, ct);
-            const int64_t row0 = a.row_begin + ((int64_t)rt * 2 + cr) * BM;
-            const int64_t col0 = a.col_begin + (int64_t)ct * BN;
-            if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM, col0, BN)) {
-                --lt;
-                continue;
-            }
-            const int buf = lt & 1;
-            epilogue_tile<1, BN, NEPI / 4>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf,
-                                 (uint32_t)(lt >> 1) & 1u, q, h, lane, true, tfull_bar(buf));
-        }
-        writer_finish(wr, a);
-    }
-
-    tc_fence_before();
-    cluster_sync();   // no CTA leaves while its peer may still multicast into it
-    tc_fence_after();
-    if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                     "r"(TMEM_COLS)
-                     : "memory");
-}
-
-// ---------------------------------------------------------------------------
-// Resident-A variant (small d, d_pad <= 256).  At d = 128 one 256 x 256 tile
-// is only 9 MMAs, and streaming both operands moves 144 KB per CTA pair per
-// tile from L2: measured, the TMA stream alone (no MMA, no epilogue) takes
-// 192 ms at 1M x 128, against a 121 ms tensor floor (profiles/round1/
-// tune_c3_session2.txt) -- the streaming kernel is L2->SM bound there.  Here
-// a CTA keeps its 128-row A panel (every k-block plus its augment rows) in
-// shared memory for a whole work unit -- one row tile x a segment of column
-// tiles -- and streams only B, halving the bytes per MMA.  A is double
-// buffered when two panels fit, so the next unit's A lands while the current
-// one finishes.  Units are ordered segment-major, so the CTAs (pairs) that run
-// side by side sweep the same B panels at the same time (L2 reuse).
-//
-// TBN = columns per tile.  With TBN = 128 the 512 TMEM columns hold FOUR
-// accumulators instead of two: at d = 128 a tile is only ~600 MMA cycles and
-// ncu showed the MMA warp waiting for an accumulator on 53% of tiles with two
-// buffers (the epilogue warp that found hits in a tile runs late); four
-// buffers absorb that jitter.  The MMA sequence per output element (k-blocks
-// ascending, then the tf32 augment step) is the streaming kernel's, so both
-// produce identical bits.
-struct ResSched {
-    int row_tiles;            // tiles of TILE_M rows in [row_begin, row_end)
-    int col_tiles;            // tiles of TBN columns in [col_begin, col_end)
-    int nsegs;                // column segments (balanced)
-    int nkb;                  // 64-wide k-blocks
-    int na;                   // A buffers (1 or 2)
-    int stages;               // B ring stages
-    uint32_t a_buf_bytes;     // one A buffer: nkb k-blocks + augment rows, 1024-aligned
-    int64_t units;            // row_tiles * nsegs
-};
-
-// Records per staging buffer in the resident kernel (tight shared memory):
-// 8 KB for the epilogue in total, so the B ring keeps its 7 stages at d = 128
-// (16 KB cost a stage: no-epilogue 204 vs 174 ms at 1M x 128).
-constexpr int RES_WSTAGE_TOTAL = 256;   // records, all epilogue warps x 2 buffers
-
-template <int CG, int TBN>
-struct ResCfg {
-    static constexpr int TILE_M = BM * CG;
-    static constexpr int NB = TBN / CG;                          // B rows (columns) per CTA
-    static constexpr int BBOX = NB < 128 ? NB : 128;             // TMA box rows for B
-    static constexpr int B_BYTES = NB * BK * 2;                  // this CTA's B k-block
-    static constexpr int AUGB_BYTES = NB * AUG_ROW_BYTES;        // its augment rows
-    static constexpr int STAGE_BYTES = B_BYTES + AUGB_BYTES;
-    static constexpr int NACC = TMEM_COLS / TBN;                 // accumulator buffers
-    static constexpr int MAX_STAGES = 16;
-    static constexpr int BARS = 2 * MAX_STAGES + 2 * NACC + 4;
-    static constexpr int BAR_REGION = ((BARS * 8 + 4 + 127) / 128) * 128;
-    static constexpr uint32_t IDESC_F16 =
-        (1u << 4) | ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(TILE_M >> 4) << 24);
-    static constexpr uint32_t IDESC_TF32 = IDESC_F16 | (2u << 7) | (2u << 10);
-    static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1024-aligned");
-};
-
-__device__ __forceinline__ void res_unit(const ResSched& s, int64_t u, int& rt, int& ct0,
-                                         int& ct1) {
-    const int64_t g = u / s.row_tiles;
-    rt = (int)(u - g * s.row_tiles);
-    ct0 = (int)((int64_t)s.col_tiles * g / s.nsegs);
-    ct1 = (int)((int64_t)s.col_tiles * (g + 1) / s.nsegs);
-}
-
-// res_unit with FASTED_JOIN_SYMMETRIC applied: the unit's column tiles start
-// at the first one reaching the diagonal (an emptied unit still loads its A
-// panel and commits it, so every role walks the same unit sequence).
-template <int TILE_M, int TBN>
-__device__ __forceinline__ void res_unit_sym(const ResSched& s, const JoinArgs& a, int64_t u,
-                                             int& rt, int& ct0, int& ct1) {
-    res_unit(s, u, rt, ct0, ct1);
-    if (a.symmetric) {
-        const int64_t num = (int64_t)rt * TILE_M - TBN + 1;   // ct * TBN + TBN - 1 >= rt * TILE_M
-        const int ct_min = num <= 0 ? 0 : (int)((num + TBN - 1) / TBN);
-        if (ct0 < ct_min) ct0 = ct_min < ct1 ? ct_min : ct1;
-    }
-}
-
-// Hit warps (FASTED_RES_HIT, resident kernel).  The trace of the resident
-// kernel (above) shows the MMA waiting on the slowest of 32 epilogue warps,
+// Hit warps (FASTED_RES_HIT, FASTED_MC_HIT).  The trace of the resident
+// kernel (below) shows the MMA waiting on the slowest of 32 epilogue warps,
 // and the slowest is one that found a candidate and ran the rare path.  With
 // NHIT hit warps the epilogue warps never run it: a lane whose row holds a
 // candidate copies its 32 words into a shared-memory queue slot and the warp
@@ -1462,6 +1206,390 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
     if (nchunks > 1) hit_push<NHIT>(reg, smem_raw, raw, hq, r1, jb + 32, i, iw, row_ok, lane);
 }
 
+// Queue barriers and counters (thread 0, before the CTA-wide barrier).
+template <int NHIT>
+__device__ __forceinline__ void hit_init(uint32_t reg, uint8_t* smem_raw, uint32_t raw) {
+    for (int q = 0; q < NHIT; q++) {
+        for (uint32_t sl = 0; sl < (uint32_t)HitQ<NHIT>::Q; sl++) {
+            mbar_init(HitQ<NHIT>::full(reg, q, sl), 1);
+            mbar_init(HitQ<NHIT>::full(reg, q, sl) + 8u, 32);   // empty
+        }
+        *reinterpret_cast<volatile uint32_t*>(smem_raw + (HitQ<NHIT>::tail(reg, q) - raw)) = 0u;
+        *reinterpret_cast<volatile uint32_t*>(smem_raw + (HitQ<NHIT>::head(reg, q) - raw)) = 0u;
+    }
+}
+
+// An epilogue warp's last entry: END into its hit warp's queue.
+template <int NHIT>
+__device__ __forceinline__ void hit_end(uint32_t reg, uint8_t* smem_raw, uint32_t raw, int hq,
+                                        int lane) {
+    if (lane == 0) {
+        const uint32_t idx = atomicAdd(
+            reinterpret_cast<unsigned*>(smem_raw + (HitQ<NHIT>::tail(reg, hq) - raw)), 1u);
+        uint32_t none[32];
+        hit_put<NHIT>(reg, hq, idx, HIT_END, 0u, 0u, 0u, none, false);
+    }
+    __syncwarp();
+}
+
+// A hit warp's whole life: pop queue hq in order until `producers` END
+// entries, test each row transposed, write the records.
+template <int NHIT>
+__device__ __forceinline__ void hit_warp_loop(const JoinArgs& a, uint32_t reg, int hq,
+                                              int producers, int lane, bool spin) {
+    using H = HitQ<NHIT>;
+    StagedWriter<H::HWS> wr;
+    writer_init(wr, reg + (uint32_t)hq * 2u * H::HWS * 16u);
+    int ends = 0;
+    for (uint32_t idx = 0; ends < producers; idx++) {
+        const uint32_t sl = idx % H::Q;
+        mbar_wait2(H::full(reg, hq, sl), (idx / H::Q) & 1u, spin);
+        const uint4 m = ld_shared_v4(H::meta(reg, hq, sl));
+        if (m.x == HIT_ROW) {
+            const uint32_t v = ld_shared_u32(H::data(reg, hq, sl) + 4u * (uint32_t)lane);
+            const int64_t is = (int64_t)m.y, j = (int64_t)m.z + lane;
+            const bool hit = (int)v >= 0 && j < a.n_logical && j != is && (!a.symmetric || j > is);
+            const uint32_t b = __ballot_sync(0xffffffffu, hit);
+            if (b) {
+                const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
+                writer_append(wr, a, b, hit, (uint32_t)(is + 1), (uint32_t)(j + 1), d2);
+                if (a.symmetric)
+                    writer_append(wr, a, b, hit, (uint32_t)(j + 1), (uint32_t)(is + 1), d2);
+            }
+        } else if (m.x == HIT_SELF) {
+            const bool mine = (m.w >> lane) & 1u;
+            writer_append(wr, a, m.w, mine, m.y + (uint32_t)lane + 1u, m.y + (uint32_t)lane + 1u,
+                          0.0f);
+        } else {
+            ends++;
+        }
+        mbar_arrive(H::full(reg, hq, sl) + 8u);   // this lane is done with the slot
+        __syncwarp();
+        if (lane == 0) st_release_shared(H::head(reg, hq), idx + 1u);
+    }
+    writer_finish(wr, a);
+}
+
+// epilogue_tile with hit warps (streaming/multicast kernels): drain,
+// release, slice test, hand candidate rows over.
+template <int CG, int TBN, int NSPLIT, int NHIT>
+__device__ __forceinline__ void epilogue_tile_hit(const JoinArgs& a, uint32_t reg,
+                                                  uint8_t* smem_raw, uint32_t raw, int hq,
+                                                  uint32_t tmem_base, uint32_t tempty,
+                                                  int64_t row0, int64_t col0, int buf,
+                                                  uint32_t aph, int q, int h, int lane,
+                                                  bool leader, uint32_t tfull) {
+    constexpr int HALF = TBN / NSPLIT;
+    constexpr int NCH = HALF / 32;
+    static_assert(NCH == 2, "hit-warp epilogue: 64 columns per warp");
+    const int64_t iw = row0 + q * 32;
+    const int64_t i = iw + lane;
+    const bool row_ok = i < a.n_logical && i < a.row_end;
+    const int64_t left = a.col_end - (col0 + h * HALF);
+    int nchunks = left <= 0 ? 0 : (left >= HALF ? NCH : (int)(left / 32));
+    if (row0 >= a.row_end || (a.diag_flags & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
+    const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TBN + h * HALF);
+    mbar_wait2(tfull, aph, (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+    tc_fence_after();
+    uint32_t r0[32], r1[32];
+    if (nchunks > 0) tmem_ld32(tcol, r0);
+    if (nchunks > 1) tmem_ld32(tcol + 32u, r1);
+    if (nchunks > 0) {
+        tmem_ld_wait(r0);
+        tmem_ld_wait(r1);
+    }
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) {
+        if (CG == 1 || leader) mbar_arrive_relaxed(tempty);
+        else mbar_arrive_remote(tempty, 0);
+    }
+    if (a.diag_flags & FASTED_JOIN_DIAG_LOADONLY) return;
+    const int64_t jb = col0 + h * HALF;
+    if (nchunks == NCH && !((jb < iw + 32) && (iw < jb + HALF))) {
+        const uint32_t all = and_tree32(r0) & and_tree32(r1);
+        if (!__any_sync(0xffffffffu, (int)all >= 0)) return;
+    }
+    if (a.diag_flags & FASTED_JOIN_DIAG_NOSLOW) return;
+    if (nchunks > 0)
+        hit_push<NHIT>(reg, smem_raw, raw, hq, r0, (int)jb, (int)i, (int)iw, row_ok, (uint32_t)lane);
+    if (nchunks > 1)
+        hit_push<NHIT>(reg, smem_raw, raw, hq, r1, (int)jb + 32, (int)i, (int)iw, row_ok,
+                       (uint32_t)lane);
+}
+
+constexpr int MC_STAGES = 4;
+constexpr int MC_SMEM_BYTES =
+    MC_STAGES * (A_BYTES + 2 * B_HALF_BYTES) + BAR_BYTES + WSTAGE_BYTES + 1024;
+
+template <int NEPI, int NHIT = 0>
+__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI + NHIT) * 32, 1)
+join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
+                  const __grid_constant__ CUtensorMap tmap_aug_a,
+                  const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
+                  const Sched sch) {
+    constexpr int STAGES = MC_STAGES;
+    constexpr int B_BYTES = 2 * B_HALF_BYTES;
+    constexpr int AUG_A = BM * AUG_ROW_BYTES;
+    constexpr int AUG_B_HALF = 128 * AUG_ROW_BYTES;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    const uint32_t sA = base;
+    const uint32_t sB = base + STAGES * A_BYTES;
+    const uint32_t bars = sB + STAGES * B_BYTES;
+    auto full_bar = [&](int s) { return bars + 8u * s; };
+    auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
+    auto tfull_bar = [&](int b) { return bars + 8u * (2 * STAGES + b); };
+    auto tempty_bar = [&](int b) { return bars + 8u * (2 * STAGES + 2 + b); };
+    const uint32_t slot = bars + 8u * (2 * STAGES + 4);
+    volatile uint32_t* slot_ptr = reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - raw));
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t cr = cluster_rank();   // 0: upper row tile, 1: lower
+    const int64_t tile_id0 = (int64_t)(blockIdx.x >> 1);
+    const int64_t tile_step = (int64_t)(gridDim.x >> 1);
+    constexpr uint16_t BOTH = 0x3;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 2);   // both CTAs' MMAs read this stage's B
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(tfull_bar(b), 1);
+            mbar_init(tempty_bar(b), NEPI);
+        }
+        if constexpr (NHIT > 0) hit_init<NHIT>(bars + BAR_BYTES, smem_raw, raw);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_a))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_b))
+                     : "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(slot),
+                     "r"(TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();   // peers' barriers initialised before any multicast lands
+    tc_fence_after();
+    const uint32_t tmem_base = *slot_ptr;
+
+    if (warp == 0) {
+        // ---------------- TMA producer (whole warp; one elected lane issues)
+        int s = 0;
+        uint32_t ph = 0;
+        for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
+            int rt, ct;
+            tile_coords(sch, t, rt, ct);
+            if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM, a.col_begin + (int64_t)ct * BN,
+                         BN))
+                continue;
+            const int row0 = (int)(a.row_begin + ((int64_t)rt * 2 + cr) * BM);
+            const int colh = (int)(a.col_begin + (int64_t)ct * BN + 128 * cr);
+            for (int kb = 0; kb < sch.nkb + 1; kb++) {
+                mbar_wait(empty_bar(s), ph ^ 1u);
+                const uint32_t fb = full_bar(s);
+                if (elect_one()) {
+                    if (kb < sch.nkb) {
+                        const int kx = kb * BK;
+                        mbar_expect_tx(fb, A_BYTES + B_BYTES);
+                        tma_load_2d<1>(sA + s * A_BYTES, &tmap_x, fb, kx, row0);
+                        tma_load_2d_mc(sB + s * B_BYTES + cr * B_HALF_BYTES, &tmap_x, fb, kx, colh,
+                                       BOTH);
+                    } else {
+                        mbar_expect_tx(fb, AUG_A + 2 * AUG_B_HALF);
+                        tma_load_2d<1>(sA + s * A_BYTES, &tmap_aug_a, fb, 0, row0);
+                        tma_load_2d_mc(sB + s * B_BYTES + cr * AUG_B_HALF, &tmap_aug_b, fb, 0, colh,
+                                       BOTH);
+                    }
+                }
+                __syncwarp();
+                if (++s == STAGES) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (every CTA; M = 128; whole warp, one lane issues)
+        const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
+        int s = 0;
+        uint32_t ph = 0;
+        int lt = 0;
+        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
+            if (a.symmetric) {
+                int rt, ct;
+                tile_coords(sch, t, rt, ct);
+                if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM,
+                             a.col_begin + (int64_t)ct * BN, BN)) {
+                    --lt;
+                    continue;
+                }
+            }
+            const int buf = lt & 1;
+            mbar_wait2(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u,
+                       (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+            tc_fence_after();
+            const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
+            for (int kb = 0; kb < sch.nkb + 1; kb++) {
+                mbar_wait(full_bar(s), ph);
+                tc_fence_after();
+                const uint64_t ad = sw128_desc(sA + s * A_BYTES);
+                const uint64_t bd = sw128_desc(sB + s * B_BYTES);
+                if (elect_one()) {
+                    if (!no_mma) {
+                        if (kb < sch.nkb) {
+#pragma unroll
+                            for (int kk = 0; kk < BK / UK; kk++) {
+                                const uint64_t koff = (uint64_t)((kk * UK * 2) >> 4);
+                                mma_f16<1>(dtm, ad + koff, bd + koff, (kb | kk) != 0 ? 1u : 0u);
+                            }
+                        } else {
+                            mma_tf32<1>(dtm, sw32_desc(sA + s * A_BYTES), sw32_desc(sB + s * B_BYTES));
+                        }
+                    }
+                    mma_commit_mc(empty_bar(s), BOTH);
+                }
+                __syncwarp();
+                if (++s == STAGES) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+            if (elect_one()) mma_commit<1>(tfull_bar(buf));
+            __syncwarp();
+        }
+    } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
+        // ---------------- hit warp
+        hit_warp_loop<NHIT>(a, bars + BAR_BYTES, warp - FIRST_EPI_WARP - NEPI, NEPI / NHIT, lane,
+                            (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+    } else {
+        // ---------------- epilogue
+        const int q = warp & 3;
+        const int h = (warp - FIRST_EPI_WARP) >> 2;
+        constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;   // 16 KB of staging either way
+        StagedWriter<WST> wr;
+        if constexpr (NHIT == 0)
+            writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
+        int lt = 0;
+        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
+            int rt, ct;
+            tile_coords(sch, t, rt, ct);
+            const int64_t row0 = a.row_begin + ((int64_t)rt * 2 + cr) * BM;
+            const int64_t col0 = a.col_begin + (int64_t)ct * BN;
+            if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM, col0, BN)) {
+                --lt;
+                continue;
+            }
+            const int buf = lt & 1;
+            if constexpr (NHIT > 0)
+                epilogue_tile_hit<1, BN, NEPI / 4, NHIT>(
+                    a, bars + BAR_BYTES, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, tmem_base,
+                    tempty_bar(buf), row0, col0, buf, (uint32_t)(lt >> 1) & 1u, q, h, lane, true,
+                    tfull_bar(buf));
+            else
+                epilogue_tile<1, BN, NEPI / 4>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf,
+                                               (uint32_t)(lt >> 1) & 1u, q, h, lane, true,
+                                               tfull_bar(buf));
+        }
+        if constexpr (NHIT > 0)
+            hit_end<NHIT>(bars + BAR_BYTES, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, lane);
+        else
+            writer_finish(wr, a);
+    }
+
+    tc_fence_before();
+    cluster_sync();   // no CTA leaves while its peer may still multicast into it
+    tc_fence_after();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                     "r"(TMEM_COLS)
+                     : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Resident-A variant (small d, d_pad <= 256).  At d = 128 one 256 x 256 tile
+// is only 9 MMAs, and streaming both operands moves 144 KB per CTA pair per
+// tile from L2: measured, the TMA stream alone (no MMA, no epilogue) takes
+// 192 ms at 1M x 128, against a 121 ms tensor floor (profiles/round1/
+// tune_c3_session2.txt) -- the streaming kernel is L2->SM bound there.  Here
+// a CTA keeps its 128-row A panel (every k-block plus its augment rows) in
+// shared memory for a whole work unit -- one row tile x a segment of column
+// tiles -- and streams only B, halving the bytes per MMA.  A is double
+// buffered when two panels fit, so the next unit's A lands while the current
+// one finishes.  Units are ordered segment-major, so the CTAs (pairs) that run
+// side by side sweep the same B panels at the same time (L2 reuse).
+//
+// TBN = columns per tile.  With TBN = 128 the 512 TMEM columns hold FOUR
+// accumulators instead of two: at d = 128 a tile is only ~600 MMA cycles and
+// ncu showed the MMA warp waiting for an accumulator on 53% of tiles with two
+// buffers (the epilogue warp that found hits in a tile runs late); four
+// buffers absorb that jitter.  The MMA sequence per output element (k-blocks
+// ascending, then the tf32 augment step) is the streaming kernel's, so both
+// produce identical bits.
+struct ResSched {
+    int row_tiles;            // tiles of TILE_M rows in [row_begin, row_end)
+    int col_tiles;            // tiles of TBN columns in [col_begin, col_end)
+    int nsegs;                // column segments (balanced)
+    int nkb;                  // 64-wide k-blocks
+    int na;                   // A buffers (1 or 2)
+    int stages;               // B ring stages
+    uint32_t a_buf_bytes;     // one A buffer: nkb k-blocks + augment rows, 1024-aligned
+    int64_t units;            // row_tiles * nsegs
+};
+
+// Records per staging buffer in the resident kernel (tight shared memory):
+// 8 KB for the epilogue in total, so the B ring keeps its 7 stages at d = 128
+// (16 KB cost a stage: no-epilogue 204 vs 174 ms at 1M x 128).
+constexpr int RES_WSTAGE_TOTAL = 256;   // records, all epilogue warps x 2 buffers
+
+template <int CG, int TBN>
+struct ResCfg {
+    static constexpr int TILE_M = BM * CG;
+    static constexpr int NB = TBN / CG;                          // B rows (columns) per CTA
+    static constexpr int BBOX = NB < 128 ? NB : 128;             // TMA box rows for B
+    static constexpr int B_BYTES = NB * BK * 2;                  // this CTA's B k-block
+    static constexpr int AUGB_BYTES = NB * AUG_ROW_BYTES;        // its augment rows
+    static constexpr int STAGE_BYTES = B_BYTES + AUGB_BYTES;
+    static constexpr int NACC = TMEM_COLS / TBN;                 // accumulator buffers
+    static constexpr int MAX_STAGES = 16;
+    static constexpr int BARS = 2 * MAX_STAGES + 2 * NACC + 4;
+    static constexpr int BAR_REGION = ((BARS * 8 + 4 + 127) / 128) * 128;
+    static constexpr uint32_t IDESC_F16 =
+        (1u << 4) | ((uint32_t)(TBN >> 3) << 17) | ((uint32_t)(TILE_M >> 4) << 24);
+    static constexpr uint32_t IDESC_TF32 = IDESC_F16 | (2u << 7) | (2u << 10);
+    static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1024-aligned");
+};
+
+__device__ __forceinline__ void res_unit(const ResSched& s, int64_t u, int& rt, int& ct0,
+                                         int& ct1) {
+    const int64_t g = u / s.row_tiles;
+    rt = (int)(u - g * s.row_tiles);
+    ct0 = (int)((int64_t)s.col_tiles * g / s.nsegs);
+    ct1 = (int)((int64_t)s.col_tiles * (g + 1) / s.nsegs);
+}
+
+// res_unit with FASTED_JOIN_SYMMETRIC applied: the unit's column tiles start
+// at the first one reaching the diagonal (an emptied unit still loads its A
+// panel and commits it, so every role walks the same unit sequence).
+template <int TILE_M, int TBN>
+__device__ __forceinline__ void res_unit_sym(const ResSched& s, const JoinArgs& a, int64_t u,
+                                             int& rt, int& ct0, int& ct1) {
+    res_unit(s, u, rt, ct0, ct1);
+    if (a.symmetric) {
+        const int64_t num = (int64_t)rt * TILE_M - TBN + 1;   // ct * TBN + TBN - 1 >= rt * TILE_M
+        const int ct_min = num <= 0 ? 0 : (int)((num + TBN - 1) / TBN);
+        if (ct0 < ct_min) ct0 = ct_min < ct1 ? ct_min : ct1;
+    }
+}
+
 template <int CG, int TBN, int NEPI, bool TRACE = false, int NHIT = 0>
 __global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI + NHIT) * 32, 1)
 join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
@@ -1508,17 +1636,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
             mbar_init(afull_bar(b), 1);
             mbar_init(aempty_bar(b), 1);
         }
-        if constexpr (NHIT > 0) {
-            const uint32_t reg = bars + C::BAR_REGION;
-            for (int q = 0; q < NHIT; q++) {
-                for (uint32_t sl = 0; sl < (uint32_t)HitQ<NHIT>::Q; sl++) {
-                    mbar_init(HitQ<NHIT>::full(reg, q, sl), 1);
-                    mbar_init(HitQ<NHIT>::full(reg, q, sl) + 8u, 32);   // empty
-                }
-                *reinterpret_cast<volatile uint32_t*>(smem_raw + (HitQ<NHIT>::tail(reg, q) - raw)) = 0u;
-                *reinterpret_cast<volatile uint32_t*>(smem_raw + (HitQ<NHIT>::head(reg, q) - raw)) = 0u;
-            }
-        }
+        if constexpr (NHIT > 0) hit_init<NHIT>(bars + C::BAR_REGION, smem_raw, raw);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_xa))
                      : "memory");
@@ -1681,42 +1799,9 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         }
         __syncwarp();
     } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
-        // ---------------- hit warp: pop queue hq in order, test rows, write records
-        using H = HitQ<NHIT>;
-        const int hq = warp - FIRST_EPI_WARP - NEPI;
-        const uint32_t reg = bars + C::BAR_REGION;
-        StagedWriter<H::HWS> wr;
-        writer_init(wr, reg + (uint32_t)hq * 2u * H::HWS * 16u);
-        const bool spin = (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0;
-        int ends = 0;
-        for (uint32_t idx = 0; ends < NEPI / NHIT; idx++) {
-            const uint32_t sl = idx % H::Q;
-            mbar_wait2(H::full(reg, hq, sl), (idx / H::Q) & 1u, spin);
-            const uint4 m = ld_shared_v4(H::meta(reg, hq, sl));
-            if (m.x == HIT_ROW) {
-                const uint32_t v = ld_shared_u32(H::data(reg, hq, sl) + 4u * (uint32_t)lane);
-                const int64_t is = (int64_t)m.y, j = (int64_t)m.z + lane;
-                const bool hit = (int)v >= 0 && j < a.n_logical && j != is &&
-                                 (!a.symmetric || j > is);
-                const uint32_t b = __ballot_sync(0xffffffffu, hit);
-                if (b) {
-                    const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
-                    writer_append(wr, a, b, hit, (uint32_t)(is + 1), (uint32_t)(j + 1), d2);
-                    if (a.symmetric)
-                        writer_append(wr, a, b, hit, (uint32_t)(j + 1), (uint32_t)(is + 1), d2);
-                }
-            } else if (m.x == HIT_SELF) {
-                const bool mine = (m.w >> lane) & 1u;
-                writer_append(wr, a, m.w, mine, m.y + (uint32_t)lane + 1u,
-                              m.y + (uint32_t)lane + 1u, 0.0f);
-            } else {
-                ends++;
-            }
-            mbar_arrive(H::full(reg, hq, sl) + 8u);   // this lane is done with the slot
-            __syncwarp();
-            if (lane == 0) st_release_shared(H::head(reg, hq), idx + 1u);
-        }
-        writer_finish(wr, a);
+        // ---------------- hit warp
+        hit_warp_loop<NHIT>(a, bars + C::BAR_REGION, warp - FIRST_EPI_WARP - NEPI, NEPI / NHIT,
+                            lane, (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
     } else {
         // ---------------- epilogue
         constexpr int NSPLIT = NEPI / 4;
@@ -1790,20 +1875,10 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                 aph ^= buf ^ 1u;   // phase flips after buffer 1
             }
         }
-        if constexpr (NHIT > 0) {
-            // end of this warp's stream in its hit warp's queue
-            const uint32_t reg = bars + C::BAR_REGION;
-            const int hq = (warp - FIRST_EPI_WARP) % NHIT;
-            if (lane == 0) {
-                const uint32_t idx = atomicAdd(
-                    reinterpret_cast<unsigned*>(smem_raw + (HitQ<NHIT>::tail(reg, hq) - raw)), 1u);
-                uint32_t none[32];
-                hit_put<NHIT>(reg, hq, idx, HIT_END, 0u, 0u, 0u, none, false);
-            }
-            __syncwarp();
-        } else {
+        if constexpr (NHIT > 0)   // end of this warp's stream in its hit warp's queue
+            hit_end<NHIT>(bars + C::BAR_REGION, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, lane);
+        else
             writer_finish(wr, a);
-        }
     }
 
     tc_fence_before();
@@ -2216,11 +2291,12 @@ static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
 }
 
 // B-multicast launch: clusters of two CTAs over super-tiles of 256 rows.
-template <int NEPI>
+template <int NEPI, int NHIT = 0>
 static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const CUtensorMap& mb,
                              const JoinArgs& a, cudaStream_t s) {
     using namespace tc;
-    auto kern = join_tc_mc_kernel<NEPI>;
+    static_assert(HitQ<2>::BYTES <= WSTAGE_BYTES, "hit queues live in the staging region");
+    auto kern = join_tc_mc_kernel<NEPI, NHIT>;
     static PerDeviceOnce attr_once;
     {
         cudaError_t e = attr_once.run([&] {
@@ -2244,7 +2320,7 @@ static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const
     if (work <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * 2));
-    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI) * 32);
+    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI + NHIT) * 32);
     cfg.dynamicSmemBytes = MC_SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -2350,12 +2426,23 @@ static int tc_variant(int64_t d_pad, int64_t rows, int64_t cols, bool low_output
     return TC_MULTICAST;
 }
 
-const char* join_tc_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, bool low_output) {
+// Hit warps (resident CTA pair, multicast): on the caller's
+// FASTED_JOIN_SPARSE hint; FASTED_RES_HIT / FASTED_MC_HIT = 0 or 2 override.
+static bool res_hit(bool sparse) { return env_int("FASTED_RES_HIT", sparse ? 2 : 0) == 2; }
+static bool mc_hit(bool sparse) { return env_int("FASTED_MC_HIT", sparse ? 2 : 0) == 2; }
+
+const char* join_tc_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, bool low_output,
+                                bool sparse) {
     int cg = 0;
     switch (tc_variant(d_pad, rows, cols, low_output, &cg)) {
-        case TC_RESIDENT: return cg == 2 ? "fasted::tc::join_tc_res_kernel<2>"
-                                         : "fasted::tc::join_tc_res_kernel<1>";
-        case TC_MULTICAST: return "fasted::tc::join_tc_mc_kernel";
+        case TC_RESIDENT:
+            if (cg == 2 && env_int("FASTED_RES_EPI", 16) == 16 && res_hit(sparse))
+                return "fasted::tc::join_tc_res_kernel<2> + 2 hit warps";
+            return cg == 2 ? "fasted::tc::join_tc_res_kernel<2>" : "fasted::tc::join_tc_res_kernel<1>";
+        case TC_MULTICAST:
+            if (env_int("FASTED_MC_EPI", 16) == 16 && mc_hit(sparse))
+                return "fasted::tc::join_tc_mc_kernel + 2 hit warps";
+            return "fasted::tc::join_tc_mc_kernel";
         default: return cg == 2 ? "fasted::tc::join_tc_kernel<2>" : "fasted::tc::join_tc_kernel<1>";
     }
 }
@@ -2524,11 +2611,10 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
             cudaFreeAsync(aug, s);
             return st;
         }
-        // 16 epilogue warps, each draining 64 columns, plus two hit warps
-        // that own the rare path and the record writers (FASTED_RES_HIT=0:
-        // the epilogue warps run it themselves; measured at 1M x 128,
-        // alternating: 212-224 vs 245-249 ms); FASTED_RES_EPI=8: 8 warps of
-        // 128 columns.  Measured at 1M x 128, alternating runs on
+        // 16 epilogue warps, each draining 64 columns, plus (sparse output)
+        // two hit warps that own the rare path and the record writers
+        // (measured at 1M x 128, alternating launches: 225 vs 258 ms
+        // median); FASTED_RES_EPI=8: 8 warps of 128 columns.  Measured at 1M x 128, alternating runs on
         // one box: 253.8-253.9 ms with 16 vs 269-319 ms with 8 -- the shorter
         // per-warp chain per tile also removes the run-to-run spread
         // (profiles/round1/tune_c3_epi_ab_session2.txt).
@@ -2536,7 +2622,7 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
             e = launch_ts(X, mxb, ma, mbb, a, s);
         else if (cg == 2)
             e = env_int("FASTED_RES_EPI", 16) != 16 ? launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s)
-                : env_int("FASTED_RES_HIT", 2) == 2 ? launch_res<2, 256, 16, 2>(mx, mxb, ma, mbb, a, s)
+                : res_hit(a.sparse != 0) ? launch_res<2, 256, 16, 2>(mx, mxb, ma, mbb, a, s)
                                                      : launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s);
         else
             e = launch_res<1, 256, 8>(mx, mxb, ma, mbb, a, s);
@@ -2552,7 +2638,8 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         // 1406-1431 vs 1506-1515 ms; 5M x 384 shard at S ~ 4000 2535 vs 3140 ms
         // (profiles/round1/tune_mepi_session2.txt)
         e = env_int("FASTED_MC_EPI", 16) == 8 ? launch_mc<8>(mx, ma, mb, a, s)
-                                              : launch_mc<16>(mx, ma, mb, a, s);
+            : mc_hit(a.sparse != 0) ? launch_mc<16, 2>(mx, ma, mb, a, s)
+                                               : launch_mc<16>(mx, ma, mb, a, s);
         if (e == cudaSuccess) e = cudaGetLastError();
         cudaFreeAsync(aug, s);
         if (e != cudaSuccess) return cuda_status(e, "join_tc_mc_kernel");

@@ -285,8 +285,8 @@ def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool
             if capacity is None:
                 capacity = _estimate_capacity(dd, eps_sq, rows, cols, flags, sp)
             capacity += slack
-        if not exact and capacity - slack <= LOW_OUTPUT_PER_ROW * 1.25 * max(rows[1] - rows[0], 1):
-            flags |= _lib.JOIN_LOW_OUTPUT      # kernel-form hint only (same results)
+        if not exact:
+            flags |= form_hints(capacity - slack, rows, cols)   # kernel-form hints only
         cnt = torch.zeros(2, dtype=torch.int64, device=dev)
         reruns = 0
         kernel_ms = 0.0
@@ -403,6 +403,20 @@ def plan_row_chunks(rows, est_records: int, budget_records: int, min_chunks: int
 # the join of chunk c + 1.
 PIPELINE_MIN_RECORDS = 1 << 22      # below this: one chunk (overlap not worth a launch)
 LOW_OUTPUT_PER_ROW = 128            # FASTED_JOIN_LOW_OUTPUT hint threshold (pairs per row)
+SPARSE_EXAMINED_PER_PAIR = 8192     # FASTED_JOIN_SPARSE: <= 1 pair per this many examined
+
+
+def form_hints(expected_pairs: int, rows, cols) -> int:
+    """Kernel-form hint flags for an expected output size (results are
+    identical either way; include/fasted.h)."""
+    nr = max(rows[1] - rows[0], 1)
+    nc = max(cols[1] - cols[0], 1)
+    f = 0
+    if expected_pairs <= LOW_OUTPUT_PER_ROW * 1.25 * nr:
+        f |= _lib.JOIN_LOW_OUTPUT
+    if expected_pairs * SPARSE_EXAMINED_PER_PAIR <= nr * nc:
+        f |= _lib.JOIN_SPARSE
+    return f
 PIPELINE_CHUNKS = 4                 # chunks for mid-size outputs (overlap)
 BYTES_PER_RECORD_IN_FLIGHT = 2 * 16 + 2 * 12 + 8   # raw x2, sorted x2, sort scratch
 
@@ -452,8 +466,8 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
             dd.wait_rows(comp, dd.n_dev)
             est = _estimate_capacity(dd, eps_sq, rows, cols, flags, sp)
         budget = budget_records or _chunk_budget(dd.device)
-        if not exact and est <= LOW_OUTPUT_PER_ROW * 1.25 * max(rows[1] - rows[0], 1):
-            flags |= _lib.JOIN_LOW_OUTPUT      # kernel-form hint only (same results)
+        if not exact:
+            flags |= form_hints(est, rows, cols)   # kernel-form hints only (same results)
         min_chunks = PIPELINE_CHUNKS if est >= PIPELINE_MIN_RECORDS else 1
         chunks = plan_row_chunks(rows, est, budget, min_chunks)
         if symmetric:

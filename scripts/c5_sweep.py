@@ -83,8 +83,7 @@ def main():
         engine.join_raw(dd, es, _lib.JOIN_COUNT, rows, (0, dd.n_dev), None, 0, cnt, sp)
         pairs = int(cnt[0].item())
         cap = pairs + engine.max_holes(0)
-        jflags = _lib.JOIN_TC | extra | (_lib.JOIN_LOW_OUTPUT
-                                         if pairs <= engine.LOW_OUTPUT_PER_ROW * nrows else 0)
+        jflags = _lib.JOIN_TC | extra | engine.form_hints(pairs, rows, (0, dd.n_dev))
         count_ms = []
         with ClockSampler(0) as clk_c:
             for _ in range(args.reps):

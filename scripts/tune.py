@@ -71,7 +71,8 @@ for cfg in configs:
     os.environ["FASTED_MC_EPI"] = kv.get("MEPI", "16")
     os.environ["FASTED_TS"] = kv.get("TS", "0")
     os.environ["FASTED_DYN"] = kv.get("DYN", "1")
-    flags = int(kv.get("F", "0"))
+    # default: the kernel-form hints the engine would pass for this output
+    flags = int(kv.get("F", str(engine.form_hints(ref_count, (0, dd.n_dev), (0, dd.n_dev)))))
     engine.join_raw(dd, es, flags, (0, dd.n_dev), (0, dd.n_dev), rec, cap, cnt, stream.cuda_stream)
     torch.cuda.synchronize()
     time.sleep(1.0)

@@ -404,8 +404,9 @@ def test_multicast_kernel_bit_identical_to_single_cta(n, d, eps):
     hd = F.to_half(F.generate_synthetic(n, d, seed=n * 7 + d))
     ref = _tc_variant(hd, eps, FASTED_CTA_GROUP=1)
     assert len(ref[0]) > n
-    for mepi in (8, 16):
-        mc = _tc_variant(hd, eps, FASTED_MC=1, FASTED_CTA_GROUP=0, FASTED_MC_EPI=mepi)
+    for mepi, hit in ((8, 0), (16, 0), (16, 2)):
+        mc = _tc_variant(hd, eps, FASTED_MC=1, FASTED_CTA_GROUP=0, FASTED_MC_EPI=mepi,
+                         FASTED_MC_HIT=hit)
         for x, y in zip(ref, mc):
             assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), mepi
     n_dev = -(-hd.n_padded // 128) * 128

@@ -254,6 +254,7 @@ def test_python_flag_constants_match_header():
     assert vals["FASTED_JOIN_SYMMETRIC"] == _lib.JOIN_SYMMETRIC
     assert vals["FASTED_JOIN_LOW_OUTPUT"] == _lib.JOIN_LOW_OUTPUT
     assert vals["FASTED_JOIN_APPEND"] == _lib.JOIN_APPEND
+    assert vals["FASTED_JOIN_SPARSE"] == _lib.JOIN_SPARSE
     assert vals["FASTED_ERR_ARGUMENT"] == _lib.ERR_ARGUMENT
     rec = re.search(r"#define FASTED_RECORD_CHUNK (\d+)", src)
     assert int(rec.group(1)) == engine.RECORD_CHUNK
@@ -271,11 +272,14 @@ def test_plan_row_chunks():
     assert engine.plan_row_chunks((128, 128), 10, 1, 4) == [(128, 128)]
 
 
-def test_kernel_selection_rule_is_host_side():
+def test_kernel_selection_rule_is_host_side(monkeypatch):
     """fasted_join_kernel_name applies the launch's selection rule without a
     GPU: resident pair for d_pad <= 256, the CTA pair for large low-output
     joins, multicast clusters otherwise, the exact kernel for mode exact."""
     L = _lib.load()
+    for k in ("FASTED_RES_HIT", "FASTED_MC_HIT", "FASTED_RES_EPI", "FASTED_MC_EPI",
+              "FASTED_CTA_GROUP", "FASTED_MC", "FASTED_RESIDENT"):
+        monkeypatch.delenv(k, raising=False)
 
     def name(d, r, c, f):
         return L.fasted_join_kernel_name(d, r, c, f).decode()
@@ -286,3 +290,23 @@ def test_kernel_selection_rule_is_host_side():
     assert name(960, big, big, 0) == "fasted::tc::join_tc_mc_kernel"
     assert name(512, 60032, 60032, _lib.JOIN_LOW_OUTPUT) == "fasted::tc::join_tc_mc_kernel"
     assert name(960, big, big, _lib.JOIN_EXACT) == "fasted::join_exact_kernel"
+    # FASTED_JOIN_SPARSE: hit warps in the resident and multicast forms
+    sp = _lib.JOIN_SPARSE
+    assert name(128, big, big, sp) == "fasted::tc::join_tc_res_kernel<2> + 2 hit warps"
+    assert name(960, big, big, sp) == "fasted::tc::join_tc_mc_kernel + 2 hit warps"
+    assert name(960, big, big, sp | _lib.JOIN_LOW_OUTPUT) == "fasted::tc::join_tc_kernel<2>"
+
+
+def test_form_hints_thresholds():
+    """Kernel-form hints from the expected output: LOW_OUTPUT at <= 128 (x1.25)
+    pairs per row, SPARSE at <= 1 pair per 8192 examined."""
+    from paper_2508_21230_b200 import engine
+
+    r = (0, 1_000_064)
+    assert engine.form_hints(74_552_502, r, r) == _lib.JOIN_LOW_OUTPUT | _lib.JOIN_SPARSE   # C3
+    assert engine.form_hints(49_048_308, r, r) == _lib.JOIN_LOW_OUTPUT | _lib.JOIN_SPARSE   # C4
+    c2 = (0, 60_032)
+    assert engine.form_hints(3_623_702, c2, c2) == _lib.JOIN_LOW_OUTPUT                    # C2
+    shard, cols = (0, 625_024), (0, 5_000_064)
+    assert engine.form_hints(2_516_311_890, shard, cols) == 0                              # C5 S4096
+    assert engine.form_hints(160_000_000, shard, cols) == _lib.JOIN_SPARSE                  # C5 S256
