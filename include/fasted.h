@@ -74,10 +74,10 @@ enum {
     FASTED_JOIN_APPEND = 16,
     /* OR-able hint: the caller expects at most one pair per 8192 examined
      * (row x column) pairs.  Only picks the kernel form (results are
-     * identical): the resident and multicast kernels then hand candidate rows
-     * to two hit warps instead of running the rare path in the epilogue
-     * warps (1M x 128: 1137 vs 992 TFLOPS; at ~1 pair per 1000 examined the
-     * hit warps cannot keep up, 2x slower). */
+     * identical): the tcgen05 kernels then hand candidate rows to two hit
+     * warps instead of running the rare path in the epilogue warps (1M x
+     * 128: 1137 vs 992 TFLOPS; at ~1 pair per 1000 examined the hit warps
+     * cannot keep up, 2x slower). */
     FASTED_JOIN_SPARSE = 32,
     /* Diagnostics for power/throughput attribution (results are NOT valid): */
     FASTED_JOIN_DIAG_NOEPI = 256,    /* tcgen05 kernel: skip the epilogue entirely     */

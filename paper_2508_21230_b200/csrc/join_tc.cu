@@ -741,301 +741,6 @@ __device__ __forceinline__ void res_epi_tile(const JoinArgs& a, W& wr, uint32_t 
     if (NCH > 2 && nchunks > 3) epi_chunk_res(a, wr, r3, jb + 96, i, iw, row_ok);
 }
 
-template <int CG, bool DIAG, int NEPI = NUM_EPI_WARPS>
-__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI) * 32, 1)
-join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
-               const __grid_constant__ CUtensorMap tmap_aug_a,
-               const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
-               const Sched sch) {
-    using C = Cfg<CG>;
-    constexpr int STAGES = C::STAGES;
-    extern __shared__ uint8_t smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    const uint32_t sA = base;
-    const uint32_t sB = base + STAGES * A_BYTES;
-    const uint32_t bars = sB + STAGES * C::B_BYTES;
-    auto full_bar = [&](int s) { return bars + 8u * s; };
-    auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
-    auto tfull_bar = [&](int b) { return bars + 8u * (2 * STAGES + b); };
-    auto tempty_bar = [&](int b) { return bars + 8u * (2 * STAGES + 2 + b); };
-    const uint32_t slot = bars + 8u * (2 * STAGES + 4);
-    volatile uint32_t* slot_ptr =
-        reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - raw));
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
-    const bool leader = rank == 0;
-    const int64_t tile_id0 = CG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
-    const int64_t tile_step = CG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; s++) {
-            // CG = 2: only the leader's full barrier is used; the leader's
-            // expect_tx covers both CTAs' bytes and the peer's TMA completes
-            // its bytes there (it cannot run ahead a phase: it first waits
-            // for this stage's empty barrier, i.e. the previous phase done).
-            mbar_init(full_bar(s), 1);
-            mbar_init(empty_bar(s), 1);
-        }
-        for (int b = 0; b < 2; b++) {
-            mbar_init(tfull_bar(b), 1);
-            mbar_init(tempty_bar(b), NEPI * CG);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x))
-                     : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_a))
-                     : "memory");
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_b))
-                     : "memory");
-    }
-    if (warp == 0) {
-        if constexpr (CG == 1) {
-            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                             slot),
-                         "r"(TMEM_COLS)
-                         : "memory");
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-        } else {
-            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                             slot),
-                         "r"(TMEM_COLS)
-                         : "memory");
-            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-        }
-    }
-    tc_fence_before();
-    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem_base = *slot_ptr;
-
-    if (warp == 0) {
-        // ---------------- TMA producer: nkb FP16 stages + 1 augment stage per tile
-        // (whole warp walks the schedule; one elected lane issues)
-        {
-            uint64_t pol_evl;
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_evl));
-            int s = 0;
-            uint32_t ph = 0;
-            for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
-                int rt, ct;
-                tile_coords(sch, t, rt, ct);
-                const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M;
-                const int64_t col0 = DIAG ? row0 : a.col_begin + (int64_t)ct * BN;
-                if (sym_skip(a, row0, col0, BN)) continue;
-                // which 128-row halves exist (a half past the range end is skipped:
-                // its rows/columns are masked in the epilogue)
-                const bool a_hi = row0 + 128 < a.row_end;
-                const bool b_hi = col0 + 128 < a.col_end;
-                const int my_a = (int)(row0 + 128 * rank);
-                const bool a_mine = rank == 0 || a_hi;
-                for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
-                    mbar_wait(empty_bar(s), ph ^ 1u);
-                    const uint32_t fb = full_bar(s);
-                    if (elect_one()) {
-                    if (kb < sch.nkb) {
-                        const int kx = kb * BK;
-                        if constexpr (CG == 1) {
-                            mbar_expect_tx(fb, A_BYTES + (b_hi ? 2 : 1) * B_HALF_BYTES);
-                            tma_load_2d<1>(sA + s * A_BYTES, &tmap_x, fb, kx, (int)row0);
-                            tma_load_2d<1>(sB + s * C::B_BYTES, &tmap_x, fb, kx, (int)col0);
-                            if (b_hi)
-                                tma_load_2d<1>(sB + s * C::B_BYTES + B_HALF_BYTES, &tmap_x, fb, kx,
-                                               (int)col0 + 128);
-                        } else {
-                            if (leader)
-                                mbar_expect_tx(fb, (a_hi ? 2 : 1) * A_BYTES +
-                                                       (b_hi ? 2 : 1) * B_HALF_BYTES);
-                            if (a_mine)
-                            {
-                                if (a.diag_flags & FASTED_JOIN_DIAG_AEVL)
-                                    tma_load_2d_pair_hint(sA + s * A_BYTES, &tmap_x, fb, kx, my_a,
-                                                          pol_evl);
-                                else
-                                    tma_load_2d<2>(sA + s * A_BYTES, &tmap_x, fb, kx, my_a);
-                            }
-                            if (rank == 0 || b_hi)
-                                tma_load_2d<2>(sB + s * C::B_BYTES, &tmap_x, fb, kx,
-                                               (int)(col0 + 128 * rank));
-                        }
-                    } else {
-                        constexpr int AUG_A = BM * AUG_ROW_BYTES;
-                        constexpr int AUG_B_HALF = 128 * AUG_ROW_BYTES;
-                        if constexpr (CG == 1) {
-                            mbar_expect_tx(fb, AUG_A + (b_hi ? 2 : 1) * AUG_B_HALF);
-                            tma_load_2d<1>(sA + s * A_BYTES, &tmap_aug_a, fb, 0, (int)row0);
-                            tma_load_2d<1>(sB + s * C::B_BYTES, &tmap_aug_b, fb, 0, (int)col0);
-                            if (b_hi)
-                                tma_load_2d<1>(sB + s * C::B_BYTES + AUG_B_HALF, &tmap_aug_b, fb,
-                                               0, (int)col0 + 128);
-                        } else {
-                            if (leader)
-                                mbar_expect_tx(fb, (a_hi ? 2 : 1) * AUG_A +
-                                                       (b_hi ? 2 : 1) * AUG_B_HALF);
-                            if (a_mine)
-                                tma_load_2d<2>(sA + s * A_BYTES, &tmap_aug_a, fb, 0, my_a);
-                            if (rank == 0 || b_hi)
-                                tma_load_2d<2>(sB + s * C::B_BYTES, &tmap_aug_b, fb, 0,
-                                               (int)(col0 + 128 * rank));
-                        }
-                    }
-                    }
-                    __syncwarp();
-                    if (++s == STAGES) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
-                }
-            }
-        }
-        __syncwarp();
-    } else if (warp == 1) {
-        // ---------------- MMA issuer (the leader CTA of a pair)
-        if (leader) {   // whole warp; one elected lane issues
-            const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
-            int s = 0;
-            uint32_t ph = 0;
-            int lt = 0;
-            for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
-                if (a.symmetric) {
-                    int rt, ct;
-                    tile_coords(sch, t, rt, ct);
-                    if (sym_skip(a, a.row_begin + (int64_t)rt * C::TILE_M,
-                                 a.col_begin + (int64_t)ct * BN, BN)) {
-                        --lt;
-                        continue;
-                    }
-                }
-                const int buf = lt & 1;
-                const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
-                mbar_wait(tempty_bar(buf), aph ^ 1u);
-                tc_fence_after();
-                const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
-                for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
-                    mbar_wait(full_bar(s), ph);
-                    tc_fence_after();
-                    if (elect_one()) {
-                    if (!no_mma) {
-                        if (kb < sch.nkb) {
-                            const uint64_t ad = sw128_desc(sA + s * A_BYTES);
-                            const uint64_t bd = sw128_desc(sB + s * C::B_BYTES);
-#pragma unroll
-                            for (int kk = 0; kk < BK / UK; kk++) {
-                                const uint64_t koff = (uint64_t)((kk * UK * 2) >> 4);
-                                mma_f16<CG>(dtm, ad + koff, bd + koff, (kb | kk) != 0 ? 1u : 0u);
-                            }
-                        } else {
-                            mma_tf32<CG>(dtm, sw32_desc(sA + s * A_BYTES),
-                                         sw32_desc(sB + s * C::B_BYTES));
-                        }
-                    }
-                    mma_commit<CG>(empty_bar(s));
-                    }
-                    __syncwarp();
-                    if (++s == STAGES) {
-                        s = 0;
-                        ph ^= 1u;
-                    }
-                }
-                if (elect_one()) mma_commit<CG>(tfull_bar(buf));
-                __syncwarp();
-            }
-        }
-        __syncwarp();
-    } else {
-        // ---------------- epilogue
-        const int q = warp & 3;          // TMEM lane quarter this warp may access
-        const int h = (warp - FIRST_EPI_WARP) >> 2;   // column half of the accumulator
-        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-        // staging: 16 KB for the epilogue warps (64 records per buffer with 8
-        // warps, 32 with 16)
-        constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;
-        StagedWriter<WST> wr;
-        writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
-        int lt = 0;
-        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
-            int rt, ct;
-            tile_coords(sch, t, rt, ct);
-            const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M + 128 * rank;
-            const int64_t col0 = a.col_begin + (int64_t)ct * BN;
-            if (sym_skip(a, a.row_begin + (int64_t)rt * C::TILE_M, col0, BN)) {
-                --lt;
-                continue;
-            }
-            const int buf = lt & 1;
-            const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
-            if constexpr (DIAG) {
-                const int64_t i = row0 + q * 32 + lane;
-                // Gram-diagonal pre-pass (CG = 1, col0 = row0): lane i's own
-                // column i - row0 = 32 q + lane sits in chunk q of half 0.
-                mbar_wait(tfull_bar(buf), aph);
-                tc_fence_after();
-                uint32_t r0[32];
-                if (h == 0) {
-                    tmem_ld32(tmem_base + lane_base + (uint32_t)(buf * BN + q * 32), r0);
-                    tmem_ld_wait(r0);
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive(tempty_bar(buf));
-                if (h == 0 && i < a.row_end) a.gram_diag[i] = __uint_as_float(pick32(r0, lane));
-                continue;
-            }
-            epilogue_tile<CG, BN, NEPI / 4>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf, aph, q, h,
-                              lane, leader, tfull_bar(buf));
-        }
-        writer_finish(wr, a);
-    }
-
-    tc_fence_before();
-    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
-    tc_fence_after();
-    if (warp == 0) {
-        if constexpr (CG == 1)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                         "r"(TMEM_COLS)
-                         : "memory");
-        else
-            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                         "r"(TMEM_COLS)
-                         : "memory");
-    }
-}
-
-// ---------------------------------------------------------------------------
-// B-multicast variant (large d).  At d = 960 the single-CTA kernel moves
-// 737 KB of A and B from L2 per 128 x 256 tile, and measurement says that
-// traffic, not the MMA, sets both the rate and the power: the TMA stream
-// alone (no MMA, no epilogue) runs at ~10 KB/clk chip-wide and takes 1452 ms
-// at the 1 kW cap against 1570 ms for the whole join (profiles/round1/
-// tune_c4_power_session2.txt).  Here two CTAs of a cluster take vertically
-// adjacent row tiles of the same column tile: each loads its own A and HALF
-// of the shared B tile, multicast into both CTAs' shared memory, so per SM
-// the bytes per tile drop by a third (491 KB).  Each CTA still issues its own
-// M = 128 MMAs (no cross-SM operand reads, unlike cta_group::2).  A stage is
-// refilled only after BOTH CTAs' MMAs released it (empty barrier count 2,
-// multicast commits).  Every load is issued even for a tile past the range
-// end (its rows/columns are masked in the epilogue; TMA zero-fills past
-// n_pad), so the byte counts are fixed.
-__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                               int c0, int c1, uint16_t mask) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-        ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
-        : "memory");
-}
-
-__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster."
-        "b64 [%0], %1;" ::"r"(bar),
-        "h"(mask)
-        : "memory");
-}
-
 // Hit warps (FASTED_RES_HIT, FASTED_MC_HIT).  The trace of the resident
 // kernel (below) shows the MMA waiting on the slowest of 32 epilogue warps,
 // and the slowest is one that found a candidate and ran the rare path.  With
@@ -1316,6 +1021,315 @@ __device__ __forceinline__ void epilogue_tile_hit(const JoinArgs& a, uint32_t re
     if (nchunks > 1)
         hit_push<NHIT>(reg, smem_raw, raw, hq, r1, (int)jb + 32, (int)i, (int)iw, row_ok,
                        (uint32_t)lane);
+}
+
+template <int CG, bool DIAG, int NEPI = NUM_EPI_WARPS, int NHIT = 0>
+__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI + NHIT) * 32, 1)
+join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
+               const __grid_constant__ CUtensorMap tmap_aug_a,
+               const __grid_constant__ CUtensorMap tmap_aug_b, const JoinArgs a,
+               const Sched sch) {
+    using C = Cfg<CG>;
+    constexpr int STAGES = C::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    const uint32_t sA = base;
+    const uint32_t sB = base + STAGES * A_BYTES;
+    const uint32_t bars = sB + STAGES * C::B_BYTES;
+    auto full_bar = [&](int s) { return bars + 8u * s; };
+    auto empty_bar = [&](int s) { return bars + 8u * (STAGES + s); };
+    auto tfull_bar = [&](int b) { return bars + 8u * (2 * STAGES + b); };
+    auto tempty_bar = [&](int b) { return bars + 8u * (2 * STAGES + 2 + b); };
+    const uint32_t slot = bars + 8u * (2 * STAGES + 4);
+    volatile uint32_t* slot_ptr =
+        reinterpret_cast<volatile uint32_t*>(smem_raw + (slot - raw));
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = CG == 2 ? cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    const int64_t tile_id0 = CG == 2 ? (int64_t)(blockIdx.x >> 1) : (int64_t)blockIdx.x;
+    const int64_t tile_step = CG == 2 ? (int64_t)(gridDim.x >> 1) : (int64_t)gridDim.x;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            // CG = 2: only the leader's full barrier is used; the leader's
+            // expect_tx covers both CTAs' bytes and the peer's TMA completes
+            // its bytes there (it cannot run ahead a phase: it first waits
+            // for this stage's empty barrier, i.e. the previous phase done).
+            mbar_init(full_bar(s), 1);
+            mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(tfull_bar(b), 1);
+            mbar_init(tempty_bar(b), NEPI * CG);
+        }
+        if constexpr (NHIT > 0) hit_init<NHIT>(bars + BAR_BYTES, smem_raw, raw);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_x))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_a))
+                     : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_aug_b))
+                     : "memory");
+    }
+    if (warp == 0) {
+        if constexpr (CG == 1) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             slot),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+        } else {
+            asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             slot),
+                         "r"(TMEM_COLS)
+                         : "memory");
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+        }
+    }
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *slot_ptr;
+
+    if (warp == 0) {
+        // ---------------- TMA producer: nkb FP16 stages + 1 augment stage per tile
+        // (whole warp walks the schedule; one elected lane issues)
+        {
+            uint64_t pol_evl;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_evl));
+            int s = 0;
+            uint32_t ph = 0;
+            for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
+                int rt, ct;
+                tile_coords(sch, t, rt, ct);
+                const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M;
+                const int64_t col0 = DIAG ? row0 : a.col_begin + (int64_t)ct * BN;
+                if (sym_skip(a, row0, col0, BN)) continue;
+                // which 128-row halves exist (a half past the range end is skipped:
+                // its rows/columns are masked in the epilogue)
+                const bool a_hi = row0 + 128 < a.row_end;
+                const bool b_hi = col0 + 128 < a.col_end;
+                const int my_a = (int)(row0 + 128 * rank);
+                const bool a_mine = rank == 0 || a_hi;
+                for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
+                    mbar_wait(empty_bar(s), ph ^ 1u);
+                    const uint32_t fb = full_bar(s);
+                    if (elect_one()) {
+                    if (kb < sch.nkb) {
+                        const int kx = kb * BK;
+                        if constexpr (CG == 1) {
+                            mbar_expect_tx(fb, A_BYTES + (b_hi ? 2 : 1) * B_HALF_BYTES);
+                            tma_load_2d<1>(sA + s * A_BYTES, &tmap_x, fb, kx, (int)row0);
+                            tma_load_2d<1>(sB + s * C::B_BYTES, &tmap_x, fb, kx, (int)col0);
+                            if (b_hi)
+                                tma_load_2d<1>(sB + s * C::B_BYTES + B_HALF_BYTES, &tmap_x, fb, kx,
+                                               (int)col0 + 128);
+                        } else {
+                            if (leader)
+                                mbar_expect_tx(fb, (a_hi ? 2 : 1) * A_BYTES +
+                                                       (b_hi ? 2 : 1) * B_HALF_BYTES);
+                            if (a_mine)
+                            {
+                                if (a.diag_flags & FASTED_JOIN_DIAG_AEVL)
+                                    tma_load_2d_pair_hint(sA + s * A_BYTES, &tmap_x, fb, kx, my_a,
+                                                          pol_evl);
+                                else
+                                    tma_load_2d<2>(sA + s * A_BYTES, &tmap_x, fb, kx, my_a);
+                            }
+                            if (rank == 0 || b_hi)
+                                tma_load_2d<2>(sB + s * C::B_BYTES, &tmap_x, fb, kx,
+                                               (int)(col0 + 128 * rank));
+                        }
+                    } else {
+                        constexpr int AUG_A = BM * AUG_ROW_BYTES;
+                        constexpr int AUG_B_HALF = 128 * AUG_ROW_BYTES;
+                        if constexpr (CG == 1) {
+                            mbar_expect_tx(fb, AUG_A + (b_hi ? 2 : 1) * AUG_B_HALF);
+                            tma_load_2d<1>(sA + s * A_BYTES, &tmap_aug_a, fb, 0, (int)row0);
+                            tma_load_2d<1>(sB + s * C::B_BYTES, &tmap_aug_b, fb, 0, (int)col0);
+                            if (b_hi)
+                                tma_load_2d<1>(sB + s * C::B_BYTES + AUG_B_HALF, &tmap_aug_b, fb,
+                                               0, (int)col0 + 128);
+                        } else {
+                            if (leader)
+                                mbar_expect_tx(fb, (a_hi ? 2 : 1) * AUG_A +
+                                                       (b_hi ? 2 : 1) * AUG_B_HALF);
+                            if (a_mine)
+                                tma_load_2d<2>(sA + s * A_BYTES, &tmap_aug_a, fb, 0, my_a);
+                            if (rank == 0 || b_hi)
+                                tma_load_2d<2>(sB + s * C::B_BYTES, &tmap_aug_b, fb, 0,
+                                               (int)(col0 + 128 * rank));
+                        }
+                    }
+                    }
+                    __syncwarp();
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (the leader CTA of a pair)
+        if (leader) {   // whole warp; one elected lane issues
+            const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
+            int s = 0;
+            uint32_t ph = 0;
+            int lt = 0;
+            for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
+                if (a.symmetric) {
+                    int rt, ct;
+                    tile_coords(sch, t, rt, ct);
+                    if (sym_skip(a, a.row_begin + (int64_t)rt * C::TILE_M,
+                                 a.col_begin + (int64_t)ct * BN, BN)) {
+                        --lt;
+                        continue;
+                    }
+                }
+                const int buf = lt & 1;
+                const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
+                mbar_wait(tempty_bar(buf), aph ^ 1u);
+                tc_fence_after();
+                const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
+                for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
+                    mbar_wait(full_bar(s), ph);
+                    tc_fence_after();
+                    if (elect_one()) {
+                    if (!no_mma) {
+                        if (kb < sch.nkb) {
+                            const uint64_t ad = sw128_desc(sA + s * A_BYTES);
+                            const uint64_t bd = sw128_desc(sB + s * C::B_BYTES);
+#pragma unroll
+                            for (int kk = 0; kk < BK / UK; kk++) {
+                                const uint64_t koff = (uint64_t)((kk * UK * 2) >> 4);
+                                mma_f16<CG>(dtm, ad + koff, bd + koff, (kb | kk) != 0 ? 1u : 0u);
+                            }
+                        } else {
+                            mma_tf32<CG>(dtm, sw32_desc(sA + s * A_BYTES),
+                                         sw32_desc(sB + s * C::B_BYTES));
+                        }
+                    }
+                    mma_commit<CG>(empty_bar(s));
+                    }
+                    __syncwarp();
+                    if (++s == STAGES) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+                if (elect_one()) mma_commit<CG>(tfull_bar(buf));
+                __syncwarp();
+            }
+        }
+        __syncwarp();
+    } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
+        // ---------------- hit warp
+        hit_warp_loop<NHIT>(a, bars + BAR_BYTES, warp - FIRST_EPI_WARP - NEPI, NEPI / NHIT, lane,
+                            (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+    } else {
+        // ---------------- epilogue
+        const int q = warp & 3;          // TMEM lane quarter this warp may access
+        const int h = (warp - FIRST_EPI_WARP) >> 2;   // column half of the accumulator
+        const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+        // staging: 16 KB for the epilogue warps (64 records per buffer with 8
+        // warps, 32 with 16); with hit warps the region holds their queues
+        constexpr int WST = WSTAGE * NUM_EPI_WARPS / NEPI;
+        StagedWriter<WST> wr;
+        if constexpr (NHIT == 0)
+            writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
+        int lt = 0;
+        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
+            int rt, ct;
+            tile_coords(sch, t, rt, ct);
+            const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M + 128 * rank;
+            const int64_t col0 = a.col_begin + (int64_t)ct * BN;
+            if (sym_skip(a, a.row_begin + (int64_t)rt * C::TILE_M, col0, BN)) {
+                --lt;
+                continue;
+            }
+            const int buf = lt & 1;
+            const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
+            if constexpr (DIAG) {
+                const int64_t i = row0 + q * 32 + lane;
+                // Gram-diagonal pre-pass (CG = 1, col0 = row0): lane i's own
+                // column i - row0 = 32 q + lane sits in chunk q of half 0.
+                mbar_wait(tfull_bar(buf), aph);
+                tc_fence_after();
+                uint32_t r0[32];
+                if (h == 0) {
+                    tmem_ld32(tmem_base + lane_base + (uint32_t)(buf * BN + q * 32), r0);
+                    tmem_ld_wait(r0);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty_bar(buf));
+                if (h == 0 && i < a.row_end) a.gram_diag[i] = __uint_as_float(pick32(r0, lane));
+                continue;
+            }
+            if constexpr (NHIT > 0)
+                epilogue_tile_hit<CG, BN, NEPI / 4, NHIT>(
+                    a, bars + BAR_BYTES, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, tmem_base,
+                    tempty_bar(buf), row0, col0, buf, aph, q, h, lane, leader, tfull_bar(buf));
+            else
+                epilogue_tile<CG, BN, NEPI / 4>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf,
+                                                aph, q, h, lane, leader, tfull_bar(buf));
+        }
+        if constexpr (NHIT > 0)
+            hit_end<NHIT>(bars + BAR_BYTES, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, lane);
+        else
+            writer_finish(wr, a);
+    }
+
+    tc_fence_before();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    if (warp == 0) {
+        if constexpr (CG == 1)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS)
+                         : "memory");
+        else
+            asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                         "r"(TMEM_COLS)
+                         : "memory");
+    }
+}
+
+// ---------------------------------------------------------------------------
+// B-multicast variant (large d).  At d = 960 the single-CTA kernel moves
+// 737 KB of A and B from L2 per 128 x 256 tile, and measurement says that
+// traffic, not the MMA, sets both the rate and the power: the TMA stream
+// alone (no MMA, no epilogue) runs at ~10 KB/clk chip-wide and takes 1452 ms
+// at the 1 kW cap against 1570 ms for the whole join (profiles/round1/
+// tune_c4_power_session2.txt).  Here two CTAs of a cluster take vertically
+// adjacent row tiles of the same column tile: each loads its own A and HALF
+// of the shared B tile, multicast into both CTAs' shared memory, so per SM
+// the bytes per tile drop by a third (491 KB).  Each CTA still issues its own
+// M = 128 MMAs (no cross-SM operand reads, unlike cta_group::2).  A stage is
+// refilled only after BOTH CTAs' MMAs released it (empty barrier count 2,
+// multicast commits).  Every load is issued even for a tile past the range
+// end (its rows/columns are masked in the epilogue; TMA zero-fills past
+// n_pad), so the byte counts are fixed.
+__device__ __forceinline__ void tma_load_2d_mc(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                               int c0, int c1, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "h"(mask)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster."
+        "b64 [%0], %1;" ::"r"(bar),
+        "h"(mask)
+        : "memory");
 }
 
 constexpr int MC_STAGES = 4;
@@ -2257,12 +2271,12 @@ static int env_int(const char* name, int dflt) {
     return v && *v ? atoi(v) : dflt;
 }
 
-template <int CG, bool DIAG = false, int NEPI = tc::NUM_EPI_WARPS>
+template <int CG, bool DIAG = false, int NEPI = tc::NUM_EPI_WARPS, int NHIT = 0>
 static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
                                   const CUtensorMap& mb, const JoinArgs& a, const tc::Sched& sch,
                                   cudaStream_t s) {
     using namespace tc;
-    auto kern = join_tc_kernel<CG, DIAG, NEPI>;
+    auto kern = join_tc_kernel<CG, DIAG, NEPI, NHIT>;
     static PerDeviceOnce attr_once;
     {
         cudaError_t e = attr_once.run([&] {
@@ -2277,7 +2291,7 @@ static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
     if (work <= 0) return cudaSuccess;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * CG));
-    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI) * 32);
+    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI + NHIT) * 32);
     cfg.dynamicSmemBytes = Cfg<CG>::SMEM_BYTES;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -2430,6 +2444,7 @@ static int tc_variant(int64_t d_pad, int64_t rows, int64_t cols, bool low_output
 // FASTED_JOIN_SPARSE hint; FASTED_RES_HIT / FASTED_MC_HIT = 0 or 2 override.
 static bool res_hit(bool sparse) { return env_int("FASTED_RES_HIT", sparse ? 2 : 0) == 2; }
 static bool mc_hit(bool sparse) { return env_int("FASTED_MC_HIT", sparse ? 2 : 0) == 2; }
+static bool stream_hit(bool sparse) { return env_int("FASTED_STREAM_HIT", sparse ? 2 : 0) == 2; }
 
 const char* join_tc_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, bool low_output,
                                 bool sparse) {
@@ -2443,7 +2458,10 @@ const char* join_tc_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, bool 
             if (env_int("FASTED_MC_EPI", 16) == 16 && mc_hit(sparse))
                 return "fasted::tc::join_tc_mc_kernel + 2 hit warps";
             return "fasted::tc::join_tc_mc_kernel";
-        default: return cg == 2 ? "fasted::tc::join_tc_kernel<2>" : "fasted::tc::join_tc_kernel<1>";
+        default:
+            if (cg == 2 && env_int("FASTED_STREAM_EPI", 16) == 16 && stream_hit(sparse))
+                return "fasted::tc::join_tc_kernel<2> + 2 hit warps";
+            return cg == 2 ? "fasted::tc::join_tc_kernel<2>" : "fasted::tc::join_tc_kernel<1>";
     }
 }
 
@@ -2664,7 +2682,8 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     // at S <= 64: 1917-1946 vs 2060-2253 ms (profiles/round1/tune_sepi_session2.txt)
     if (cg == 2)
         e = env_int("FASTED_STREAM_EPI", 16) == 8 ? launch_variant<2>(mx, ma, mb, a, sch, s)
-                                                  : launch_variant<2, false, 16>(mx, ma, mb, a, sch, s);
+            : stream_hit(a.sparse != 0) ? launch_variant<2, false, 16, 2>(mx, ma, mb, a, sch, s)
+                                                   : launch_variant<2, false, 16>(mx, ma, mb, a, sch, s);
     else
         e = launch_variant<1>(mx, ma, mb, a, sch, s);
     if (e == cudaSuccess) e = cudaGetLastError();

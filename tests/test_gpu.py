@@ -624,10 +624,11 @@ def test_cta_pair_low_output_form_matches_single_cta():
     hd = F.to_half(F.generate_synthetic(3000, 520, seed=77))
     one = _tc_variant(hd, 8.5, FASTED_CTA_GROUP=1)
     assert len(one[0]) > 3000
-    for sepi in (8, 16):
-        pair = _tc_variant(hd, 8.5, FASTED_CTA_GROUP=2, FASTED_STREAM_EPI=sepi)
+    for sepi, hit in ((8, 0), (16, 0), (16, 2)):
+        pair = _tc_variant(hd, 8.5, FASTED_CTA_GROUP=2, FASTED_STREAM_EPI=sepi,
+                           FASTED_STREAM_HIT=hit)
         for x, y in zip(one, pair):
-            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), sepi
+            assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (sepi, hit)
 
 
 def test_sort_long_rows_bucket_and_fallback_paths():

@@ -277,7 +277,8 @@ def test_kernel_selection_rule_is_host_side(monkeypatch):
     GPU: resident pair for d_pad <= 256, the CTA pair for large low-output
     joins, multicast clusters otherwise, the exact kernel for mode exact."""
     L = _lib.load()
-    for k in ("FASTED_RES_HIT", "FASTED_MC_HIT", "FASTED_RES_EPI", "FASTED_MC_EPI",
+    for k in ("FASTED_RES_HIT", "FASTED_MC_HIT", "FASTED_STREAM_HIT", "FASTED_STREAM_EPI",
+              "FASTED_RES_EPI", "FASTED_MC_EPI",
               "FASTED_CTA_GROUP", "FASTED_MC", "FASTED_RESIDENT"):
         monkeypatch.delenv(k, raising=False)
 
@@ -294,7 +295,8 @@ def test_kernel_selection_rule_is_host_side(monkeypatch):
     sp = _lib.JOIN_SPARSE
     assert name(128, big, big, sp) == "fasted::tc::join_tc_res_kernel<2> + 2 hit warps"
     assert name(960, big, big, sp) == "fasted::tc::join_tc_mc_kernel + 2 hit warps"
-    assert name(960, big, big, sp | _lib.JOIN_LOW_OUTPUT) == "fasted::tc::join_tc_kernel<2>"
+    assert name(960, big, big, sp | _lib.JOIN_LOW_OUTPUT) == \
+        "fasted::tc::join_tc_kernel<2> + 2 hit warps"
 
 
 def test_form_hints_thresholds():
