@@ -37,10 +37,17 @@ flags = _lib.JOIN_TC | engine.form_hints(ref, rows, (0, dd.n_dev))
 times = {k: [] for k in settings}
 
 
+extra = {}
+
+
 def apply(setting):
+    extra.clear()
     for kv in setting.split(","):
         k, v = kv.split("=")
-        os.environ[k] = v
+        if k == "F":          # extra fasted_join flag bits for this setting
+            extra["F"] = int(v)
+        else:
+            os.environ[k] = v
 
 
 for r in range(rounds + 1):
@@ -48,7 +55,8 @@ for r in range(rounds + 1):
         apply(st)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(s)
-        engine.join_raw(dd, es, flags, rows, (0, dd.n_dev), rec, cap, cnt, s.cuda_stream)
+        engine.join_raw(dd, es, flags | extra.get("F", 0), rows, (0, dd.n_dev), rec, cap, cnt,
+                        s.cuda_stream)
         e1.record(s)
         e1.synchronize()
         assert int(cnt[0]) == ref, (st, int(cnt[0]), ref)
