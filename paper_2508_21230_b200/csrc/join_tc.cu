@@ -26,7 +26,7 @@
 //   join_tc_mc_kernel    clusters of two single-CTA MMAs sharing B by TMA
 //                        multicast (d_pad > 256 otherwise).
 //   join_tc_res_kernel   CTA pair with the A panel resident in shared memory
-//                        for a row tile x column segment (d_pad <= 256).
+//                        for a row tile x column segment (d_pad <= 512).
 //
 // The distance matrix never reaches HBM.  Replaces the reference's tile
 // sweep (tiling.py:307-344): compute_block_tile (tiling.py:199-285),
@@ -1534,7 +1534,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
 }
 
 // ---------------------------------------------------------------------------
-// Resident-A variant (small d, d_pad <= 256).  At d = 128 one 256 x 256 tile
+// Resident-A variant (d_pad <= 512).  At d = 128 one 256 x 256 tile
 // is only 9 MMAs, and streaming both operands moves 144 KB per CTA pair per
 // tile from L2: measured, the TMA stream alone (no MMA, no epilogue) takes
 // 192 ms at 1M x 128, against a 121 ms tensor floor (profiles/round1/
@@ -2421,7 +2421,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
 // Which tcgen05 join kernel (and CTA group) a launch uses (env overrides:
 // FASTED_CTA_GROUP=1|2 forces the streaming kernel, FASTED_RESIDENT=0 and
 // FASTED_MC=0 disable the resident and multicast forms).
-//   d_pad <= 256                          resident-A CTA pair
+//   d_pad <= 512                          resident-A CTA pair
 //   d_pad >  256, large, low output       streaming CTA pair, 16K-row raster
 //   d_pad >  256 otherwise                B-multicast clusters
 // The CTA pair (cta_group::2) reaches ~91% tensor-pipe utilisation per
@@ -2435,8 +2435,14 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
 enum { TC_STREAMING = 0, TC_RESIDENT = 1, TC_MULTICAST = 2 };
 static int tc_variant(int64_t d_pad, int64_t rows, int64_t cols, bool low_output, int* cg) {
     const int cg_env = env_int("FASTED_CTA_GROUP", 0);
-    *cg = cg_env == 1 ? 1 : cg_env == 2 ? 2 : (d_pad <= 256 ? 2 : 1);
-    if (d_pad <= 256) return env_int("FASTED_RESIDENT", 1) != 0 ? TC_RESIDENT : TC_STREAMING;
+    // resident A up to d_pad 512 (one 132 KB A buffer + 4 B stages at 512);
+    // measured at 60K x 512: 2.52 vs 2.85 ms, 5M x 384 shard: 1616-1640 vs
+    // 2003-2122 ms for S <= 1000 (alternating launches) -- the streaming
+    // forms move A and B from L2 per tile (~64 B/clk/SM at d = 512, above
+    // what L2 delivers at 1.97 GHz), resident A only B
+    const int64_t res_max = env_int("FASTED_RES_MAXD", 512);
+    *cg = cg_env == 1 ? 1 : cg_env == 2 ? 2 : (d_pad <= res_max ? 2 : 1);
+    if (d_pad <= res_max) return env_int("FASTED_RESIDENT", 1) != 0 ? TC_RESIDENT : TC_STREAMING;
     if (cg_env != 0 || env_int("FASTED_MC", 1) == 0) return TC_STREAMING;
     if (low_output && (double)rows * (double)cols >= 68.7e9) {   // >= 2^36 pairs examined
         *cg = 2;
@@ -2528,7 +2534,7 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         return FASTED_ERR_ARGUMENT;
     }
     // Variant choice (profiles/round1/tune_*.txt, measured on B200):
-    //   d_pad <= 256: resident-A CTA pair (join_tc_res_kernel; 1M x 128:
+    //   d_pad <= 512: resident-A CTA pair (join_tc_res_kernel; 1M x 128:
     //                 1013 TFLOPS vs 693 for the streaming pair);
     //   d_pad >  256: B-multicast clusters of single-CTA MMAs
     //                 (join_tc_mc_kernel; 1M x 960: 1374 vs 1226 single-CTA
@@ -2616,7 +2622,7 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
             return cuda_status(e, "aug_prepare_kernel");
         }
     }
-    // Resident-A form for d_pad <= 256 (FASTED_RESIDENT=0 selects streaming),
+    // Resident-A form for d_pad <= 512 (FASTED_RESIDENT=0 selects streaming),
     // 256-column tiles, two accumulators.  (128-column tiles with four
     // accumulators measured slower, 372 vs 283 ms at 1M x 128 -- the N=128
     // MMAs re-read A every 64 cycles -- and were removed.)

@@ -344,9 +344,11 @@ def _tc_variant(hd, eps, rows=None, cols=None, **env):
 
 @pytest.mark.parametrize("n,d,eps,seg", [(3000, 128, 3.7, 64), (2999, 100, 3.3, 3),
                                          (1100, 16, 1.0, 1), (2048, 256, 5.6, 2),
-                                         (777, 200, 5.0, 64), (5000, 64, 2.6, 7)])
+                                         (777, 200, 5.0, 64), (5000, 64, 2.6, 7),
+                                         (2000, 512, 8.6, 5), (1500, 384, 7.7, 3),
+                                         (999, 300, 6.8, 2)])
 def test_resident_kernel_bit_identical_to_streaming(n, d, eps, seg):
-    """The resident-A kernel (d_pad <= 256) issues the streaming kernel's MMA
+    """The resident-A kernel (d_pad <= 512) issues the streaming kernel's MMA
     sequence per tile, so every record is bit-identical, for both CTA-group
     forms, ragged segments and ragged row/column ranges."""
     hd = F.to_half(F.generate_synthetic(n, d, seed=n + d))
@@ -402,17 +404,17 @@ def test_multicast_kernel_bit_identical_to_single_cta(n, d, eps):
     kernel's M=128 MMA sequence per tile: identical bits, including odd
     row-tile counts (a masked partner tile) and ragged shard ranges."""
     hd = F.to_half(F.generate_synthetic(n, d, seed=n * 7 + d))
-    ref = _tc_variant(hd, eps, FASTED_CTA_GROUP=1)
+    ref = _tc_variant(hd, eps, FASTED_CTA_GROUP=1, FASTED_RESIDENT=0)
     assert len(ref[0]) > n
     for mepi, hit in ((8, 0), (16, 0), (16, 2)):
         mc = _tc_variant(hd, eps, FASTED_MC=1, FASTED_CTA_GROUP=0, FASTED_MC_EPI=mepi,
-                         FASTED_MC_HIT=hit)
+                         FASTED_MC_HIT=hit, FASTED_RES_MAXD=256)
         for x, y in zip(ref, mc):
             assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), mepi
     n_dev = -(-hd.n_padded // 128) * 128
     rows, cols = (128, min(n_dev, 1152)), (256, n_dev)
-    ref = _tc_variant(hd, eps, rows, cols, FASTED_CTA_GROUP=1)
-    mc = _tc_variant(hd, eps, rows, cols, FASTED_MC=1, FASTED_CTA_GROUP=0)
+    ref = _tc_variant(hd, eps, rows, cols, FASTED_CTA_GROUP=1, FASTED_RESIDENT=0)
+    mc = _tc_variant(hd, eps, rows, cols, FASTED_MC=1, FASTED_CTA_GROUP=0, FASTED_RES_MAXD=256)
     for x, y in zip(ref, mc):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
 
@@ -617,11 +619,12 @@ def test_cta_pair_low_output_form_matches_single_cta():
     L = _lib.load()
     name = lambda d, r, c, f: L.fasted_join_kernel_name(d, r, c, f).decode()
     big = 1 << 19
-    assert "join_tc_kernel<2>" in name(512, big, big, _lib.JOIN_LOW_OUTPUT)
-    assert "mc" in name(512, big, big, 0)
-    assert "mc" in name(512, 60032, 60032, _lib.JOIN_LOW_OUTPUT)
+    assert "join_tc_kernel<2>" in name(960, big, big, _lib.JOIN_LOW_OUTPUT)
+    assert "mc" in name(960, big, big, 0)
+    assert "mc" in name(960, 60032, 60032, _lib.JOIN_LOW_OUTPUT)
     assert "res" in name(128, big, big, _lib.JOIN_LOW_OUTPUT)
-    hd = F.to_half(F.generate_synthetic(3000, 520, seed=77))
+    assert "res" in name(512, big, big, _lib.JOIN_LOW_OUTPUT)
+    hd = F.to_half(F.generate_synthetic(3000, 520, seed=77))    # d_pad 528: streaming forms
     one = _tc_variant(hd, 8.5, FASTED_CTA_GROUP=1)
     assert len(one[0]) > 3000
     for sepi, hit in ((8, 0), (16, 0), (16, 2)):

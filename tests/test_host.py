@@ -274,10 +274,11 @@ def test_plan_row_chunks():
 
 def test_kernel_selection_rule_is_host_side(monkeypatch):
     """fasted_join_kernel_name applies the launch's selection rule without a
-    GPU: resident pair for d_pad <= 256, the CTA pair for large low-output
+    GPU: resident pair for d_pad <= 512, the CTA pair for large low-output
     joins, multicast clusters otherwise, the exact kernel for mode exact."""
     L = _lib.load()
     for k in ("FASTED_RES_HIT", "FASTED_MC_HIT", "FASTED_STREAM_HIT", "FASTED_STREAM_EPI",
+              "FASTED_RES_MAXD",
               "FASTED_RES_EPI", "FASTED_MC_EPI",
               "FASTED_CTA_GROUP", "FASTED_MC", "FASTED_RESIDENT"):
         monkeypatch.delenv(k, raising=False)
@@ -289,7 +290,9 @@ def test_kernel_selection_rule_is_host_side(monkeypatch):
     assert name(128, big, big, 0) == "fasted::tc::join_tc_res_kernel<2>"
     assert name(960, big, big, _lib.JOIN_LOW_OUTPUT) == "fasted::tc::join_tc_kernel<2>"
     assert name(960, big, big, 0) == "fasted::tc::join_tc_mc_kernel"
-    assert name(512, 60032, 60032, _lib.JOIN_LOW_OUTPUT) == "fasted::tc::join_tc_mc_kernel"
+    assert name(960, 60032, 60032, _lib.JOIN_LOW_OUTPUT) == "fasted::tc::join_tc_mc_kernel"
+    assert name(512, 60032, 60032, _lib.JOIN_LOW_OUTPUT) == "fasted::tc::join_tc_res_kernel<2>"
+    assert name(528, big, big, 0) == "fasted::tc::join_tc_mc_kernel"
     assert name(960, big, big, _lib.JOIN_EXACT) == "fasted::join_exact_kernel"
     # FASTED_JOIN_SPARSE: hit warps in the resident and multicast forms
     sp = _lib.JOIN_SPARSE
