@@ -524,6 +524,7 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
         tj = [None, None]
         sort_ev = []
         join_ev = []
+        cnt_evs = []
 
         host_t0 = time.perf_counter()
         marks = []
@@ -555,9 +556,10 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
             aux.wait_event(e1)
             with torch.cuda.stream(aux):
                 cnt_h[b].copy_(cnt[b], non_blocking=True)
-            ev = torch.cuda.Event()
+            ev = torch.cuda.Event(enable_timing=True)
             ev.record(aux)
             cnt_ev[b] = ev
+            cnt_evs.append((c, ev))
             mark("launched%d" % c)
 
         launch_join(0)
@@ -567,7 +569,9 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
             b = c % 2
             e0, e1 = tj[b]
             tc0 = time.perf_counter()
+            mark("wait%d" % c)
             cnt_ev[b].synchronize()
+            mark("synced%d" % c)
             count, used = (int(v) for v in cnt_h[b].tolist())
             tr["wait_join"] += time.perf_counter() - tc0
             tc0 = time.perf_counter()
@@ -642,7 +646,8 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
                 [("join%d" % c, round(t0e.elapsed_time(a), 2), round(t0e.elapsed_time(b), 2))
                  for c, a, b in join_ev] +
                 [("sort%d" % c, round(t0e.elapsed_time(a), 2), round(t0e.elapsed_time(b), 2))
-                 for c, (a, b) in enumerate(sort_ev)])
+                 for c, (a, b) in enumerate(sort_ev)] +
+                [("count%d" % c, round(t0e.elapsed_time(e), 2)) for c, e in cnt_evs])
         with _memo_lock:
             _count_memo[key] = total
     return kernel_ms, sort_ms, reruns, len(chunks)
