@@ -38,10 +38,19 @@ times = {k: [] for k in settings}
 
 
 extra = {}
+# every env key any setting touches is reset to its starting value before
+# each setting applies its own (settings do not leak into each other)
+_keys = {kv.split("=")[0] for st in settings for kv in st.split(",") if not kv.startswith("F=")}
+_orig = {k: os.environ.get(k) for k in _keys}
 
 
 def apply(setting):
     extra.clear()
+    for k, v in _orig.items():
+        if v is None:
+            os.environ.pop(k, None)
+        else:
+            os.environ[k] = v
     for kv in setting.split(","):
         k, v = kv.split("=")
         if k == "F":          # extra fasted_join flag bits for this setting
@@ -59,7 +68,8 @@ for r in range(rounds + 1):
                         s.cuda_stream)
         e1.record(s)
         e1.synchronize()
-        assert int(cnt[0]) == ref, (st, int(cnt[0]), ref)
+        if extra.get("F", 0) < 256:   # diagnostic flags (>= 256) invalidate results
+            assert int(cnt[0]) == ref, (st, int(cnt[0]), ref)
         if r:   # round 0 warms up every setting
             times[st].append(e0.elapsed_time(e1))
 fl = 2.0 * min(nrows, n) * n * d
