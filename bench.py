@@ -330,7 +330,13 @@ def main():
         st = F.EngineStats()
         t0 = time.perf_counter()
         rs = F.self_join(hd_host, eps, stats_out=st, shard=(rank, world))
-        torch.cuda.synchronize()
+        # self_join returns host arrays after waiting for its own streams; the
+        # device-wide check polls (a blocking sync can return 10-1000 ms late
+        # here, see engine._poll)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        while not ev.query():
+            time.sleep(0.0002)
         dt = time.perf_counter() - t0
         if s > 0:
             phases.append({"h2d_s": st.stage_seconds, "join_kernels_s": st.kernel_wall_seconds,
