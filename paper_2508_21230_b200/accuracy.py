@@ -14,7 +14,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _lib
+from . import _lib, engine
 from .analysis import distance_error_stats, overlap_accuracy
 from .tiling import ResultSet
 
@@ -43,7 +43,7 @@ def fp64_truth_rows(values: np.ndarray, rows, epsilon: float, device: int = 0):
             _lib.check(L.fasted_fp64_rows(x.data_ptr(), n, d, q.data_ptr(), len(rows),
                                           float(epsilon), rec.data_ptr(), cap, cnt.data_ptr(),
                                           stream), "fasted_fp64_rows")
-            count = int(cnt.item())
+            count = engine.read_counts(cnt)[0]
             if count <= cap:
                 break
             cap = count

@@ -204,6 +204,19 @@ def _poll_stream(stream) -> None:
     _poll(ev)
 
 
+def read_counts(cnt, stream=None) -> list:
+    """Device int64 counters -> Python ints, ordered after `stream`'s work
+    (the current stream by default), waiting by polling (see _poll)."""
+    import torch
+
+    st = stream if stream is not None else torch.cuda.current_stream(cnt.device)
+    host = torch.empty(cnt.shape, dtype=cnt.dtype, pin_memory=True)
+    with torch.cuda.stream(st):
+        host.copy_(cnt, non_blocking=True)
+    _poll_stream(st)
+    return [int(v) for v in host.tolist()]
+
+
 # Last exact count per problem, so repeated joins size their buffers once.
 _count_memo: dict = {}
 _memo_lock = threading.Lock()
@@ -230,11 +243,11 @@ def _estimate_capacity(dd: DeviceData, eps_sq: float, rows, cols, flags: int, st
     if samples == 0:
         return 0
     cnt = torch.zeros(2, dtype=torch.int64, device=f"cuda:{dd.device}")
-    tot = 0
-    for s in range(samples):
+    for s in range(samples):   # the sample blocks append into one count: one readback
         b = r0 + (nblk * s // samples) * BLOCK
-        join_raw(dd, eps_sq, flags | _lib.JOIN_COUNT, (b, b + BLOCK), cols, None, 0, cnt, stream)
-        tot += int(cnt[0].item())
+        join_raw(dd, eps_sq, flags | _lib.JOIN_COUNT | (_lib.JOIN_APPEND if s else 0),
+                 (b, b + BLOCK), cols, None, 0, cnt, stream)
+    tot = read_counts(cnt)[0]
     return int(tot * nblk / samples * 1.25) + 65536
 
 
@@ -316,7 +329,7 @@ def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool
             e0.record(stream)
             join_raw(dd, eps_sq, flags, rows, cols, rec, cap, cnt, sp)
             e1.record(stream)
-            count, chunks = (int(v) for v in cnt.tolist())
+            count, chunks = read_counts(cnt, stream)
             slots = chunks * RECORD_CHUNK
             kernel_ms += e0.elapsed_time(e1)
             if slots <= cap:
