@@ -9,7 +9,8 @@ import sys, os, numpy as np
 sys.path.insert(0, os.getcwd())
 import paper_2508_21230_b200 as F
 from paper_2508_21230_b200 import engine
-for n, d, eps in ((2000, 200, 5.4), (1500, 520, 8.6), (3000, 64, 2.6)):
+for n, d, eps in ((2000, 200, 5.4), (1500, 520, 8.6), (3000, 64, 2.6), (1500, 384, 7.7),
+                  (1000, 512, 8.6)):
     hd = F.to_half(F.generate_synthetic(n, d, seed=n))
     a = F.self_join(hd, eps); b = F.self_join(hd, eps, symmetric=True)
     c = F.self_join(hd, eps, mode="exact")
