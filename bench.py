@@ -9,16 +9,25 @@ far larger than the 126 MB L2, so no flush is needed between steps).
 `value` = whole-job distance TFLOPS, 2 n^2 d / (max over ranks of the
 per-step device time).  `e2e` is the same metric through the public API
 (paper_2508_21230_b200.self_join on a pinned host HalfDataset: H2D of the
-FP16 matrix + norms, join, device sort, D2H of the sorted pair list).
+FP16 matrix + norms, join, device sort, D2H of the sorted pair list), with
+every phase timed on the device.
+
+On one GPU the same run also measures the other north-star configs
+(`configs`: C2 and C3 in full, and rank 0's shard of the 8-GPU C5 job over
+its selectivity sweep), each with its roofline, clocks, sort time and a band
+check of sampled row blocks against the CPU oracle (the checker, outside
+every timed region).
 
 --impl reference times the reference's CPU path (the C oracle restatement
 of mpjoin's RZ join, oracle/fasted_oracle.c, all host threads) on a bounded
-sample of the same workload.
+sample of the same workload, plus one full unextrapolated C1 join as an
+anchor (checked against the reference's C1 digest).
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -26,6 +35,7 @@ import subprocess
 import sys
 import threading
 import time
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -42,16 +52,25 @@ WORKLOADS = {
     "C4": ("GIST-shaped synthetic 1M x 960, S~64", 1000000, 960, 11.700486640655093),
     "C5": ("Tiny-shaped synthetic 5M x 384, S~1024", 5000000, 384, 7.1352369182727085),
 }
+# C5 sweep (reference CLI calibrate, sample 4096)
+C5_SWEEP = [("S0 (eps 0: self pairs only)", 0.0), ("S16", 6.896041752764515),
+            ("S1024", 7.1352369182727085), ("S4096", 7.2300123612099165)]
 SEED = 12345
+C1_PAIRS = 1199444
+C1_SHA256 = None   # read from tests/golden/reference_meta.json when present
+LONG_LAUNCH_MS = 100.0   # launches longer than this are rated against the sustained peak
+SM_COUNT = 148
+FLOP_PER_CLK_SM = 8192   # dense FP16 tcgen05 rate per SM per clock
 
 
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", 0) or 0), "measured"
+        return (float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", 0) or 0),
+                float(p.get("hbm_gbs", 0) or 6540.5), "measured")
     except Exception:
-        return 1590.0, 1400.0, "fallback (B200_PROFILING.md)"
+        return 1590.0, 1400.0, 6540.5, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -118,10 +137,22 @@ def dist_env():
     return rank, world, local
 
 
+def config_of(wl: str) -> dict:
+    """The `config` object both arms print (identical dicts)."""
+    name, n, d, eps = WORKLOADS[wl]
+    n_pad, d_pad = -(-n // 128) * 128, -(-d // 16) * 16
+    return {"workload": f"{wl}: {name}", "n": n, "d": d, "epsilon": eps, "seed": SEED,
+            "fp16_dataset_bytes": n_pad * d_pad * 2,
+            "l2": "inputs %.2f GB >> 126 MB L2; no flush" % (n_pad * d_pad * 2 / 1e9)}
+
+
+# ── CPU side (the reference arm and cpu_baseline) ───────────────────────
+
+
 def cpu_sample(n, d, eps, seconds_target=12.0, threads=None):
-    """Oracle (reference restatement) TFLOPS on a bounded sample: one
-    128-row block of the workload against a column range sized so the run
-    takes ~seconds_target.  Returns (tflops, sample description, threads)."""
+    """Oracle (reference restatement) TFLOPS on a bounded sample: a few
+    128-row blocks of the workload against a column range sized so the run
+    takes ~seconds_target.  Returns (tflops, description, threads, seconds)."""
     from oracle import oracle as O
     from paper_2508_21230_b200.dataset import synthetic_rows
 
@@ -149,7 +180,33 @@ def cpu_sample(n, d, eps, seconds_target=12.0, threads=None):
            count_only=True)
     dt = time.perf_counter() - t0
     tflops = 2.0 * rows * cols_eff * d / dt / 1e12
-    return tflops, f"rows 0..{rows} x cols 0..{cols_eff} of {n}x{d} ({dt:.1f} s)", threads
+    return (tflops, f"rows 0..{rows} x cols 0..{cols_eff} of {n}x{d} ({dt:.1f} s)", threads, dt)
+
+
+def c1_anchor(threads):
+    """One FULL C1 self-join (16384 x 128) on the CPU oracle, unextrapolated:
+    seconds, TFLOPS, pair count and whether the pairs-file digest equals the
+    reference's own (tests/golden/reference_meta.json)."""
+    from oracle import oracle as O
+    from paper_2508_21230_b200.dataset import generate_synthetic
+
+    _, n, d, eps = WORKLOADS["C1"]
+    x = generate_synthetic(n, d, seed=SEED).values
+    v16, norms, _ = O.to_half(x)
+    t0 = time.perf_counter()
+    oi, oj, od = O.join(v16, norms, n, eps, threads=threads, capacity=2 * C1_PAIRS)
+    dt = time.perf_counter() - t0
+    out = {"workload": "C1 16384 x 128, eps 3.973260466174982, full join (no extrapolation)",
+           "seconds": dt, "tflops": 2.0 * n * n * d / dt / 1e12, "pairs": int(len(oi)),
+           "cores": threads, "reference_probe": "60.5 s on 8 cores (mpjoin numba, BASELINE.md)"}
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "reference_meta.json")) as f:
+            want = json.load(f)["C1"]["result_sha256"]
+        got = hashlib.sha256(O.pairs_payload(oi, oj, od)).hexdigest()
+        out["digest_equals_reference"] = got == want
+    except Exception as exc:
+        out["digest_equals_reference"] = f"unchecked: {exc}"
+    return out
 
 
 def run_reference(args):
@@ -158,28 +215,288 @@ def run_reference(args):
         return 0
     name, n, d, eps = WORKLOADS[args.workload]
     threads = len(os.sched_getaffinity(0))
-    vals = []
+    vals, secs = [], []
     desc = ""
     for s in range(args.warmup + args.steps):
-        tf, desc, threads = cpu_sample(n, d, eps, seconds_target=args.ref_seconds, threads=threads)
+        tf, desc, threads, dt = cpu_sample(n, d, eps, seconds_target=args.ref_seconds,
+                                           threads=threads)
         if s >= args.warmup:
             vals.append(tf)
+            secs.append(dt)
     v = statistics.mean(vals)
+    anchor = c1_anchor(threads)
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOPS",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        # the full workload on the CPU, extrapolated from the sampled rate
-        "ms_per_step": 2.0 * n * n * d / (v * 1e12) * 1e3, "higher_is_better": True,
-        "scaling": "strong",
+        # each step is a bounded sample of the workload (measured time); the
+        # full workload's CPU time is extrapolated from the sampled rate
+        "ms_per_step": statistics.mean(secs) * 1e3,
+        "extrapolated": True,
+        "full_workload_ms_extrapolated": 2.0 * n * n * d / (v * 1e12) * 1e3,
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "fp16 in / fp32 RZ accumulate", "data": "synthetic",
-        "config": {"workload": f"{args.workload}: {name}", "n": n, "d": d, "epsilon": eps,
-                   "seed": SEED},
+        "config": config_of(args.workload),
         "cpu_baseline": {"value": v, "unit": "TFLOPS", "cores": threads, "kind": "port",
-                         "sample": desc},
+                         "sample": desc, "sample_seconds_per_step": secs,
+                         "anchor_c1_full": anchor},
         "e2e": {"value": v, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ── GPU helpers ─────────────────────────────────────────────────────────
+
+
+def timed_launches(stream, fn, reps):
+    """Per-launch CUDA-event times (ms) of `reps` back-to-back calls."""
+    import torch
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
+    ev[0].record(stream)
+    for r in range(reps):
+        fn()
+        ev[r + 1].record(stream)
+    ev[-1].synchronize()
+    return [ev[r].elapsed_time(ev[r + 1]) for r in range(reps)]
+
+
+def tensor_roofline(flops, launch_ms, clocks, peaks):
+    peak_burst, peak_sus, _, src = peaks
+    long = launch_ms > LONG_LAUNCH_MS and peak_sus
+    peak = peak_sus if long else peak_burst
+    achieved = flops / (launch_ms / 1e3) / 1e12
+    out = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+           "frac": achieved / peak,
+           "peak_source": f"{src} " + ("bf16_tflops_sustained (launch > 100 ms)" if long
+                                       else "bf16_tflops burst (launch <= 100 ms)")}
+    mhz = clocks.get("sm_mhz") if clocks else None
+    if mhz:
+        at_clock = FLOP_PER_CLK_SM * SM_COUNT * mhz * 1e6 / 1e12
+        out["frac_of_tensor_rate_at_median_clock"] = achieved / at_clock
+    return out
+
+
+def device_synthetic(n, d, seed, device, chunk_rows=131072):
+    """generate_synthetic(n, d, seed) quantised straight into HBM: host
+    generation of row chunks in parallel (bit-identical PCG64 streams,
+    dataset.synthetic_rows), each chunk copied up and cast by the GPU
+    quantise kernel (fasted_quantize) -- the 7.7 GB FP32 C5 matrix never
+    exists in full on the host.  Returns engine.DeviceData."""
+    import torch
+
+    from paper_2508_21230_b200 import _lib, engine
+    from paper_2508_21230_b200.dataset import synthetic_rows
+
+    n_pad, d_pad = -(-n // 128) * 128, -(-d // 16) * 16
+    dev = f"cuda:{device}"
+    values = torch.zeros((n_pad, d_pad), dtype=torch.float16, device=dev)
+    norms = torch.zeros(n_pad, dtype=torch.float32, device=dev)
+    L = _lib.load()
+    bounds = list(range(0, n, chunk_rows)) + [n]
+    stream = torch.cuda.current_stream()
+
+    def gen(k):
+        return synthetic_rows(n, d, seed, bounds[k], bounds[k + 1])
+
+    with ThreadPoolExecutor(max_workers=min(16, len(os.sched_getaffinity(0)))) as ex:
+        for k, x in enumerate(ex.map(gen, range(len(bounds) - 1))):
+            r0, r1 = bounds[k], bounds[k + 1]
+            xd = torch.from_numpy(x).to(dev)
+            rows_out = (n_pad - r0) if k == len(bounds) - 2 else (r1 - r0)
+            first = ctypes_i64()
+            _lib.check(L.fasted_quantize(xd.data_ptr(), r1 - r0, d,
+                                         values.data_ptr() + r0 * d_pad * 2, rows_out, d_pad,
+                                         norms.data_ptr() + r0 * 4, first, stream.cuda_stream),
+                       "fasted_quantize")
+            del xd
+    return engine.DeviceData(device, values, norms, n, n_pad, d_pad)
+
+
+def ctypes_i64():
+    import ctypes
+
+    return ctypes.byref(ctypes.c_int64(0))
+
+
+def band_check(oracle_rows, dd_host, es, tc_rows_fn, band=1e-3):
+    """Band contract on sampled row blocks: the TC pairs of each block vs
+    the reference's (oracle) pairs at eps_sq `es`."""
+    import paper_2508_21230_b200 as F
+    from oracle import oracle as O
+
+    v16, norms = dd_host
+    tot = None
+    for (r0, r1), (oi, oj, od) in oracle_rows.items():
+        keep = od <= np.float32(es)
+        ri, rj, rd = oi[keep], oj[keep], od[keep]
+        ti, tj, td = tc_rows_fn((r0, r1))
+        rep = F.band_compare(ti, tj, td, ri, rj, rd, es,
+                             lambda i, j: O.pair_d2(v16, norms, i, j), band=band)
+        d = rep.__dict__.copy()
+        if tot is None:
+            tot = d
+        else:
+            for k, v in d.items():
+                tot[k] = max(tot[k], v) if k == "max_rel_dd2_matched" else tot[k] + v
+    tot["ok"] = tot["missing_out_of_band"] == 0 and tot["extra_out_of_band"] == 0
+    tot["row_blocks"] = [f"{r0}..{r1}" for r0, r1 in oracle_rows]
+    return tot
+
+
+def oracle_row_blocks(v16, norms, n, eps_max, blocks, threads):
+    """Reference pairs of whole 128-row blocks (all columns) at eps_max --
+    filtering by dist_sq gives the reference result at any smaller eps."""
+    from oracle import oracle as O
+
+    out = {}
+    for rb in blocks:
+        r = (rb * 128, min(rb * 128 + 128, v16.shape[0]))
+        cap = 128 * 200000
+        oi, oj, od = O.join(v16, norms, n, eps_max, rows=r, threads=threads, capacity=cap)
+        if len(oi) >= cap:
+            oi, oj, od = O.join(v16, norms, n, eps_max, rows=r, threads=threads)
+        out[r] = (oi, oj, od)
+    return out
+
+
+def measure_workload(dd, n, d, eps, rows, peaks, device, reps, warmup, host_copy=None,
+                     oracle_rows=None, label=None):
+    """One config's device-timed join over rows x all columns: TFLOPS,
+    roofline, clocks, pairs/s, output-write bound, sort, band check."""
+    import torch
+
+    from paper_2508_21230_b200 import _lib, engine
+    from paper_2508_21230_b200.tiling import _eps_sq
+
+    L = _lib.load()
+    stream = torch.cuda.current_stream()
+    sp = stream.cuda_stream
+    es = float(_eps_sq(eps))
+    cols = (0, dd.n_dev)
+    cnt = torch.zeros(2, dtype=torch.int64, device=f"cuda:{device}")
+    engine.join_raw(dd, es, _lib.JOIN_COUNT, rows, cols, None, 0, cnt, sp)
+    pairs = int(cnt[0].item())
+    cap = pairs + engine.max_holes(device)
+    flags = _lib.JOIN_TC | engine.form_hints(pairs, rows, cols)
+    rec = torch.empty((cap, 4), dtype=torch.int32, device=f"cuda:{device}")
+
+    def step():
+        engine.join_raw(dd, es, flags, rows, cols, rec, cap, cnt, sp)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    with ClockSampler(device) as clk:
+        ms = timed_launches(stream, step, reps)
+    clocks = clk.summary()
+    got, used = (int(v) for v in cnt.tolist())
+    assert got == pairs, (got, pairs)
+    slots = used * engine.RECORD_CHUNK
+    t = timed_launches(stream, lambda: engine._sort_records(dd, rec, slots, pairs, rows, stream,
+                                                           timed=False), 1)
+    del rec
+    torch.cuda.empty_cache()
+    nrows = max(0, min(rows[1], n) - min(rows[0], n))
+    flops = 2.0 * nrows * n * d
+    best, med = min(ms), statistics.median(ms)
+    _, _, hbm, _ = peaks
+    rec_bytes = slots * engine.RECORD_BYTES
+    out = {
+        "workload": label, "epsilon": eps, "eps_sq": es,
+        "rows": f"{rows[0]}..{rows[1]} ({nrows} points) x all {n} columns",
+        "pairs": pairs, "selectivity": (pairs - nrows) / max(nrows, 1),
+        "launch_ms": ms, "tflops_median": flops / med / 1e9, "tflops_best": flops / best / 1e9,
+        "roofline": tensor_roofline(flops, med, clocks, peaks),
+        "clocks": clocks,
+        "pairs_per_s": pairs / (med / 1e3),
+        "record_bytes": rec_bytes,
+        "output_write_bound_ms": rec_bytes / (hbm * 1e9) * 1e3,
+        "sort_ms": t[0], "sort_GBps_records": rec_bytes / (t[0] / 1e3) / 1e9 if t[0] else None,
+        "kernel": L.fasted_join_kernel_name(dd.d_pad, rows[1] - rows[0], dd.n_dev,
+                                            flags).decode(),
+    }
+    if oracle_rows is not None:
+        def tc_rows(r):
+            return engine.to_host(engine.join_device(dd, es, rows=r))
+        out["band_check_vs_oracle"] = band_check(oracle_rows, host_copy, es, tc_rows)
+    return out
+
+
+def run_configs(args, device, peaks, threads):
+    """C2, C3 (full) and rank 0 of the 8-GPU C5 job over its sweep."""
+    import torch
+
+    import paper_2508_21230_b200 as F
+    from paper_2508_21230_b200 import engine
+
+    out = {}
+    for wl, reps, blocks in (("C2", 10, (0, 233, 468)), ("C3", 3, (0, 5000, 7812))):
+        t0 = time.perf_counter()
+        name, n, d, eps = WORKLOADS[wl]
+        hd = F.to_half(F.generate_synthetic(n, d, seed=SEED))
+        dd = engine.upload(hd, device)
+        orc = oracle_row_blocks(hd.values, hd.norms, n, eps, blocks, threads)
+        out[wl] = measure_workload(dd, n, d, eps, (0, dd.n_dev), peaks, device, reps, 2,
+                                   (hd.values, hd.norms), orc, f"{wl}: {name}")
+        out[wl]["wall_s"] = time.perf_counter() - t0
+        del dd, hd
+        torch.cuda.empty_cache()
+    # C5: one rank's share of the 8-GPU job (the path has no exchange step,
+    # so the job time is the max over ranks of this)
+    t0 = time.perf_counter()
+    _, n, d, _ = WORKLOADS["C5"]
+    dd = device_synthetic(n, d, SEED, device)
+    rows = engine.partition_rows(dd.n_dev, 8)[0]
+    host = (dd.values.cpu().numpy(), dd.norms.cpu().numpy())
+    blocks = (rows[0] // 128 + 17, (rows[0] + rows[1]) // 256 + 3)
+    orc = oracle_row_blocks(host[0], host[1], n, C5_SWEEP[-1][1], blocks, threads)
+    sweep = []
+    for label, eps in C5_SWEEP:
+        r = measure_workload(dd, n, d, eps, rows, peaks, device, 2, 1, host, orc,
+                             f"C5 {n}x{d} {label}, rank 0 of 8")
+        r["eight_gpu_job_tflops_if_balanced"] = 8 * r["tflops_median"]
+        sweep.append(r)
+    out["C5_rank0_of_8"] = {"sweep": sweep, "wall_s": time.perf_counter() - t0,
+                            "data": "generate_synthetic(5M, 384, seed 12345) bit-identical rows, "
+                                    "quantised chunk-wise on the GPU"}
+    del dd
+    torch.cuda.empty_cache()
+    return out
+
+
+def quantize_roofline(ds_values, device, peaks):
+    """to_half's quantise kernel (FP32 -> FP16 + RZ norms) on a resident
+    FP32 matrix: algorithmic bytes 4d + 2 d_pad + 4 per point."""
+    import torch
+
+    from paper_2508_21230_b200 import _lib
+
+    n, d = ds_values.shape
+    n_pad, d_pad = -(-n // 128) * 128, -(-d // 16) * 16
+    dev = f"cuda:{device}"
+    x = torch.from_numpy(ds_values).to(dev)
+    v = torch.empty((n_pad, d_pad), dtype=torch.float16, device=dev)
+    s = torch.empty(n_pad, dtype=torch.float32, device=dev)
+    L = _lib.load()
+    stream = torch.cuda.current_stream()
+
+    def q():
+        _lib.check(L.fasted_quantize(x.data_ptr(), n, d, v.data_ptr(), n_pad, d_pad,
+                                     s.data_ptr(), ctypes_i64(), stream.cuda_stream),
+                   "fasted_quantize")
+
+    q()
+    ms = timed_launches(stream, q, 5)
+    med = statistics.median(ms)
+    by = n * 4 * d + n_pad * 2 * d_pad + n_pad * 4
+    _, _, hbm, _ = peaks
+    del x, v, s
+    torch.cuda.empty_cache()
+    return {"bound": "hbm", "kernel": "fasted::quantize_kernel", "launch_ms": ms,
+            "algorithmic_bytes": by, "achieved": by / (med / 1e3) / 1e9, "peak": hbm,
+            "unit": "GB/s", "frac": by / (med / 1e3) / 1e9 / hbm,
+            "note": "launch time includes the host read of the overflow flag (one sync)"}
 
 
 def main():
@@ -194,6 +511,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-accuracy", action="store_true")
     ap.add_argument("--no-symmetric", action="store_true")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the C2/C3/C5 measurements (one-GPU runs only)")
     ap.add_argument("--accuracy-blocks", type=int, default=8)
     args = ap.parse_args()
     if args.impl == "reference":
@@ -201,7 +520,8 @@ def main():
 
     import torch
     import paper_2508_21230_b200 as F
-    from paper_2508_21230_b200 import _lib, engine
+    from paper_2508_21230_b200 import _lib, dist as D, engine
+    from paper_2508_21230_b200.tiling import _eps_sq
 
     rank, world, local = dist_env()
     if world > 1:
@@ -212,16 +532,20 @@ def main():
     device = torch.cuda.current_device()
     _lib.require_device(device)
     name, n, d, eps = WORKLOADS[args.workload]
+    peaks = load_peaks()
+    peak_burst, peak_sus, hbm, peak_src = peaks
+    threads = len(os.sched_getaffinity(0))
 
     # ---- data: every rank holds the full FP16 dataset
     ds = F.generate_synthetic(n, d, seed=SEED)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
     hd = F.to_half(ds, pin_host=True)          # GPU quantise; device copy cached
-    if rank != 0 or args.no_accuracy:
-        del ds
+    to_half_s = time.perf_counter() - t0
     n_dev = -(-hd.n_padded // 128) * 128
-    rows = engine.partition_rows(n_dev, world)[rank]
+    rows = D.shard_rows(hd.n_padded, rank, world)
     dd = engine.upload(hd, device)
-    eps_sq = float(np.float32(np.float32(eps) * np.float32(eps)))
+    eps_sq = float(_eps_sq(eps))
     stream = torch.cuda.current_stream()
     # size the record buffer once (exact count + per-warp chunk slack)
     first = engine.join_device(dd, eps_sq, rows=rows, sort=False)
@@ -229,34 +553,30 @@ def main():
     del first
     rec = torch.empty((max(cap, 1), 4), dtype=torch.int32, device=f"cuda:{device}")
     cnt = torch.zeros(2, dtype=torch.int64, device=f"cuda:{device}")
-
-    nrows = max(rows[1] - rows[0], 1)
     # the product path's kernel-form hint (engine.stream_join sets it the same way)
-    jflags = _lib.JOIN_TC | engine.form_hints(cap - engine.hole_slack(device), rows, (0, dd.n_dev))
+    jflags = _lib.JOIN_TC | engine.form_hints(cap - engine.hole_slack(device), rows,
+                                              (0, dd.n_dev))
 
     def step():
         engine.join_raw(dd, eps_sq, jflags, rows, (0, dd.n_dev), rec, cap, cnt,
                         stream.cuda_stream)
 
-    def barrier():
-        if world > 1:
-            torch.distributed.barrier()
-        torch.cuda.synchronize()
-
     for _ in range(args.warmup):
         step()
-    barrier()
+    D.barrier()
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     with ClockSampler(device) as clk:
-        barrier()
+        D.barrier()
         ev[0].record(stream)
         for s in range(args.steps):
             step()
             ev[s + 1].record(stream)
         torch.cuda.synchronize()
-        barrier()
+        D.barrier()
     per_step = [ev[s].elapsed_time(ev[s + 1]) for s in range(args.steps)]
     ms_local = ev[0].elapsed_time(ev[-1]) / args.steps
+    pairs_local = int(cnt[0].item())      # the timed full join's count
+    slots_local = int(cnt[1].item()) * engine.RECORD_CHUNK
     # opt-in symmetric schedule (upper tiles + mirrored records; world == 1):
     # same record set, half the MMA work -- reported beside the headline,
     # which stays the full n^2 computation of the reference and the paper
@@ -266,47 +586,28 @@ def main():
             engine.join_raw(dd, eps_sq, jflags | _lib.JOIN_SYMMETRIC, rows,
                             (0, dd.n_dev), rec, cap, cnt, stream.cuda_stream)
         sym_step()
-        barrier()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        for _ in range(max(1, args.steps // 2)):
-            sym_step()
-        s1.record(stream)
-        torch.cuda.synchronize()
-        sym_ms = s0.elapsed_time(s1) / max(1, args.steps // 2)
-        sym_pairs = int(cnt[0].item())
-        sym = {"ms_per_step": sym_ms, "pairs": sym_pairs,
+        D.barrier()
+        sms = timed_launches(stream, sym_step, max(1, args.steps // 2))
+        sym_ms = statistics.mean(sms)
+        sym = {"ms_per_step": sym_ms, "pairs": int(cnt[0].item()),
                "time_to_solution_speedup": (ms_local / sym_ms),
                # 256 x 256 tiles on or above the diagonal (both kernel forms tile so)
                "executed_tflops": (lambda R: R * (R + 1) / 2 * 2.0 * 256 * 256 * d)(
                    -(-dd.n_dev // 256)) / (sym_ms / 1e3) / 1e12,
                "note": "self_join(..., symmetric=True): tiles on/above the diagonal only, "
                        "mirrored records; the headline value is the full n^2 computation"}
-    pairs_local = int(cnt[0].item())
-    ms = ms_local
-    pairs = pairs_local
-    if world > 1:
-        t = torch.tensor([ms_local], dtype=torch.float64, device=f"cuda:{device}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms = float(t.item())
-        c = torch.tensor([pairs_local], dtype=torch.int64, device=f"cuda:{device}")
-        torch.distributed.all_reduce(c)   # counts summed (bookkeeping, not data path)
-        pairs = int(c.item())
+    ms = D.reduce_max(ms_local)
+    pairs = D.reduce_sum(pairs_local)
     flops = 2.0 * n * n * d
     value = flops / (ms / 1e3) / 1e12
-    peak_burst, peak_sus, peak_src = load_peaks()
-    # A join launch at C4 runs ~1.4 s back to back under the 1 kW cap: the
-    # "kernel inside a long step" case, whose denominator is the sustained
-    # cuBLAS figure (B200_PROFILING.md); the burst fraction is kept beside it.
-    peak = peak_sus if peak_sus else peak_burst
-    peak_kind = "bf16_tflops_sustained" if peak_sus else "bf16_tflops (burst)"
+    clocks = clk.summary()
     kernel_name = _lib.load().fasted_join_kernel_name(dd.d_pad, rows[1] - rows[0], dd.n_dev,
                                                       jflags).decode()
     # roofline of the dominant kernel (the join): algorithmic flops per launch
     rows_logical = max(0, min(rows[1], n) - min(rows[0], n))
     flops_launch = 2.0 * rows_logical * n * d
     avg_launch_ms = statistics.mean(per_step)
-    achieved = flops_launch / (avg_launch_ms / 1e3) / 1e12
+    roof = tensor_roofline(flops_launch, avg_launch_ms, clocks, peaks)
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
@@ -314,6 +615,12 @@ def main():
         traffic = prof.get(args.workload, {}).get("dram_bytes_per_launch")
     except Exception:
         pass
+    roof.update({"traffic": traffic, "frac_of_burst": roof["achieved"] / peak_burst,
+                 "frac_of_sustained": (roof["achieved"] / peak_sus if peak_sus else None),
+                 "kernel": kernel_name,
+                 "launch_includes": "Gram-diagonal pre-pass + augment-row prep "
+                                    "(~1/7800 of the join) + the join",
+                 "output_write_bound_ms": slots_local * engine.RECORD_BYTES / (hbm * 1e9) * 1e3})
     del rec
     torch.cuda.empty_cache()
 
@@ -326,26 +633,27 @@ def main():
     phases = []
     d2h = 0
     for s in range(args.e2e_steps + 1):
-        barrier()
+        D.barrier()
         st = F.EngineStats()
         t0 = time.perf_counter()
         rs = F.self_join(hd_host, eps, stats_out=st, shard=(rank, world))
         # self_join returns host arrays after waiting for its own streams; the
         # device-wide check polls (a blocking sync can return 10-1000 ms late
         # here, see engine._poll)
-        ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream())
-        while not ev.query():
+        evd = torch.cuda.Event()
+        evd.record(torch.cuda.current_stream())
+        while not evd.query():
             time.sleep(0.0002)
         dt = time.perf_counter() - t0
         if s > 0:
-            phases.append({"h2d_s": st.stage_seconds, "join_kernels_s": st.kernel_wall_seconds,
-                           "sort_d2h_not_hidden_s": st.merge_seconds, "wall_s": dt,
-                           "engine": st.per_device})
-        if world > 1:
-            t = torch.tensor([dt], dtype=torch.float64, device=f"cuda:{device}")
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            dt = float(t.item())
+            dev0 = st.per_device[0]
+            phases.append({"h2d_device_s": st.stage_seconds,
+                           "join_kernels_s": st.kernel_wall_seconds,
+                           "sort_device_s": dev0["sort_ms"] / 1e3,
+                           "d2h_device_s": dev0["d2h_ms"] / 1e3,
+                           "not_hidden_behind_join_s": st.merge_seconds, "wall_s": dt,
+                           "chunks": dev0["chunks"], "reruns": dev0["reruns"]})
+        dt = D.reduce_max(dt)
         if s > 0:          # first call warms the pinned-host caching allocator
             e2e_times.append(dt)
         d2h = len(rs) * 12
@@ -356,6 +664,7 @@ def main():
     # ---- pair accuracy vs FP64 (Eq. 3) on sampled whole row blocks: the
     # tcgen05 path and the reference arithmetic (exact kernel) side by side
     acc = None
+    quant = None
     if rank == 0 and not args.no_accuracy:
         from paper_2508_21230_b200 import accuracy
 
@@ -366,55 +675,61 @@ def main():
         for label, exact in (("tcgen05", False), ("reference_arithmetic_exact_kernel", True)):
             part = accuracy.join_row_blocks(dd_a, eps, arows, exact=exact)
             acc[label] = accuracy.accuracy_vs_fp64(ds.values, part, eps, arows, device)
-        del dd_a, ds
+        del dd_a
         torch.cuda.empty_cache()
+    if rank == 0:
+        quant = quantize_roofline(ds.values, device, peaks)
+        quant["to_half_wall_s"] = to_half_s
+        quant["to_half_note"] = ("to_half(ds, pin_host=True) end to end: H2D of the FP32 matrix, "
+                                 "the quantise kernel, D2H of the FP16 copy into pinned memory")
+    del ds
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:
         try:
-            tf, desc, threads = cpu_sample(n, d, eps, seconds_target=args.ref_seconds)
-            cpu = {"value": tf, "unit": "TFLOPS", "cores": threads, "kind": "port",
-                   "sample": desc + "; oracle/fasted_oracle.c (RZ join restated from mpjoin)"}
+            tf, desc, thr, dt = cpu_sample(n, d, eps, seconds_target=args.ref_seconds)
+            cpu = {"value": tf, "unit": "TFLOPS", "cores": thr, "kind": "port",
+                   "sample": desc + "; oracle/fasted_oracle.c (RZ join restated from mpjoin)",
+                   "extrapolated": True, "anchor_c1_full": c1_anchor(thr)}
         except Exception as exc:   # reported, never silently replaced
             cpu = {"value": None, "unit": "TFLOPS", "cores": None, "kind": "port",
                    "sample": f"failed: {exc}"}
+
+    configs = None
+    if rank == 0 and world == 1 and not args.no_configs:
+        del hd, hd_host
+        torch.cuda.empty_cache()
+        configs = run_configs(args, device, peaks, threads)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None,
             "dtype": "fp16 in / fp32 accumulate (tcgen05 kind::f16)",
             "data": "synthetic uniform [0,1), generate_synthetic seed 12345",
-            "config": {
-                "workload": f"{args.workload}: {name}", "n": n, "d": d, "epsilon": eps,
-                "eps_sq": eps_sq, "pairs": pairs, "selectivity": (pairs - n) / n,
-                "parallelism": f"row-block shard x{world} (no collective)",
-                "l2": "inputs %.2f GB >> 126 MB L2; no flush" % (h2d / 1e9),
-            },
+            "config": config_of(args.workload),
+            "parallelism": f"row-block shard x{world} (no collective)",
+            "eps_sq": eps_sq, "pairs": pairs, "selectivity": (pairs - n) / n,
             "pct_of_fp16_peak": {"measured_burst": value / peak_burst, "measured_sustained":
                                  (value / peak_sus if peak_sus else None),
                                  "nominal_2250": value / 2250.0},
             "pairs_per_s": pairs / (ms / 1e3),
-            "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak,
-                         "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_source": f"{peak_src} {peak_kind} (MEASURED_PEAKS.json)",
-                         "frac_of_burst": achieved / peak_burst,
-                         "kernel": kernel_name,
-                         "launch_includes": "Gram-diagonal pre-pass + augment-row prep "
-                                            "(~1/7800 of the join) + the join",
-                         "output_write_bound_ms": pairs_local * 12 / 6552e9 * 1e3},
+            "roofline": roof,
             "e2e": {"value": flops / e2e_s / 1e12, "unit": "TFLOPS",
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "seconds_per_step": e2e_s, "api": "paper_2508_21230_b200.self_join",
                     "phases_per_step": phases},
+            "quantize": quant,
             "accuracy_vs_fp64": acc,
             "symmetric_schedule": sym,
             # per step: Gram-diagonal pre-pass, aug_prepare_kernel, the join
             "gpu_launches": 3 * args.steps,
-            "clocks": clk.summary(),
+            "clocks": clocks,
             "cpu_baseline": cpu,
             "per_step_ms": per_step,
+            "configs": configs,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -78,24 +78,10 @@ enum {
      * warps instead of running the rare path in the epilogue warps (1M x
      * 128: 1137 vs 992 TFLOPS; at ~1 pair per 1000 examined the hit warps
      * cannot keep up, 2x slower). */
-    FASTED_JOIN_SPARSE = 32,
-    /* Diagnostics for power/throughput attribution (results are NOT valid): */
-    FASTED_JOIN_DIAG_NOEPI = 256,    /* tcgen05 kernel: skip the epilogue entirely     */
-    FASTED_JOIN_DIAG_NOMMA = 512,    /* tcgen05 kernel: skip the MMAs (TMA + epilogue) */
-    FASTED_JOIN_DIAG_LOADONLY = 1024, /* epilogue: TMEM loads only, no math           */
-    FASTED_JOIN_DIAG_NOSLOW = 2048,  /* epilogue: sign test only, never write         */
-    /* 4096: retired (column-scan hit search) */
-    FASTED_JOIN_DIAG_SPIN = 8192,    /* accumulator waits spin (no suspend hint)      */
-    FASTED_JOIN_DIAG_LDX64 = 16384,  /* epilogue: 32x32b.x64 TMEM loads               */
-    FASTED_JOIN_DIAG_AEVL = 32768,   /* CTA pair: A panel loads with L2 evict_last    */
-    FASTED_JOIN_DIAG_TRACE = 65536,  /* resident kernel: per-tile clock64 timeline of
-                                        CTA 0 in the last 266240 bytes of out_records */
-    /* epilogue hit-search A/B (results stay valid): always per-lane masks /
-     * always transposed rows (default: rows for one candidate row in a
-     * 32 x 32 chunk, masks for two or more) */
-    FASTED_JOIN_DIAG_RARE_LM = 131072,
-    FASTED_JOIN_DIAG_RARE_ROWS = 262144
+    FASTED_JOIN_SPARSE = 32
 };
+/* Every other flag bit is rejected (FASTED_ERR_ARGUMENT): no flag, and no
+ * environment setting, changes which pairs are returned. */
 
 int fasted_abi_version(void);
 const char* fasted_strerror(int status);

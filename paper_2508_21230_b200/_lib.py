@@ -16,6 +16,11 @@ from .errors import ArgumentError, CapacityError, DeviceError, RangeError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libfasted.so")
+# Same sources built with -DFASTED_EXPERIMENTS (csrc/experiments.h): the
+# environment overrides of the kernel-form choice, the diagnostic flags and
+# the retired kernel forms.  Used by scripts/ and by the bit-identity tests
+# only; the product path never loads it.
+EXP_LIB_PATH = os.path.join(_HERE, "libfasted_exp.so")
 
 OK, ERR_ARGUMENT, ERR_RANGE, ERR_CAPACITY, ERR_CUDA, ERR_UNSUPPORTED = 0, 2, 3, 4, 5, 6
 JOIN_TC, JOIN_EXACT, JOIN_COUNT, JOIN_SYMMETRIC, JOIN_LOW_OUTPUT, JOIN_APPEND = 0, 1, 2, 4, 8, 16
@@ -28,20 +33,28 @@ EXPORTS = (
     "fasted_sort_workspace_bytes", "fasted_sort_pairs", "fasted_fp64_rows",
 )
 
-_lib = None
+_libs: dict = {}
 _lock = threading.Lock()
 
 
 def load():
-    """Load and type the shared library (no GPU needed)."""
-    global _lib
+    """Load and type the product library libfasted.so (no GPU needed)."""
+    return _load(LIB_PATH)
+
+
+def load_experimental():
+    """Load libfasted_exp.so (experiments and bit-identity tests only)."""
+    return _load(EXP_LIB_PATH)
+
+
+def _load(path):
     with _lock:
-        if _lib is not None:
-            return _lib
-        if not os.path.exists(LIB_PATH):
+        if path in _libs:
+            return _libs[path]
+        if not os.path.exists(path):
             raise DeviceError(
-                f"{LIB_PATH} is not built; run `python __graft_entry__.py` (build()) first")
-        L = ctypes.CDLL(LIB_PATH)
+                f"{path} is not built; run `python __graft_entry__.py` (build()) first")
+        L = ctypes.CDLL(path)
         i64, u64, p, ci, f = (ctypes.c_int64, ctypes.c_uint64, ctypes.c_void_p, ctypes.c_int,
                               ctypes.c_float)
         L.fasted_abi_version.restype = ci
@@ -72,16 +85,19 @@ def load():
         L.fasted_fp64_rows.argtypes = [p, i64, i64, p, i64, ctypes.c_double, p, u64, p, p]
         if L.fasted_abi_version() != 1:
             raise DeviceError("libfasted ABI version mismatch")
-        _lib = L
+        _libs[path] = L
         return L
 
 
-def check(status: int, what: str) -> None:
-    """Map a C-ABI status to the reference's exception classes."""
+def check(status: int, what: str, lib=None) -> None:
+    """Map a C-ABI status to the reference's exception classes (`lib`: the
+    library that returned it -- its thread-local last error -- default the
+    product library)."""
     if status == OK:
         return
-    msg = (load().fasted_last_error() or b"").decode(errors="replace")
-    text = f"{what}: {load().fasted_strerror(status).decode()}" + (f" ({msg})" if msg else "")
+    L = lib if lib is not None else load()
+    msg = (L.fasted_last_error() or b"").decode(errors="replace")
+    text = f"{what}: {L.fasted_strerror(status).decode()}" + (f" ({msg})" if msg else "")
     if status == ERR_ARGUMENT:
         raise ArgumentError(text)
     if status == ERR_RANGE:

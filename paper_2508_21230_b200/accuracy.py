@@ -70,8 +70,9 @@ def join_row_blocks(dd, epsilon: float, rows, exact: bool = False) -> ResultSet:
     `rows` (all columns); `dd` is an engine.DeviceData."""
     from . import engine
 
-    e32 = np.float32(epsilon)
-    eps_sq = float(np.float32(e32 * e32))
+    from .tiling import _eps_sq
+
+    eps_sq = float(_eps_sq(epsilon))
     blocks = np.unique(np.asarray(rows, dtype=np.int64) // engine.BLOCK)
     parts = []
     for b in blocks:

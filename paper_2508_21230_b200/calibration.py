@@ -16,6 +16,7 @@ import math
 
 import numpy as np
 
+from .tiling import _eps_sq
 from . import _lib, engine
 from .analysis import CalibrationResult
 from .errors import ArgumentError, CalibrationError
@@ -70,7 +71,7 @@ def calibrate_epsilon_device(hd, target_s: float, tol: float = 0.01, sample_bloc
     count, m, max_norm = _count_fn(hd, sample_blocks, seed, device)
 
     def estimate(eps: float) -> float:
-        es = float(np.float32(np.float32(eps) * np.float32(eps)))
+        es = float(_eps_sq(eps))
         return (count(es) - m) / m
 
     band = tol * target_s

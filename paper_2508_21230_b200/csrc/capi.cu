@@ -22,6 +22,41 @@ int cuda_status(cudaError_t e, const char* what) {
     return FASTED_ERR_CUDA;
 }
 
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+int encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+                     uint64_t rows, uint64_t row_bytes, uint32_t box_inner, uint32_t box_rows,
+                     CUtensorMapSwizzle swz) {
+    auto encode = tensor_map_encoder();
+    if (!encode) {
+        set_error("cuTensorMapEncodeTiled unavailable from the driver");
+        return FASTED_ERR_CUDA;
+    }
+    cuuint64_t gdim[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+    cuuint64_t gstride[1] = {(cuuint64_t)row_bytes};
+    cuuint32_t box[2] = {box_inner, box_rows};
+    cuuint32_t estride[2] = {1, 1};
+    CUresult cr = encode(map, dt, 2, const_cast<void*>(base), gdim, gstride, box, estride,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d)", (int)cr);
+        return FASTED_ERR_CUDA;
+    }
+    return FASTED_OK;
+}
+
 int sm_count_current() {
     int dev = 0, sms = 148;
     if (cudaGetDevice(&dev) == cudaSuccess)
@@ -91,6 +126,12 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
                            void* stream) {
     const bool count_only = (flags & FASTED_JOIN_COUNT) != 0;
     const int kind = flags & 1;
+    constexpr int kPublicFlags = FASTED_JOIN_EXACT | FASTED_JOIN_COUNT | FASTED_JOIN_SYMMETRIC |
+                                 FASTED_JOIN_LOW_OUTPUT | FASTED_JOIN_APPEND | FASTED_JOIN_SPARSE;
+    if (flags & ~(kPublicFlags | FASTED_JOIN_DIAG_ALL)) {
+        set_error("fasted_join: unknown flag bits 0x%x", flags & ~(kPublicFlags | FASTED_JOIN_DIAG_ALL));
+        return FASTED_ERR_ARGUMENT;
+    }
     if (!values16 || !norms || !count || n_pad < 128 || (n_pad % 128) != 0 || d_pad < 16 ||
         (d_pad % 16) != 0 || n_logical < 1 || n_logical > n_pad || n_pad > 0xffffffffLL) {
         set_error("fasted_join: bad dataset geometry (n_logical=%lld n_pad=%lld d_pad=%lld)",
@@ -109,12 +150,12 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     }
     if (!count_only && capacity > 0 &&
         (!out_records || (reinterpret_cast<uintptr_t>(out_records) & 15u) != 0)) {
-        set_error("fasted_join: 16-byte aligned record buffer required unless FASTED_JOIN_COUNT");
+        set_error("fasted_join: 16-byte aligned record buffer required unless count-only");
         return FASTED_ERR_ARGUMENT;
     }
     const bool symmetric = (flags & FASTED_JOIN_SYMMETRIC) != 0;
     if (symmetric && (kind == FASTED_JOIN_EXACT || row_begin != col_begin || row_end != col_end)) {
-        set_error("fasted_join: FASTED_JOIN_SYMMETRIC needs the tcgen05 kernel and row range == "
+        set_error("fasted_join: the symmetric schedule needs the tcgen05 kernel and row range == "
                   "column range");
         return FASTED_ERR_ARGUMENT;
     }
@@ -138,26 +179,24 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     a.symmetric = symmetric ? 1 : 0;
     a.low_output = (flags & FASTED_JOIN_LOW_OUTPUT) != 0 ? 1 : 0;
     a.sparse = (flags & FASTED_JOIN_SPARSE) != 0 ? 1 : 0;
-    a.diag_flags = flags & (FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA |
-                            FASTED_JOIN_DIAG_LOADONLY | FASTED_JOIN_DIAG_NOSLOW |
-                            FASTED_JOIN_DIAG_SPIN | FASTED_JOIN_DIAG_LDX64 |
-                            FASTED_JOIN_DIAG_AEVL | FASTED_JOIN_DIAG_TRACE |
-                            FASTED_JOIN_DIAG_RARE_LM | FASTED_JOIN_DIAG_RARE_ROWS);
+    a.diag_flags = flags & FASTED_JOIN_DIAG_ALL;   // always 0 in libfasted.so
     a.out = reinterpret_cast<uint4*>(out_records);
     a.capacity = count_only ? 0ull : (unsigned long long)capacity;
     a.count = count;
     a.gram_diag = nullptr;
     a.trace = nullptr;
+#ifdef FASTED_EXPERIMENTS
     if (flags & FASTED_JOIN_DIAG_TRACE) {
         const unsigned long long trace_recs = TRACE_WORDS / 2;
         if (count_only || a.capacity < trace_recs) {
-            set_error("fasted_join: FASTED_JOIN_DIAG_TRACE needs a record buffer with room for "
-                      "the timeline");
+            set_error("fasted_join: the trace flag needs a record buffer with room for the "
+                      "timeline");
             return FASTED_ERR_ARGUMENT;
         }
         a.capacity -= trace_recs;
         a.trace = reinterpret_cast<unsigned long long*>(a.out + a.capacity);
     }
+#endif
     const __half* X = reinterpret_cast<const __half*>(values16);
     return kind == FASTED_JOIN_EXACT ? launch_join_exact(X, a, s) : launch_join_tc(X, a, s);
 }

@@ -1,6 +1,7 @@
 // Shared device/host helpers for libfasted (sm_100a only).
 #pragma once
 
+#include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -27,6 +28,13 @@ int cuda_status(cudaError_t e, const char* what);
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 int sm_count_current();
+
+// A 2-D TMA tensor map: `rows` x `inner` elements of type dt, row pitch
+// row_bytes (multiple of 16), box box_rows x box_inner, given swizzle;
+// out-of-range elements load as zero.  Returns a FASTED_* status.
+int encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
+              uint64_t rows, uint64_t row_bytes, uint32_t box_inner, uint32_t box_rows,
+              CUtensorMapSwizzle swz);
 
 // cudaFuncSetAttribute applies per device context: a launcher keeps one of
 // these per kernel and sets the attribute once for each device it runs on

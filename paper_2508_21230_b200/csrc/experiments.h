@@ -1,0 +1,75 @@
+// Experiment switches: compiled into libfasted_exp.so only.
+//
+// The product library (libfasted.so) is built WITHOUT FASTED_EXPERIMENTS.
+// There, the kernel form is a fixed rule of (d_pad, rows, cols) and the
+// caller's LOW_OUTPUT / SPARSE hints (all forms give bit-identical records,
+// tests/test_gpu.py), nothing reads the environment, and the diagnostic
+// flags below do not exist -- results never depend on configuration
+// (the reference's own rule, tiling.py:296-297).
+//
+// libfasted_exp.so (same sources, -DFASTED_EXPERIMENTS) is used by scripts/
+// (A/B timing, power and trace experiments) and by the bit-identity tests,
+// which force every kernel form through the environment overrides and
+// compare the records with the product library's.
+#pragma once
+
+#include <stdlib.h>
+
+namespace fasted {
+
+#ifdef FASTED_EXPERIMENTS
+
+// Diagnostic fasted_join flags (results are NOT valid unless stated).
+enum {
+    FASTED_JOIN_DIAG_NOEPI = 256,      // tcgen05 kernel: skip the epilogue entirely
+    FASTED_JOIN_DIAG_NOMMA = 512,      // tcgen05 kernel: skip the MMAs (TMA + epilogue)
+    FASTED_JOIN_DIAG_LOADONLY = 1024,  // epilogue: TMEM loads only, no math
+    FASTED_JOIN_DIAG_NOSLOW = 2048,    // epilogue: sign test only, never write
+    FASTED_JOIN_DIAG_SPIN = 8192,      // accumulator waits spin (no suspend hint)
+    FASTED_JOIN_DIAG_LDX64 = 16384,    // epilogue: 32x32b.x64 TMEM loads
+    FASTED_JOIN_DIAG_AEVL = 32768,     // CTA pair: A panel loads with L2 evict_last
+    FASTED_JOIN_DIAG_TRACE = 65536,    // resident kernel: clock64 timeline of CTA 0 in the
+                                       // last 266240 bytes of out_records
+    // epilogue hit-search A/B (results stay valid): always per-lane masks /
+    // always transposed rows
+    FASTED_JOIN_DIAG_RARE_LM = 131072,
+    FASTED_JOIN_DIAG_RARE_ROWS = 262144
+};
+constexpr int FASTED_JOIN_DIAG_ALL =
+    FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA | FASTED_JOIN_DIAG_LOADONLY |
+    FASTED_JOIN_DIAG_NOSLOW | FASTED_JOIN_DIAG_SPIN | FASTED_JOIN_DIAG_LDX64 |
+    FASTED_JOIN_DIAG_AEVL | FASTED_JOIN_DIAG_TRACE | FASTED_JOIN_DIAG_RARE_LM |
+    FASTED_JOIN_DIAG_RARE_ROWS;
+
+inline int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+// An environment override of a kernel-form or schedule default.
+#define FASTED_KNOB(name, dflt) ::fasted::env_int(name, dflt)
+// The diagnostic flags of a launch.
+#define FASTED_DFLAGS(a) ((a).diag_flags)
+
+#else
+
+constexpr int FASTED_JOIN_DIAG_ALL = 0;
+// Product build: every knob is its default, no diagnostic flag is set (the
+// compiler removes the diagnostic branches).
+#define FASTED_KNOB(name, dflt) (dflt)
+#define FASTED_DFLAGS(a) 0
+enum {
+    FASTED_JOIN_DIAG_NOEPI = 0,
+    FASTED_JOIN_DIAG_NOMMA = 0,
+    FASTED_JOIN_DIAG_LOADONLY = 0,
+    FASTED_JOIN_DIAG_NOSLOW = 0,
+    FASTED_JOIN_DIAG_SPIN = 0,
+    FASTED_JOIN_DIAG_LDX64 = 0,
+    FASTED_JOIN_DIAG_AEVL = 0,
+    FASTED_JOIN_DIAG_TRACE = 0,
+    FASTED_JOIN_DIAG_RARE_LM = 0,
+    FASTED_JOIN_DIAG_RARE_ROWS = 0
+};
+
+#endif
+
+}  // namespace fasted

@@ -2,6 +2,7 @@
 // combine, and the chunked pair writer.
 #pragma once
 #include "common.cuh"
+#include "experiments.h"
 
 namespace fasted {
 
@@ -11,7 +12,7 @@ struct JoinArgs {
     int64_t row_begin, row_end, col_begin, col_end;
     float eps_sq;
     int count_only;
-    int diag_flags;                    // FASTED_JOIN_DIAG_* (experiments only)
+    int diag_flags;                    // diagnostic flags (libfasted_exp.so only; 0 here)
     int symmetric;                     // FASTED_JOIN_SYMMETRIC: upper tiles, mirrored records
     int low_output;                    // FASTED_JOIN_LOW_OUTPUT hint (kernel choice only)
     int sparse;                        // FASTED_JOIN_SPARSE hint (kernel choice only)

@@ -482,7 +482,7 @@ __device__ __forceinline__ void epi_chunk(const JoinArgs& a, W& wr, const uint32
     const uint32_t acc = and_tree32(r);
     const bool diag = (jb < iw + 32) && (iw < jb + 32);   // warp-uniform
     if (!__any_sync(0xffffffffu, (int)acc >= 0) && !diag) return;
-    if (a.diag_flags & FASTED_JOIN_DIAG_NOSLOW) return;
+    if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOSLOW) return;
     // rare path.  Self pairs first: distance exactly 0 (the reference's
     // a_ii and s_i are the same chain), one append for the whole warp.
     if (diag) {
@@ -545,7 +545,7 @@ __device__ __forceinline__ void epi_chunk_res(const JoinArgs& a, W& wr, const ui
     const bool diag = (jb < iw + 32) && (iw < jb + 32);   // warp-uniform
     const uint32_t rows = __ballot_sync(0xffffffffu, (int)acc >= 0 && row_ok);
     if (rows == 0u && !diag) return;
-    if (a.diag_flags & FASTED_JOIN_DIAG_NOSLOW) return;
+    if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOSLOW) return;
     const uint32_t lane = threadIdx.x & 31u;
     // rare path.  Self pairs first: distance exactly 0 (the reference's
     // a_ii and s_i are the same chain), one append for the whole warp.
@@ -559,8 +559,8 @@ __device__ __forceinline__ void epi_chunk_res(const JoinArgs& a, W& wr, const ui
     // masks, all rows at once (serialising rows measured 20% slower at
     // 60K x 512, where a 32 x 32 chunk holds ~1 pair; A/B flags force either).
     const bool multi = (rows & (rows - 1u)) != 0u;
-    if (((a.diag_flags & FASTED_JOIN_DIAG_RARE_LM) || multi) &&
-        !(a.diag_flags & FASTED_JOIN_DIAG_RARE_ROWS)) {
+    if (((FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_RARE_LM) || multi) &&
+        !(FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_RARE_ROWS)) {
         // per-lane hit masks: all candidate rows at once
         uint32_t lm = hit_mask32(r);
         const int64_t valid = a.n_logical - jb;
@@ -638,12 +638,12 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
     // CTA's rows lie past the range end
     const int64_t left = a.col_end - (col0 + h * HALF);
     int nchunks = left <= 0 ? 0 : (left >= HALF ? NCH : (int)(left / 32));
-    if (row0 >= a.row_end || (a.diag_flags & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
+    if (row0 >= a.row_end || (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
     const uint32_t tcol = tmem_base + lane_base + (uint32_t)(buf * TBN + h * HALF);
-    mbar_wait2(tfull, aph, (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+    mbar_wait2(tfull, aph, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
     tc_fence_after();
     uint32_t r0[32], r1[32], r2[32], r3[32];
-    if (NCH > 1 && (a.diag_flags & FASTED_JOIN_DIAG_LDX64) && nchunks == NCH) {
+    if (NCH > 1 && (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_LDX64) && nchunks == NCH) {
         tmem_ld64(tcol, r0, r1);
         if (NCH > 2) tmem_ld64(tcol + 64u, r2, r3);
     } else {
@@ -667,7 +667,7 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
         else mbar_arrive_remote(tempty, 0);
     }
     const int64_t jb = col0 + h * HALF;
-    if (a.diag_flags & FASTED_JOIN_DIAG_LOADONLY) return;
+    if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_LOADONLY) return;
     // Whole-slice sign test first: one vote per tile in the common case (no
     // hit in the warp's 32 x HALF slice, no diagonal), instead of a vote and
     // a dependent AND chain per 32-column chunk (measured at 1M x 128: the
@@ -997,9 +997,9 @@ __device__ __forceinline__ void epilogue_tile_hit(const JoinArgs& a, uint32_t re
     const bool row_ok = i < a.n_logical && i < a.row_end;
     const int64_t left = a.col_end - (col0 + h * HALF);
     int nchunks = left <= 0 ? 0 : (left >= HALF ? NCH : (int)(left / 32));
-    if (row0 >= a.row_end || (a.diag_flags & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
+    if (row0 >= a.row_end || (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
     const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TBN + h * HALF);
-    mbar_wait2(tfull, aph, (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+    mbar_wait2(tfull, aph, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
     tc_fence_after();
     uint32_t r0[32], r1[32];
     if (nchunks > 0) tmem_ld32(tcol, r0);
@@ -1014,13 +1014,13 @@ __device__ __forceinline__ void epilogue_tile_hit(const JoinArgs& a, uint32_t re
         if (CG == 1 || leader) mbar_arrive_relaxed(tempty);
         else mbar_arrive_remote(tempty, 0);
     }
-    if (a.diag_flags & FASTED_JOIN_DIAG_LOADONLY) return;
+    if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_LOADONLY) return;
     const int64_t jb = col0 + h * HALF;
     if (nchunks == NCH && !((jb < iw + 32) && (iw < jb + HALF))) {
         const uint32_t all = and_tree32(r0) & and_tree32(r1);
         if (!__any_sync(0xffffffffu, (int)all >= 0)) return;
     }
-    if (a.diag_flags & FASTED_JOIN_DIAG_NOSLOW) return;
+    if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOSLOW) return;
     if (nchunks > 0)
         hit_push<NHIT>(reg, smem_raw, raw, hq, r0, (int)jb, (int)i, (int)iw, row_ok, (uint32_t)lane);
     if (nchunks > 1)
@@ -1138,7 +1138,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                                                        (b_hi ? 2 : 1) * B_HALF_BYTES);
                             if (a_mine)
                             {
-                                if (a.diag_flags & FASTED_JOIN_DIAG_AEVL)
+                                if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_AEVL)
                                     tma_load_2d_pair_hint(sA + s * A_BYTES, &tmap_x, fb, kx, my_a,
                                                           pol_evl);
                                 else
@@ -1182,7 +1182,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
     } else if (warp == 1) {
         // ---------------- MMA issuer (the leader CTA of a pair)
         if (leader) {   // whole warp; one elected lane issues
-            const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
+            const bool no_mma = (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOMMA) != 0;
             int s = 0;
             uint32_t ph = 0;
             int lt = 0;
@@ -1235,7 +1235,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
     } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
         // ---------------- hit warp
         hit_warp_loop<NHIT>(a, bars + BAR_BYTES, warp - FIRST_EPI_WARP - NEPI, NEPI / NHIT, lane,
-                            (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+                            (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
     } else {
         // ---------------- epilogue
         const int q = warp & 3;          // TMEM lane quarter this warp may access
@@ -1438,7 +1438,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (every CTA; M = 128; whole warp, one lane issues)
-        const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
+        const bool no_mma = (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOMMA) != 0;
         int s = 0;
         uint32_t ph = 0;
         int lt = 0;
@@ -1454,7 +1454,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
             const int buf = lt & 1;
             mbar_wait2(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u,
-                       (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+                       (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
             tc_fence_after();
             const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
             for (int kb = 0; kb < sch.nkb + 1; kb++) {
@@ -1488,7 +1488,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
     } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
         // ---------------- hit warp
         hit_warp_loop<NHIT>(a, bars + BAR_BYTES, warp - FIRST_EPI_WARP - NEPI, NEPI / NHIT, lane,
-                            (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+                            (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
     } else {
         // ---------------- epilogue
         const int q = warp & 3;
@@ -1760,7 +1760,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
     } else if (warp == 1) {
         // ---------------- MMA issuer (the leader CTA of a pair)
         if (leader) {   // whole warp; one elected lane issues
-            const bool no_mma = (a.diag_flags & FASTED_JOIN_DIAG_NOMMA) != 0;
+            const bool no_mma = (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOMMA) != 0;
             int s = 0;
             uint32_t ph = 0;
             int lt = 0, ua = 0;
@@ -1774,7 +1774,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                 for (int ct = ct0; ct < ct1; ct++, ++lt) {
                     const int buf = lt % NACC;
                     mbar_wait2(tempty_bar(buf), ((uint32_t)(lt / NACC) & 1u) ^ 1u,
-                               (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+                               (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
                     tc_fence_after();
                     unsigned long long* tr =
                         (TRACE && a.trace && blockIdx.x == 0 && lt < TRACE_TILES)
@@ -1820,7 +1820,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
     } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
         // ---------------- hit warp
         hit_warp_loop<NHIT>(a, bars + C::BAR_REGION, warp - FIRST_EPI_WARP - NEPI, NEPI / NHIT,
-                            lane, (a.diag_flags & FASTED_JOIN_DIAG_SPIN) != 0);
+                            lane, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
     } else {
         // ---------------- epilogue
         constexpr int NSPLIT = NEPI / 4;
@@ -1841,7 +1841,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         const uint32_t release0 = local_release ? tempty_bar(0) : mapa_shared(tempty_bar(0), 0);
         const uint32_t release1 = local_release ? tempty_bar(1) : mapa_shared(tempty_bar(1), 0);
         const uint32_t tfull0 = tfull_bar(0);
-        const int dflags = a.diag_flags;
+        const int dflags = FASTED_DFLAGS(a);
         const bool spin = (dflags & FASTED_JOIN_DIAG_SPIN) != 0;
         const bool noepi = (dflags & FASTED_JOIN_DIAG_NOEPI) != 0;
         // 32-bit point indices (n_pad < 2^31; records hold 32-bit ids anyway);
@@ -1915,6 +1915,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
     }
 }
 
+#ifdef FASTED_EXPERIMENTS
 // ---------------------------------------------------------------------------
 // TMEM-A variant (d_pad <= 128, CTA pair).  The resident kernel at d = 128 is
 // epilogue bound: a 256 x 256 tile is ~1150 MMA cycles and, with only two
@@ -2200,6 +2201,7 @@ join_tc_ts_kernel(const uint4* __restrict__ X, const __grid_constant__ CUtensorM
                      "r"(TMEM_COLS)
                      : "memory");
 }
+#endif  // FASTED_EXPERIMENTS
 
 // Exact split of an FP32 value into three TF32 values (10-bit mantissas,
 // low 13 bits zero) whose sum is the input: 3 x 11 significant bits >= 24.
@@ -2215,66 +2217,37 @@ __device__ __forceinline__ void split_tf32(float x, float& h1, float& h2, float&
     h3 = tf32(__fsub_rn(r1, h2));
 }
 
-// Augment rows: A_i = [sigma_i parts, 1, 1, 1, 0, 0], B_j = [1, 1, 1,
-// rho_j parts, 0, 0] with sigma = -s/2 and rho = -s/2 + eps^2/2, so that
-// A_i . B_j = (eps^2 - s_i - s_j) / 2.
+// Augment rows: A_i = [sigma_i parts (3), 1, 1, 1, 1, 1] and
+// B_j = [1, 1, 1, rho_j parts (3), rho'_j parts (2)] with sigma = -s/2 (exact)
+// and rho + rho' = sigma + eps^2/2 EXACTLY (TwoSum: rho = RN(sigma + eps^2/2),
+// rho' its rounding error, an FP32 value below ulp(rho)/2 whose two TF32
+// parts drop at most its last 2 bits, i.e. < 2^-46 |rho|).  So
+// A_i . B_j = (eps^2 - s_i - s_j) / 2 up to the tensor core's own summation:
+// even when eps^2 >> s, an exact duplicate pair comes out at
+// D = eps^2/2, i.e. distance 0, as in the reference.
 __global__ void aug_prepare_kernel(const float* __restrict__ norms, int64_t begin, int64_t end,
                                    float eps_sq, float4* __restrict__ aug_a,
                                    float4* __restrict__ aug_b) {
     const int64_t i = begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= end) return;
     const float sigma = -0.5f * norms[i];
-    const float rho = __fadd_rn(sigma, 0.5f * eps_sq);
-    float a1, a2, a3, b1, b2, b3;
+    const float half_eps = 0.5f * eps_sq;   // exact (no underflow for eps_sq >= 2^-125)
+    const float rho = __fadd_rn(sigma, half_eps);
+    // TwoSum (Knuth): rho + err == sigma + half_eps exactly
+    const float bv = __fsub_rn(rho, sigma);
+    const float av = __fsub_rn(rho, bv);
+    const float err = __fadd_rn(__fsub_rn(sigma, av), __fsub_rn(half_eps, bv));
+    float a1, a2, a3, b1, b2, b3, c1, c2, c3;
     split_tf32(sigma, a1, a2, a3);
     split_tf32(rho, b1, b2, b3);
+    split_tf32(err, c1, c2, c3);
     aug_a[2 * i] = make_float4(a1, a2, a3, 1.0f);
-    aug_a[2 * i + 1] = make_float4(1.0f, 1.0f, 0.0f, 0.0f);
+    aug_a[2 * i + 1] = make_float4(1.0f, 1.0f, 1.0f, 1.0f);
     aug_b[2 * i] = make_float4(1.0f, 1.0f, 1.0f, b1);
-    aug_b[2 * i + 1] = make_float4(b2, b3, 0.0f, 0.0f);
+    aug_b[2 * i + 1] = make_float4(b2, b3, c1, c2);
 }
 
 }  // namespace tc
-
-static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    }
-    return fn;
-}
-
-static int encode_2d(CUtensorMap* map, CUtensorMapDataType dt, const void* base, uint64_t inner,
-                     uint64_t rows, uint64_t row_bytes, uint32_t box_inner, uint32_t box_rows,
-                     CUtensorMapSwizzle swz) {
-    auto encode = tensor_map_encoder();
-    if (!encode) {
-        set_error("cuTensorMapEncodeTiled unavailable from the driver");
-        return FASTED_ERR_CUDA;
-    }
-    cuuint64_t gdim[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
-    cuuint64_t gstride[1] = {(cuuint64_t)row_bytes};
-    cuuint32_t box[2] = {box_inner, box_rows};
-    cuuint32_t estride[2] = {1, 1};
-    CUresult cr = encode(map, dt, 2, const_cast<void*>(base), gdim, gstride, box, estride,
-                         CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (cr != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed (%d)", (int)cr);
-        return FASTED_ERR_CUDA;
-    }
-    return FASTED_OK;
-}
-
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
 
 template <int CG, bool DIAG = false, int NEPI = tc::NUM_EPI_WARPS, int NHIT = 0>
 static cudaError_t launch_variant(const CUtensorMap& mx, const CUtensorMap& ma,
@@ -2330,7 +2303,7 @@ static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const
     sch.col_tiles = (int)((a.col_end - a.col_begin + BN - 1) / BN);
     // 8192-row groups (measured at 1M x 960: 1374 TFLOPS vs 1305 for 4096 and
     // 1182 for 16384; profiles/round1/tune_c4_elect_session2.txt)
-    sch.group = env_int("FASTED_GROUP_ROWS", 8192) / (2 * BM);
+    sch.group = FASTED_KNOB("FASTED_GROUP_ROWS", 8192) / (2 * BM);
     if (sch.group < 1) sch.group = 1;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.total = (int64_t)sch.row_tiles * sch.col_tiles;
@@ -2361,19 +2334,22 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     using namespace tc;
     using C = ResCfg<CG, TBN>;
     constexpr int SMEM_MAX = 227 * 1024;
+#ifdef FASTED_EXPERIMENTS
     constexpr bool CAN_TRACE = CG == 2 && TBN == 256 && NEPI == 16 && NHIT == 0;
-    auto kern = (CAN_TRACE && a.trace) ? join_tc_res_kernel<CG, TBN, NEPI, CAN_TRACE, 0>
-                                       : join_tc_res_kernel<CG, TBN, NEPI, false, NHIT>;
+#else
+    constexpr bool CAN_TRACE = false;   // the clock64 timeline exists in libfasted_exp.so only
+#endif
+    auto kern = join_tc_res_kernel<CG, TBN, NEPI, false, NHIT>;
     static PerDeviceOnce attr_once, attr_once_trace;
-    if (CAN_TRACE && a.trace) {
-        cudaError_t e = attr_once_trace.run([&] {
-            return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        SMEM_MAX);
-        });
-        if (e != cudaSuccess) return e;
-    } else
+    PerDeviceOnce* once = &attr_once;
+    if constexpr (CAN_TRACE) {
+        if (a.trace) {
+            kern = join_tc_res_kernel<CG, TBN, NEPI, true, 0>;
+            once = &attr_once_trace;
+        }
+    }
     {
-        cudaError_t e = attr_once.run([&] {
+        cudaError_t e = once->run([&] {
             return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         SMEM_MAX);
         });
@@ -2394,7 +2370,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     sch.col_tiles = (int)((a.col_end - a.col_begin + TBN - 1) / TBN);
     // a segment of ~16K columns per unit: the A panel load is amortised over
     // many tiles and the units stay small enough to balance
-    int seg = env_int("FASTED_SEG_TILES", 16384 / TBN);
+    int seg = FASTED_KNOB("FASTED_SEG_TILES", 16384 / TBN);
     if (seg < 1) seg = 1;
     sch.nsegs = (sch.col_tiles + seg - 1) / seg;
     sch.units = (int64_t)sch.row_tiles * sch.nsegs;
@@ -2434,16 +2410,16 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
 // (60K x 512: 1203 vs 1186).
 enum { TC_STREAMING = 0, TC_RESIDENT = 1, TC_MULTICAST = 2 };
 static int tc_variant(int64_t d_pad, int64_t rows, int64_t cols, bool low_output, int* cg) {
-    const int cg_env = env_int("FASTED_CTA_GROUP", 0);
+    const int cg_env = FASTED_KNOB("FASTED_CTA_GROUP", 0);
     // resident A up to d_pad 512 (one 132 KB A buffer + 4 B stages at 512);
     // measured at 60K x 512: 2.52 vs 2.85 ms, 5M x 384 shard: 1616-1640 vs
     // 2003-2122 ms for S <= 1000 (alternating launches) -- the streaming
     // forms move A and B from L2 per tile (~64 B/clk/SM at d = 512, above
     // what L2 delivers at 1.97 GHz), resident A only B
-    const int64_t res_max = env_int("FASTED_RES_MAXD", 512);
+    const int64_t res_max = FASTED_KNOB("FASTED_RES_MAXD", 512);
     *cg = cg_env == 1 ? 1 : cg_env == 2 ? 2 : (d_pad <= res_max ? 2 : 1);
-    if (d_pad <= res_max) return env_int("FASTED_RESIDENT", 1) != 0 ? TC_RESIDENT : TC_STREAMING;
-    if (cg_env != 0 || env_int("FASTED_MC", 1) == 0) return TC_STREAMING;
+    if (d_pad <= res_max) return FASTED_KNOB("FASTED_RESIDENT", 1) != 0 ? TC_RESIDENT : TC_STREAMING;
+    if (cg_env != 0 || FASTED_KNOB("FASTED_MC", 1) == 0) return TC_STREAMING;
     if (low_output && (double)rows * (double)cols >= 68.7e9) {   // >= 2^36 pairs examined
         *cg = 2;
         return TC_STREAMING;
@@ -2453,29 +2429,30 @@ static int tc_variant(int64_t d_pad, int64_t rows, int64_t cols, bool low_output
 
 // Hit warps (resident CTA pair, multicast): on the caller's
 // FASTED_JOIN_SPARSE hint; FASTED_RES_HIT / FASTED_MC_HIT = 0 or 2 override.
-static bool res_hit(bool sparse) { return env_int("FASTED_RES_HIT", sparse ? 2 : 0) == 2; }
-static bool mc_hit(bool sparse) { return env_int("FASTED_MC_HIT", sparse ? 2 : 0) == 2; }
-static bool stream_hit(bool sparse) { return env_int("FASTED_STREAM_HIT", sparse ? 2 : 0) == 2; }
+static bool res_hit(bool sparse) { return FASTED_KNOB("FASTED_RES_HIT", sparse ? 2 : 0) == 2; }
+static bool mc_hit(bool sparse) { return FASTED_KNOB("FASTED_MC_HIT", sparse ? 2 : 0) == 2; }
+static bool stream_hit(bool sparse) { return FASTED_KNOB("FASTED_STREAM_HIT", sparse ? 2 : 0) == 2; }
 
 const char* join_tc_kernel_name(int64_t d_pad, int64_t rows, int64_t cols, bool low_output,
                                 bool sparse) {
     int cg = 0;
     switch (tc_variant(d_pad, rows, cols, low_output, &cg)) {
         case TC_RESIDENT:
-            if (cg == 2 && env_int("FASTED_RES_EPI", 16) == 16 && res_hit(sparse))
+            if (cg == 2 && FASTED_KNOB("FASTED_RES_EPI", 16) == 16 && res_hit(sparse))
                 return "fasted::tc::join_tc_res_kernel<2> + 2 hit warps";
             return cg == 2 ? "fasted::tc::join_tc_res_kernel<2>" : "fasted::tc::join_tc_res_kernel<1>";
         case TC_MULTICAST:
-            if (env_int("FASTED_MC_EPI", 16) == 16 && mc_hit(sparse))
+            if (FASTED_KNOB("FASTED_MC_EPI", 16) == 16 && mc_hit(sparse))
                 return "fasted::tc::join_tc_mc_kernel + 2 hit warps";
             return "fasted::tc::join_tc_mc_kernel";
         default:
-            if (cg == 2 && env_int("FASTED_STREAM_EPI", 16) == 16 && stream_hit(sparse))
+            if (cg == 2 && FASTED_KNOB("FASTED_STREAM_EPI", 16) == 16 && stream_hit(sparse))
                 return "fasted::tc::join_tc_kernel<2> + 2 hit warps";
             return cg == 2 ? "fasted::tc::join_tc_kernel<2>" : "fasted::tc::join_tc_kernel<1>";
     }
 }
 
+#ifdef FASTED_EXPERIMENTS
 // TMEM-A launch (d_pad <= 128, CTA pair).
 static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUtensorMap& ma,
                              const CUtensorMap& mbb, const JoinArgs& a, cudaStream_t s) {
@@ -2500,7 +2477,7 @@ static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUte
     if (sch.stages > TS_MAX_STAGES) sch.stages = TS_MAX_STAGES;
     sch.row_tiles = (int)((a.row_end - a.row_begin + 2 * BM - 1) / (2 * BM));
     sch.col_tiles = (int)((a.col_end - a.col_begin + TS_TBN - 1) / TS_TBN);
-    int seg = env_int("FASTED_SEG_TILES", 16384 / TS_TBN);
+    int seg = FASTED_KNOB("FASTED_SEG_TILES", 16384 / TS_TBN);
     if (seg < 1) seg = 1;
     sch.nsegs = (sch.col_tiles + seg - 1) / seg;
     sch.units = (int64_t)sch.row_tiles * sch.nsegs;
@@ -2522,6 +2499,7 @@ static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUte
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, reinterpret_cast<const uint4*>(X), mxb, ma, mbb, a, sch);
 }
+#endif  // FASTED_EXPERIMENTS
 
 int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     using namespace tc;
@@ -2540,7 +2518,9 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     //                 (join_tc_mc_kernel; 1M x 960: 1374 vs 1226 single-CTA
     //                 and ~980 for the CTA pair, which at the 1 kW cap runs
     //                 its clock down to ~920 MHz; 60K x 512: 1373 vs 1307).
-    // FASTED_CTA_GROUP=1|2 forces the streaming kernel with that CTA group.
+    //   d_pad >  512, >= 2^36 examined pairs, LOW_OUTPUT hint: the streaming
+    //                 CTA pair with a 16K-row raster (C4: 1376-1415 TFLOPS).
+    // (libfasted_exp.so: FASTED_CTA_GROUP=1|2 forces the streaming kernel.)
     int cg = 1;
     const int variant = tc_variant(a.d_pad, a.row_end - a.row_begin, a.col_end - a.col_begin,
                                    a.low_output != 0, &cg);
@@ -2553,14 +2533,13 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     float4* aug_a = aug;
     float4* aug_b = aug + 2 * a.n_pad;
     float* gram = reinterpret_cast<float*>(aug + 4 * a.n_pad);
-    // Norms for the augment rows: by default the tensor core's own a_ii
-    // (Gram-diagonal pre-pass, ~1/(n/128) of the join's work), so the norm
-    // terms carry the same accumulation error as a_ij and cancel in
-    // d2 = a_ii + a_jj - 2 a_ij (the reference's own RZ norms paired with
-    // tensor-core a_ij bias d2 low by ~2e-3 relative at d = 960, measured
-    // as a 0.43% vs 0.14% Eq. 3 loss).  It also makes exact duplicates
-    // distance 0, as in the reference.  FASTED_TC_NORMS=0 uses the RZ norms.
-    const bool tc_norms = env_int("FASTED_TC_NORMS", 1) != 0;
+    // Norms for the augment rows: the tensor core's own a_ii (Gram-diagonal
+    // pre-pass, ~1/(n/128) of the join's work), so the norm terms carry the
+    // same accumulation error as a_ij and cancel in d2 = a_ii + a_jj - 2 a_ij
+    // (the reference's RZ norms paired with tensor-core a_ij bias d2 low by
+    // ~2e-3 relative at d = 960, twice the 1e-3 band -- measured as a 0.43% vs
+    // 0.14% Eq. 3 loss -- so they are never used here).  It also makes exact
+    // duplicates distance 0, as in the reference.
     CUtensorMap mx, ma, mb;
     int st = encode_2d(&mx, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, X, a.d_pad, a.n_pad, a.d_pad * 2, BK,
                        BM, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -2588,46 +2567,53 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     for (int g = 0; g < nrg; g++) {
         const int64_t lo = rg[g][0], hi = rg[g][1];
         if (hi <= lo) continue;
-        if (tc_norms) {
-            JoinArgs ad = a;
-            ad.row_begin = lo;
-            ad.row_end = hi;
-            ad.col_begin = lo;
-            ad.col_end = hi;
-            ad.count_only = 1;
-            ad.capacity = 0;
-            ad.diag_flags = 0;
-            ad.symmetric = 0;
-            ad.trace = nullptr;
-            ad.gram_diag = gram;
-            Sched sd;
-            sd.row_tiles = (int)((hi - lo + BM - 1) / BM);
-            sd.col_tiles = 1;
-            sd.group = 1;
-            sd.nkb = (int)((a.d_pad + BK - 1) / BK);
-            sd.total = sd.row_tiles;
-            sd.diag = 1;
-            e = launch_variant<1, true>(mx, ma, mb, ad, sd, s);
-            if (e == cudaSuccess) e = cudaGetLastError();
-            if (e != cudaSuccess) {
-                cudaFreeAsync(aug, s);
-                return cuda_status(e, "join_tc_kernel (Gram diagonal)");
-            }
+        JoinArgs ad = a;
+        ad.row_begin = lo;
+        ad.row_end = hi;
+        ad.col_begin = lo;
+        ad.col_end = hi;
+        ad.count_only = 1;
+        ad.capacity = 0;
+        ad.diag_flags = 0;
+        ad.symmetric = 0;
+        ad.trace = nullptr;
+        ad.gram_diag = gram;
+        Sched sd;
+        sd.row_tiles = (int)((hi - lo + BM - 1) / BM);
+        sd.col_tiles = 1;
+        sd.group = 1;
+        sd.nkb = (int)((a.d_pad + BK - 1) / BK);
+        sd.total = sd.row_tiles;
+        sd.diag = 1;
+        e = launch_variant<1, true>(mx, ma, mb, ad, sd, s);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e != cudaSuccess) {
+            cudaFreeAsync(aug, s);
+            return cuda_status(e, "join_tc_kernel (Gram diagonal)");
         }
-        aug_prepare_kernel<<<(unsigned)((hi - lo + 255) / 256), 256, 0, s>>>(
-            tc_norms ? gram : a.norms, lo, hi, a.eps_sq, aug_a, aug_b);
+        aug_prepare_kernel<<<(unsigned)((hi - lo + 255) / 256), 256, 0, s>>>(gram, lo, hi,
+                                                                             a.eps_sq, aug_a, aug_b);
         e = cudaGetLastError();
         if (e != cudaSuccess) {
             cudaFreeAsync(aug, s);
             return cuda_status(e, "aug_prepare_kernel");
         }
     }
-    // Resident-A form for d_pad <= 512 (FASTED_RESIDENT=0 selects streaming),
-    // 256-column tiles, two accumulators.  (128-column tiles with four
-    // accumulators measured slower, 372 vs 283 ms at 1M x 128 -- the N=128
-    // MMAs re-read A every 64 cycles -- and were removed.)
+    // Resident-A form for d_pad <= 512: CTA pair, 256-column tiles, two
+    // accumulators, 16 epilogue warps of 64 columns each plus, on the
+    // caller's SPARSE hint, two hit warps that own the rare path and the
+    // record writers (1M x 128, alternating launches: 225 vs 258 ms median).
+    // Measured alternatives kept in libfasted_exp.so: 8 epilogue warps of 128
+    // columns (269-319 vs 254 ms at 1M x 128, profiles/round1/
+    // tune_c3_epi_ab_session2.txt); 128-column tiles with four accumulators
+    // (372 vs 283 ms: the N=128 MMAs re-read A every 64 cycles); A in TMEM
+    // (286-296 vs 256 ms).
     if (variant == TC_RESIDENT) {
-        const bool ts = cg == 2 && a.d_pad <= 128 && env_int("FASTED_TS", 0) != 0;
+#ifdef FASTED_EXPERIMENTS
+        const bool ts = cg == 2 && a.d_pad <= 128 && FASTED_KNOB("FASTED_TS", 0) != 0;
+#else
+        constexpr bool ts = false;
+#endif
         const int tbn = ts ? 128 : 256;
         const int nb = tbn / cg, bbox = nb < 128 ? nb : 128;
         CUtensorMap mxb, mbb;
@@ -2640,35 +2626,34 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
             cudaFreeAsync(aug, s);
             return st;
         }
-        // 16 epilogue warps, each draining 64 columns, plus (sparse output)
-        // two hit warps that own the rare path and the record writers
-        // (measured at 1M x 128, alternating launches: 225 vs 258 ms
-        // median); FASTED_RES_EPI=8: 8 warps of 128 columns.  Measured at 1M x 128, alternating runs on
-        // one box: 253.8-253.9 ms with 16 vs 269-319 ms with 8 -- the shorter
-        // per-warp chain per tile also removes the run-to-run spread
-        // (profiles/round1/tune_c3_epi_ab_session2.txt).
+#ifdef FASTED_EXPERIMENTS
         if (ts)
             e = launch_ts(X, mxb, ma, mbb, a, s);
-        else if (cg == 2)
-            e = env_int("FASTED_RES_EPI", 16) != 16 ? launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s)
-                : res_hit(a.sparse != 0) ? launch_res<2, 256, 16, 2>(mx, mxb, ma, mbb, a, s)
-                                                     : launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s);
-        else
+        else if (cg == 1)
             e = launch_res<1, 256, 8>(mx, mxb, ma, mbb, a, s);
+        else if (FASTED_KNOB("FASTED_RES_EPI", 16) != 16)
+            e = launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
+        else
+#endif
+            e = res_hit(a.sparse != 0) ? launch_res<2, 256, 16, 2>(mx, mxb, ma, mbb, a, s)
+                                       : launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s);
         if (e == cudaSuccess) e = cudaGetLastError();
         cudaFreeAsync(aug, s);
         if (e != cudaSuccess) return cuda_status(e, "join_tc_res_kernel");
         return FASTED_OK;
     }
-    // Large d: B-multicast clusters unless FASTED_MC=0 (or a CTA group is forced).
+    // d_pad > 512: B-multicast clusters of single-CTA MMAs, 16 epilogue warps
+    // of 64 columns (alternating runs against 8 of 128: 60K x 512 2.63-2.67
+    // vs 2.94-3.55 ms; 1M x 960 1406-1431 vs 1506-1515 ms; 5M x 384 shard at
+    // S ~ 4000 2535 vs 3140 ms, profiles/round1/tune_mepi_session2.txt).
     if (variant == TC_MULTICAST) {
-        // 16 epilogue warps of 64 columns (FASTED_MC_EPI=8: 8 of 128).  Measured,
-        // alternating runs: 60K x 512 2.63-2.67 vs 2.94-3.55 ms; 1M x 960
-        // 1406-1431 vs 1506-1515 ms; 5M x 384 shard at S ~ 4000 2535 vs 3140 ms
-        // (profiles/round1/tune_mepi_session2.txt)
-        e = env_int("FASTED_MC_EPI", 16) == 8 ? launch_mc<8>(mx, ma, mb, a, s)
-            : mc_hit(a.sparse != 0) ? launch_mc<16, 2>(mx, ma, mb, a, s)
-                                               : launch_mc<16>(mx, ma, mb, a, s);
+#ifdef FASTED_EXPERIMENTS
+        if (FASTED_KNOB("FASTED_MC_EPI", 16) == 8)
+            e = launch_mc<8>(mx, ma, mb, a, s);
+        else
+#endif
+            e = mc_hit(a.sparse != 0) ? launch_mc<16, 2>(mx, ma, mb, a, s)
+                                      : launch_mc<16>(mx, ma, mb, a, s);
         if (e == cudaSuccess) e = cudaGetLastError();
         cudaFreeAsync(aug, s);
         if (e != cudaSuccess) return cuda_status(e, "join_tc_mc_kernel");
@@ -2679,24 +2664,26 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     const int tile_m = BM * cg;
     sch.row_tiles = (int)((a.row_end - a.row_begin + tile_m - 1) / tile_m);
     sch.col_tiles = (int)((a.col_end - a.col_begin + BN - 1) / BN);
-    // grouped raster: GROUP row tiles (default 8192 rows) sweep all columns
-    // (2048 rows measured best for the single-CTA form at 1M x 960: 0.82 vs
-    // 0.93 pJ/flop for 8192)
-    // (CTA pair: 16384 rows -- 1376 TFLOPS vs 1331 for 8192, 1031 for 2048
-    // and 1246 for 32768 at 1M x 960; profiles/round1/tune_c4_cg2b_session2.txt)
-    sch.group = env_int("FASTED_GROUP_ROWS", cg == 2 ? 16384 : 2048) / tile_m;
+    // grouped raster: GROUP row tiles sweep all columns.  CTA pair: 16384
+    // rows -- 1376 TFLOPS vs 1331 for 8192, 1031 for 2048 and 1246 for 32768
+    // at 1M x 960 (profiles/round1/tune_c4_cg2b_session2.txt); single CTA
+    // (libfasted_exp.so only): 2048 rows, 0.82 vs 0.93 pJ/flop for 8192.
+    sch.group = FASTED_KNOB("FASTED_GROUP_ROWS", cg == 2 ? 16384 : 2048) / tile_m;
     if (sch.group < 1) sch.group = 1;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.total = (int64_t)sch.row_tiles * sch.col_tiles;
-    // CTA pair: 16 epilogue warps of 64 columns (FASTED_STREAM_EPI=8: 8 of
-    // 128).  1M x 960: 1466-1472 vs 1450-1491 TFLOPS (even); 5M x 384 shard
-    // at S <= 64: 1917-1946 vs 2060-2253 ms (profiles/round1/tune_sepi_session2.txt)
-    if (cg == 2)
-        e = env_int("FASTED_STREAM_EPI", 16) == 8 ? launch_variant<2>(mx, ma, mb, a, sch, s)
-            : stream_hit(a.sparse != 0) ? launch_variant<2, false, 16, 2>(mx, ma, mb, a, sch, s)
-                                                   : launch_variant<2, false, 16>(mx, ma, mb, a, sch, s);
-    else
+    // CTA pair: 16 epilogue warps of 64 columns (8 of 128: 1M x 960
+    // 1466-1472 vs 1450-1491 TFLOPS, even; 5M x 384 shard at S <= 64:
+    // 1917-1946 vs 2060-2253 ms, profiles/round1/tune_sepi_session2.txt)
+#ifdef FASTED_EXPERIMENTS
+    if (cg == 1)
         e = launch_variant<1>(mx, ma, mb, a, sch, s);
+    else if (FASTED_KNOB("FASTED_STREAM_EPI", 16) == 8)
+        e = launch_variant<2>(mx, ma, mb, a, sch, s);
+    else
+#endif
+        e = stream_hit(a.sparse != 0) ? launch_variant<2, false, 16, 2>(mx, ma, mb, a, sch, s)
+                                      : launch_variant<2, false, 16>(mx, ma, mb, a, sch, s);
     if (e == cudaSuccess) e = cudaGetLastError();
     cudaFreeAsync(aug, s);
     if (e != cudaSuccess) return cuda_status(e, "join_tc_kernel");

@@ -67,13 +67,16 @@ class Dataset:
 class HalfDataset:
     """Zero-padded FP16 working copy plus FP32 RZ squared norms
     (dataset.py:65-86).  ``device_cache`` maps a CUDA device index to the
-    resident (values, norms) tensors; it never takes part in equality."""
+    resident (values, norms) tensors; ``count_memo`` holds the engine's last
+    exact pair count per (epsilon, range, kernel) so repeated joins of this
+    dataset size their buffers once.  Neither takes part in equality."""
 
     n_logical: int
     d_logical: int
     values: np.ndarray  # (n_padded, d_padded) float16
     norms: np.ndarray   # (n_padded,) float32
     device_cache: dict = field(default_factory=dict, compare=False, repr=False)
+    count_memo: dict = field(default_factory=dict, compare=False, repr=False)
 
     @property
     def n_padded(self) -> int:

@@ -21,28 +21,57 @@ def shard_rows(n_padded: int, rank: int, world: int) -> tuple:
     return partition_rows(n_dev, world)[rank]
 
 
+def _device(device):
+    """Where a bookkeeping tensor must live for the process group's backend:
+    NCCL reduces only CUDA tensors (the current device), gloo CPU ones."""
+    import torch
+    import torch.distributed as dist
+
+    if device is not None:
+        return device
+    if dist.get_backend() == "nccl":
+        return torch.device("cuda", torch.cuda.current_device())
+    return torch.device("cpu")
+
+
 def reduce_max(value: float, device=None) -> float:
+    """Max over ranks (the contract's timing rule: the job time is the
+    slowest rank's device time)."""
     import torch
     import torch.distributed as dist
 
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return float(value)
-    t = torch.tensor([float(value)], dtype=torch.float64,
-                     device=device if device is not None else "cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
 
 def reduce_sum(value: int, device=None) -> int:
+    """Sum over ranks (pair counts: bookkeeping, not the data path)."""
     import torch
     import torch.distributed as dist
 
     if not dist.is_initialized() or dist.get_world_size() == 1:
         return int(value)
-    t = torch.tensor([int(value)], dtype=torch.int64,
-                     device=device if device is not None else "cpu")
+    t = torch.tensor([int(value)], dtype=torch.int64, device=_device(device))
     dist.all_reduce(t)
     return int(t.item())
+
+
+def barrier() -> None:
+    """Process-group barrier (no-op without one) followed by a device sync
+    when CUDA is in use -- the bracket around every timed region."""
+    import torch
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_world_size() > 1:
+        if dist.get_backend() == "nccl":
+            dist.barrier(device_ids=[torch.cuda.current_device()])
+        else:
+            dist.barrier()
+    if torch.cuda.is_available() and torch.cuda.is_initialized():
+        torch.cuda.synchronize()
 
 
 def merge_shards(parts) -> tuple:
@@ -59,7 +88,9 @@ def merge_shards(parts) -> tuple:
 
 def gather_shards(local, dst: int = 0):
     """Gather every rank's (i, j, d) to `dst` (host objects over the process
-    group); returns the merged arrays on dst, None elsewhere."""
+    group: gather_object pickles through the backend -- CPU tensors on gloo,
+    the current CUDA device on NCCL); returns the merged arrays on dst, None
+    elsewhere."""
     import torch.distributed as dist
 
     if not dist.is_initialized() or dist.get_world_size() == 1:

@@ -19,7 +19,7 @@ from __future__ import annotations
 import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 
@@ -42,9 +42,19 @@ class DeviceData:
     # upload_segmented: [(row_end, cuda event)] ascending -- rows [0, row_end)
     # are resident once the event completed (None: resident on the stream)
     ready: "object" = None
-    # identity of the host dataset this copy came from (keys the count memo:
-    # a fresh device copy per call must still find the last exact count)
-    source: int = 0
+    # the host dataset's count memo (HalfDataset.count_memo): a fresh device
+    # copy per call still finds the last exact count; a DeviceData made
+    # without a HalfDataset keeps its own
+    memo: dict = field(default_factory=dict)
+    # (start, end) timing events around the H2D copy (None: no copy made)
+    h2d: "object" = None
+
+    def h2d_ms(self) -> float:
+        """Device time of the upload (waits for it; 0 if nothing was copied)."""
+        if self.h2d is None:
+            return 0.0
+        _poll(self.h2d[1])
+        return self.h2d[0].elapsed_time(self.h2d[1])
 
     def wait_rows(self, stream, row_end: int) -> None:
         """Make `stream` wait until rows [0, row_end) are resident."""
@@ -104,20 +114,25 @@ def upload(hd, device: int) -> DeviceData:
     cached = hd.device_cache.get(device) if hasattr(hd, "device_cache") else None
     if cached is not None and tuple(cached[0].shape) == (n_pad, d_pad) and n_dev == n_pad:
         return DeviceData(device, cached[0], cached[1], hd.n_logical, n_dev, d_pad,
-                          source=id(hd.values))
+                          memo=_memo_of(hd))
     dev = f"cuda:{device}"
     with torch.cuda.device(device):
         hv = torch.from_numpy(np.ascontiguousarray(hd.values))
         hn = torch.from_numpy(np.ascontiguousarray(hd.norms, dtype=np.float32))
+        cur = torch.cuda.current_stream()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if n_dev == n_pad:
-            values = hv.to(dev, non_blocking=True)
-            norms = hn.to(dev, non_blocking=True)
+            values = torch.empty((n_dev, d_pad), dtype=torch.float16, device=dev)
+            norms = torch.empty(n_dev, dtype=torch.float32, device=dev)
         else:
             values = torch.zeros((n_dev, d_pad), dtype=torch.float16, device=dev)
             norms = torch.zeros(n_dev, dtype=torch.float32, device=dev)
-            values[:n_pad].copy_(hv, non_blocking=True)
-            norms[:n_pad].copy_(hn, non_blocking=True)
-    return DeviceData(device, values, norms, hd.n_logical, n_dev, d_pad, source=id(hd.values))
+        t0.record(cur)
+        values[:n_pad].copy_(hv, non_blocking=True)
+        norms[:n_pad].copy_(hn, non_blocking=True)
+        t1.record(cur)
+    return DeviceData(device, values, norms, hd.n_logical, n_dev, d_pad, memo=_memo_of(hd),
+                      h2d=(t0, t1))
 
 
 SEGMENT_MIN_BYTES = 256 << 20   # datasets below this upload in one piece
@@ -151,13 +166,15 @@ def upload_segmented(hd, device: int, segments: int = UPLOAD_SEGMENTS) -> Device
         blocks = n_dev // BLOCK
         bounds = [BLOCK * (blocks * k // segments) for k in range(segments + 1)]
         ready = []
+        t0 = torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(copy):
+            t0.record(copy)
             for a, b in zip(bounds[:-1], bounds[1:]):
                 if b <= a:
                     continue
                 values[a:b].copy_(hv[a:b], non_blocking=True)
                 norms[a:b].copy_(hn[a:b], non_blocking=True)
-                ev = torch.cuda.Event()
+                ev = torch.cuda.Event(enable_timing=True)
                 ev.record(copy)
                 ready.append((b, ev))
         # the tensors were produced on `copy`: keep the allocator from reusing
@@ -165,7 +182,7 @@ def upload_segmented(hd, device: int, segments: int = UPLOAD_SEGMENTS) -> Device
         values.record_stream(copy)
         norms.record_stream(copy)
     return DeviceData(device, values, norms, hd.n_logical, n_dev, d_pad, ready,
-                      source=id(hd.values))
+                      memo=_memo_of(hd), h2d=(t0, ready[-1][1]))
 
 
 def column_segments(dd: DeviceData, cols, first_rows_end: int) -> list:
@@ -217,23 +234,45 @@ def read_counts(cnt, stream=None) -> list:
     return [int(v) for v in host.tolist()]
 
 
-# Last exact count per problem, so repeated joins size their buffers once.
-_count_memo: dict = {}
+# Last exact count per problem (kept on the dataset, HalfDataset.count_memo),
+# so repeated joins size their buffers once.
 _memo_lock = threading.Lock()
+MEMO_MAX = 64
+
+
+def _memo_of(hd) -> dict:
+    memo = getattr(hd, "count_memo", None)
+    return memo if memo is not None else {}
+
+
+def _memo_get(dd: DeviceData, key):
+    with _memo_lock:
+        return dd.memo.get(key)
+
+
+def _memo_put(dd: DeviceData, key, count: int) -> None:
+    with _memo_lock:
+        if key not in dd.memo and len(dd.memo) >= MEMO_MAX:
+            dd.memo.clear()
+        dd.memo[key] = int(count)
 
 
 def join_raw(dd: DeviceData, eps_sq: float, flags: int, rows, cols, records, capacity: int,
-             count, stream) -> None:
-    """One fasted_join launch (results stay on the device)."""
-    st = _lib.load().fasted_join(dd.values.data_ptr(), dd.norms.data_ptr(), dd.n_logical,
+             count, stream, lib=None) -> None:
+    """One fasted_join launch (results stay on the device).  `lib`: the
+    library to call (default libfasted.so; the bit-identity tests pass
+    _lib.load_experimental() to force other kernel forms)."""
+    L = lib if lib is not None else _lib.load()
+    st = L.fasted_join(dd.values.data_ptr(), dd.norms.data_ptr(), dd.n_logical,
                                  dd.n_dev, dd.d_pad, rows[0], rows[1], cols[0], cols[1],
                                  float(eps_sq), flags,
                                  records.data_ptr() if records is not None else None,
                                  capacity, count.data_ptr(), stream)
-    _lib.check(st, "fasted_join")
+    _lib.check(st, "fasted_join", L)
 
 
-def _estimate_capacity(dd: DeviceData, eps_sq: float, rows, cols, flags: int, stream) -> int:
+def _estimate_capacity(dd: DeviceData, eps_sq: float, rows, cols, flags: int, stream,
+                       lib=None) -> int:
     """Count-only join on a few evenly spaced row blocks -> capacity guess."""
     import torch
 
@@ -246,7 +285,7 @@ def _estimate_capacity(dd: DeviceData, eps_sq: float, rows, cols, flags: int, st
     for s in range(samples):   # the sample blocks append into one count: one readback
         b = r0 + (nblk * s // samples) * BLOCK
         join_raw(dd, eps_sq, flags | _lib.JOIN_COUNT | (_lib.JOIN_APPEND if s else 0),
-                 (b, b + BLOCK), cols, None, 0, cnt, stream)
+                 (b, b + BLOCK), cols, None, 0, cnt, stream, lib)
     tot = read_counts(cnt)[0]
     return int(tot * nblk / samples * 1.25) + 65536
 
@@ -294,27 +333,29 @@ def _sort_records(dd: DeviceData, rec, slots: int, count: int, rows, stream, out
 
 
 def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool = False,
-                capacity: int | None = None, sort: bool = True) -> DeviceResult:
+                capacity: int | None = None, sort: bool = True, flags: int = 0,
+                lib=None) -> DeviceResult:
     """Run the join for rows x cols on dd.device; results stay on the device.
-    With sort=False the raw 16-byte records are returned (res.records)."""
+    With sort=False the raw 16-byte records are returned (res.records).
+    `flags`: extra fasted_join flags (e.g. _lib.JOIN_SYMMETRIC); `lib`: see
+    join_raw."""
     import torch
 
     L = _lib.load()
     rows = rows or (0, dd.n_dev)
     cols = cols or (0, dd.n_dev)
-    flags = _lib.JOIN_EXACT if exact else _lib.JOIN_TC
+    flags |= _lib.JOIN_EXACT if exact else _lib.JOIN_TC
     dev = f"cuda:{dd.device}"
     with torch.cuda.device(dd.device):
         stream = torch.cuda.current_stream()
         sp = stream.cuda_stream
-        key = (dd.n_dev, dd.d_pad, dd.n_logical, float(eps_sq), rows, cols, flags,
-               dd.source or dd.values.data_ptr())
+        key = (dd.n_dev, dd.d_pad, dd.n_logical, float(eps_sq), tuple(rows), tuple(cols), flags)
         slack = hole_slack(dd.device)
         if capacity is None:
-            with _memo_lock:
-                capacity = _count_memo.get(key)
+            capacity = _memo_get(dd, key)
             if capacity is None:
-                capacity = _estimate_capacity(dd, eps_sq, rows, cols, flags, sp)
+                capacity = _estimate_capacity(dd, eps_sq, rows, cols,
+                                              flags & ~_lib.JOIN_SYMMETRIC, sp, lib)
             capacity += slack
         if not exact:
             flags |= form_hints(capacity - slack, rows, cols)   # kernel-form hints only
@@ -327,7 +368,7 @@ def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            join_raw(dd, eps_sq, flags, rows, cols, rec, cap, cnt, sp)
+            join_raw(dd, eps_sq, flags, rows, cols, rec, cap, cnt, sp, lib)
             e1.record(stream)
             count, chunks = read_counts(cnt, stream)
             slots = chunks * RECORD_CHUNK
@@ -336,8 +377,7 @@ def join_device(dd: DeviceData, eps_sq: float, rows=None, cols=None, exact: bool
                 break
             capacity = count + slack
             reruns += 1
-        with _memo_lock:
-            _count_memo[key] = count
+        _memo_put(dd, key, count)
         rec = rec[:slots]
         if not sort:
             return DeviceResult(None, None, None, count, kernel_ms, 0.0, reruns, slots, rec)
@@ -377,6 +417,7 @@ class HostPairs:
         self.cap = 0
         self.n = 0
         self.trace = None
+        self.d2h_ms = 0.0
         self._alloc(max(int(capacity), 1))
 
     def _alloc(self, cap):
@@ -487,12 +528,10 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
         comp = torch.cuda.current_stream()
         copy = torch.cuda.Stream(dd.device)
         sp = comp.cuda_stream
-        key = (dd.n_dev, dd.d_pad, dd.n_logical, float(eps_sq), rows, cols, flags,
-               dd.source or dd.values.data_ptr())
+        key = (dd.n_dev, dd.d_pad, dd.n_logical, float(eps_sq), tuple(rows), tuple(cols), flags)
         tr = {"estimate": 0.0, "reserve": 0.0, "wait_join": 0.0, "enqueue": 0.0, "drain": 0.0}
         tc0 = time.perf_counter()
-        with _memo_lock:
-            est = _count_memo.get(key)
+        est = _memo_get(dd, key)
         if est is None:
             dd.wait_rows(comp, dd.n_dev)
             est = _estimate_capacity(dd, eps_sq, rows, cols, flags, sp)
@@ -554,6 +593,7 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
         total = 0
         tj = [None, None]
         sort_ev = []
+        d2h_ev = []
         join_ev = []
         cnt_evs = []
 
@@ -651,10 +691,13 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
             host.reserve(count, sync_streams=(copy,))
             tr["reserve"] += time.perf_counter() - tc0
             copy.wait_event(s1)
+            h0 = torch.cuda.Event(enable_timing=True)
+            h0.record(copy)
             host.append_async(out[0], out[1], out[2], count, copy)
-            ev = torch.cuda.Event()
+            ev = torch.cuda.Event(enable_timing=True)
             ev.record(copy)
             d2h_done[b] = ev
+            d2h_ev.append((h0, ev))
             mark("d2h%d" % c)
             total += count
             # join c+2 reuses chunk c's record buffer: queued after sort c
@@ -669,6 +712,7 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
             dd.ready = None            # resident from here on
         tr["drain"] = time.perf_counter() - tc0
         sort_ms = sum(a.elapsed_time(b) for a, b in sort_ev)
+        host.d2h_ms = sum(a.elapsed_time(b) for a, b in d2h_ev)
         host.trace = {k: round(v * 1e3, 2) for k, v in tr.items()}
         host.trace["host_marks"] = marks
         if join_ev:   # GPU timeline (ms from the first join start): gaps = GPU idle
@@ -679,18 +723,19 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
                 [("sort%d" % c, round(t0e.elapsed_time(a), 2), round(t0e.elapsed_time(b), 2))
                  for c, (a, b) in enumerate(sort_ev)] +
                 [("count%d" % c, round(t0e.elapsed_time(e), 2)) for c, e in cnt_evs])
-        with _memo_lock:
-            _count_memo[key] = total
+        _memo_put(dd, key, total)
     return kernel_ms, sort_ms, reruns, len(chunks)
 
 
 @dataclass
 class JoinReport:
-    kernel_seconds: float      # max over devices of the join kernel time
+    kernel_seconds: float      # max over devices of the join kernel time (CUDA events)
     merge_seconds: float       # pipeline time not hidden behind the join (sort + D2H tail)
-    stage_seconds: float       # H2D upload
+    stage_seconds: float       # H2D upload, device time (CUDA events on the copy stream)
     wall_seconds: float
     per_device: list
+    sort_seconds: float = 0.0  # max over devices of the device sort time
+    d2h_seconds: float = 0.0   # max over devices of the result D2H device time
 
 
 def self_join_devices(hd, eps_sq: float, devices, exact: bool = False, row_range=None,
@@ -715,13 +760,12 @@ def self_join_devices(hd, eps_sq: float, devices, exact: bool = False, row_range
             dd = upload_segmented(hd, dev)
             if dd.ready is None:
                 _poll_stream(torch.cuda.current_stream())
-            t_up = time.perf_counter() - t0
             t1 = time.perf_counter()
             host = HostPairs(1)
             kms, sms, reruns, nch = stream_join(dd, eps_sq, parts[g], exact, host,
                                                 symmetric=symmetric)
             t_all = time.perf_counter() - t1
-            return host, (kms, sms, reruns, nch), t_up, t_all
+            return host, (kms, sms, reruns, nch), dd.h2d_ms() / 1e3, t_all
 
     if len(devices) == 1:
         results = [run(0)]
@@ -751,7 +795,10 @@ def self_join_devices(hd, eps_sq: float, devices, exact: bool = False, row_range
         merge_seconds=max(r[3] - r[1][0] / 1e3 for r in results),
         stage_seconds=max(r[2] for r in results),
         wall_seconds=time.perf_counter() - t_start,
+        sort_seconds=max(r[1][1] for r in results) / 1e3,
+        d2h_seconds=max(r[0].d2h_ms for r in results) / 1e3,
         per_device=[{"device": devices[g], "rows": parts[g], "pairs": results[g][0].n,
+                     "h2d_ms": results[g][2] * 1e3, "d2h_ms": results[g][0].d2h_ms,
                      "kernel_ms": results[g][1][0], "sort_ms": results[g][1][1],
                      "reruns": results[g][1][2], "chunks": results[g][1][3],
                      "host_ms": getattr(results[g][0], "trace", None)}

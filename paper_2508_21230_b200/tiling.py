@@ -173,9 +173,20 @@ def _check_engine_inputs(hd: HalfDataset, cfg: TileConfig) -> None:
         raise ConfigError(f"d_padded {hd.d_padded} not a multiple of warp_kslice {cfg.warp_kslice}")
 
 
+FLT_MAX = np.float32(np.finfo(np.float32).max)
+
+
 def _eps_sq(epsilon) -> np.float32:
-    eps32 = np.float32(epsilon)
-    return np.float32(eps32 * eps32)   # tiling.py:304-305
+    """eps32 = f32(eps); eps_sq = f32(eps32 * eps32) (tiling.py:304-305).
+
+    Where the reference's square overflows to inf (eps above ~1.8e19, or an
+    eps that is itself beyond FP32 range) every finite dist_sq is <= inf, so
+    it returns all n^2 pairs; clamping to FLT_MAX selects the same set and
+    keeps the C ABI's finite-eps_sq contract."""
+    with np.errstate(over="ignore"):
+        eps32 = np.float32(epsilon)
+        es = np.float32(eps32 * eps32)
+    return es if es <= FLT_MAX else FLT_MAX
 
 
 def _default_devices():

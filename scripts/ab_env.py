@@ -15,6 +15,8 @@ import torch  # noqa: E402
 import paper_2508_21230_b200 as F  # noqa: E402
 from bench import SEED, WORKLOADS  # noqa: E402
 from paper_2508_21230_b200 import _lib, engine  # noqa: E402
+# env knobs and diagnostic flags exist only in the experiment build
+_lib.LIB_PATH = os.path.abspath(os.environ.get("FASTED_LIB", _lib.EXP_LIB_PATH))
 
 wl, rounds = sys.argv[1], int(sys.argv[2])
 settings = sys.argv[3:]

@@ -26,9 +26,9 @@ import torch  # noqa: E402
 import paper_2508_21230_b200 as F  # noqa: E402
 from bench import SEED, ClockSampler, load_peaks  # noqa: E402
 from paper_2508_21230_b200 import _lib, engine  # noqa: E402
+# env knobs and diagnostic flags exist only in the experiment build
+_lib.LIB_PATH = os.path.abspath(os.environ.get("FASTED_LIB", _lib.EXP_LIB_PATH))
 
-if os.environ.get("FASTED_LIB"):   # A/B against another build of the library
-    _lib.LIB_PATH = os.path.abspath(os.environ["FASTED_LIB"])
 
 # eps per target selectivity (reference CLI calibrate, sample 4096)
 SWEEP = [("S0 (self pairs only)", 0.0), ("S16", 6.896041752764515), ("S64", 6.97276473038035),

@@ -14,6 +14,8 @@ import torch  # noqa: E402
 import paper_2508_21230_b200 as F  # noqa: E402
 from bench import SEED, WORKLOADS  # noqa: E402
 from paper_2508_21230_b200 import _lib, engine  # noqa: E402
+# env knobs and diagnostic flags exist only in the experiment build
+_lib.LIB_PATH = os.path.abspath(os.environ.get("FASTED_LIB", _lib.EXP_LIB_PATH))
 
 name, n, d, eps = WORKLOADS["C4"]
 hd = F.to_half(F.generate_synthetic(n, d, seed=SEED))

@@ -79,6 +79,31 @@ def test_to_half_large_matches_oracle(oracle):
     assert np.array_equal(hd.norms, norms)
 
 
+@pytest.mark.parametrize("n,d", [(1000, 64), (777, 100), (130, 8), (300, 1024), (5, 4),
+                                 (2000, 384), (129, 4100)])
+def test_quantize_tma_path_matches_oracle(oracle, n, d):
+    """The TMA-streamed quantise kernel (d % 4 == 0): FP16 bits and RZ norms
+    equal the oracle's for ragged n, d_pad not a multiple of the 32-column
+    box, wide rows and a tiny matrix; the first overflow is reported by flat
+    index (RangeError names the lowest point/dimension)."""
+    rng = np.random.default_rng(n * 7 + d)
+    x = (rng.standard_normal((n, d)) * 50).astype(np.float32)
+    x[0, 0] = 1e-6
+    x[min(3, n - 1), d // 2] = -65504.0
+    hd = F.to_half(F.Dataset(x))
+    v16, norms, _ = oracle.to_half(x)
+    assert np.array_equal(hd.values.view(np.uint16), v16.view(np.uint16))
+    assert np.array_equal(hd.norms, norms)
+    y = x.copy()
+    y[n - 1, d - 1] = 70000.0
+    if n > 2:
+        y[n // 2, min(3, d - 1)] = -1e6
+    with pytest.raises(F.RangeError) as e:
+        F.to_half(F.Dataset(y))
+    i, k = (n // 2, min(3, d - 1)) if n > 2 else (n - 1, d - 1)
+    assert f"of point {i} (dimension {k})" in str(e.value)
+
+
 # ── exact kernel: bit parity ─────────────────────────────────────────────
 
 
@@ -142,9 +167,18 @@ def test_sampled_tiles_exact_and_tc(golden, golden_meta, oracle):
             ti, tj, td, hd = _panel_join(rec["n"], rec["d"], rec["seed"], rec["epsilon"], rb, cb,
                                          False)
             es = float(oracle.eps_sq_of(rec["epsilon"]))
+
+            def ref_d2(a, b, hd=hd, rb=rb, cb=cb):
+                # reference dist_sq of TC extras, from the two-panel dataset
+                # (row block rb = panel rows 1..128, column block cb = 129..256)
+                la = np.asarray(a, np.int64) - rb * 128
+                lb = np.asarray(b, np.int64) - cb * 128 + 128
+                return oracle.pair_d2(hd.values, hd.norms, la.astype(np.uint32),
+                                      lb.astype(np.uint32))
+
             rep = F.band_compare(ti, tj, td, golden[key + "_i"], golden[key + "_j"],
-                                 golden[key + "_d"], es, lambda a, b: np.full(len(a), np.inf))
-            assert rep.missing_out_of_band == 0, (key, rep)
+                                 golden[key + "_d"], es, ref_d2)
+            assert rep.ok, (key, rep)
 
 
 # ── tcgen05 kernel: band parity ──────────────────────────────────────────
@@ -200,6 +234,39 @@ def test_duplicates_eps_zero(golden):
     # reference (whose a_ij and s_i are the same RZ chain)
     assert tc.index_pairs() == rs.index_pairs()
     assert not tc.dist_sq.any()
+
+
+def test_large_eps_duplicates_and_dist_error():
+    """eps^2 >> the squared norms (points in a 0.01-wide cube, eps = 10):
+    every pair qualifies, exact duplicates i != j come out at distance 0 as
+    in the reference (the augment rows carry eps^2/2 + sigma_j exactly,
+    TwoSum), and the dist_sq error of the D = (eps^2 - d2)/2 form stays
+    within a few ulp of eps^2."""
+    rng = np.random.default_rng(4)
+    x = (rng.random((600, 48)) * 0.01).astype(np.float32)
+    x[300:350] = x[0:50]                  # 50 exact duplicate pairs (both orders)
+    hd = F.to_half(F.Dataset(x))
+    ref = F.self_join(hd, 10.0, mode="exact")
+    tc = F.self_join(hd, 10.0)
+    assert len(ref) == len(tc) == 600 * 600
+    assert tc.same_pairs(ref)
+    dup = (np.abs(tc.i.astype(np.int64) - tc.j.astype(np.int64)) == 300) & \
+        (np.minimum(tc.i, tc.j) <= 50)
+    assert dup.sum() == 100
+    assert not tc.dist_sq[dup].any(), tc.dist_sq[dup].max()
+    ulp = np.spacing(np.float32(100.0))
+    err = np.abs(tc.dist_sq.astype(np.float64) - ref.dist_sq.astype(np.float64))
+    assert err.max() <= 4 * ulp, err.max() / ulp
+
+
+def test_eps_beyond_fp32_square_returns_all_pairs():
+    """An epsilon whose FP32 square overflows (the reference's eps_sq = inf)
+    selects every pair, as the reference does: eps_sq clamps to FLT_MAX."""
+    hd = F.to_half(F.generate_synthetic(300, 16, seed=2))
+    for eps in (2e19, 1e39):
+        rs = F.self_join(hd, eps)
+        assert len(rs) == 300 * 300
+        assert len(F.self_join(hd, eps, mode="exact")) == 300 * 300
 
 
 def test_c1_tc_vs_reference(golden_meta, oracle):
@@ -273,6 +340,28 @@ def test_invalid_arguments_raise():
         F.compute_block_tile(hd, F.TileCoord(5, 0), 1.0, F.TileConfig())
 
 
+def _exact_and_tc_vs_oracle_blocks(oracle, hd, n, eps, ref, rs, blocks=16):
+    """On `blocks` random 128-row blocks (plus the first and the last) at the
+    full column range: the exact kernel's records equal the C oracle's bit
+    for bit, and the tcgen05 records meet the band contract against the
+    oracle directly."""
+    nblk = -(-n // 128)
+    rng = np.random.default_rng(n + hd.d_padded)
+    picks = sorted({0, nblk - 1} | set(rng.choice(nblk, blocks, replace=False).tolist()))
+    es = float(oracle.eps_sq_of(eps))
+    for rb in picks:
+        lo, hi = rb * 128, min(rb * 128 + 128, n)
+        oi, oj, od = oracle.join(hd.values, hd.norms, n, eps, rows=(lo, hi))
+        sel = (ref.i > lo) & (ref.i <= hi)
+        assert np.array_equal(oi, ref.i[sel]) and np.array_equal(oj, ref.j[sel]), rb
+        assert np.array_equal(od.view(np.uint32), ref.dist_sq[sel].view(np.uint32)), rb
+        tsel = (rs.i > lo) & (rs.i <= hi)
+        rep = F.band_compare(rs.i[tsel], rs.j[tsel], rs.dist_sq[tsel], oi, oj, od, es,
+                             lambda i, j: oracle.pair_d2(hd.values, hd.norms, i, j))
+        assert rep.ok, (rb, rep)
+    return picks
+
+
 @pytest.mark.slow
 def test_c3_full_size_tc_vs_exact(oracle):
     """1M x 128 (C3): full tcgen05 join against the bit-exact kernel (itself
@@ -285,12 +374,7 @@ def test_c3_full_size_tc_vs_exact(oracle):
     rep = _band_ok(oracle, hd, rs, ref.i, ref.j, ref.dist_sq, eps)
     print("C3 band report:", rep)
     assert rep.ok, rep
-    # exact kernel == oracle on two row blocks at full column range
-    for rb in (0, 5000):
-        oi, oj, od = oracle.join(hd.values, hd.norms, n, eps, rows=(rb * 128, rb * 128 + 128))
-        sel = (ref.i > rb * 128) & (ref.i <= rb * 128 + 128)
-        assert np.array_equal(oi, ref.i[sel]) and np.array_equal(oj, ref.j[sel])
-        assert np.array_equal(od.view(np.uint32), ref.dist_sq[sel].view(np.uint32))
+    _exact_and_tc_vs_oracle_blocks(oracle, hd, n, eps, ref, rs)
     assert es > 0
 
 
@@ -326,20 +410,94 @@ def test_sort_pairs_random_records(n_rows, maxc):
     assert np.array_equal(od.cpu().numpy(), d[order])
 
 
-def _tc_variant(hd, eps, rows=None, cols=None, **env):
-    """One tcgen05 join with kernel-selection env knobs (read per launch)."""
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update({k: str(v) for k, v in env.items()})
-    try:
-        dd = engine.upload(hd, 0)
-        es = float(np.float32(np.float32(eps) ** 2))
-        return engine.to_host(engine.join_device(dd, es, rows=rows, cols=cols))
-    finally:
-        for k, v in old.items():
+class _env:
+    """Temporarily set libfasted_exp.so's kernel-form overrides (read per launch)."""
+
+    def __init__(self, **env):
+        self.env = {k: str(v) for k, v in env.items()}
+
+    def __enter__(self):
+        self.old = {k: os.environ.get(k) for k in self.env}
+        os.environ.update(self.env)
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
             if v is None:
                 os.environ.pop(k, None)
             else:
                 os.environ[k] = v
+
+
+def _tc_variant(hd, eps, rows=None, cols=None, flags=0, **env):
+    """One tcgen05 join through libfasted_exp.so with kernel-form overrides
+    (the product library reads no environment: test_product_library_* pins
+    its records to these)."""
+    with _env(**env):
+        dd = engine.upload(hd, 0)
+        es = float(np.float32(np.float32(eps) ** 2))
+        return engine.to_host(engine.join_device(dd, es, rows=rows, cols=cols, flags=flags,
+                                                 lib=_lib.load_experimental()))
+
+
+def _same(a, b):
+    return all(np.array_equal(np.asarray(x).view(np.uint32), np.asarray(y).view(np.uint32))
+               for x, y in zip(a, b))
+
+
+@pytest.mark.parametrize("n,d,eps", [(3000, 128, 3.7), (2999, 100, 3.3), (2000, 512, 8.6),
+                                     (1500, 384, 7.7), (3000, 520, 8.5), (1100, 960, 12.0)])
+def test_product_library_matches_experiment_forms(n, d, eps):
+    """libfasted.so (no environment, no diagnostic flags) gives exactly the
+    records of libfasted_exp.so's reference forms -- the streaming kernel
+    with one CTA (resident-A at d <= 512 is the same MMA chain) -- with and
+    without the SPARSE hint (hit warps) and on a ragged shard range; so every
+    bit-identity test below, run on the experiment build, pins the product."""
+    hd = F.to_half(F.generate_synthetic(n, d, seed=n + 11 * d))
+    ref = _tc_variant(hd, eps, FASTED_CTA_GROUP=1, FASTED_RESIDENT=0)
+    assert len(ref[0]) > n
+    dd = engine.upload(hd, 0)
+    es = float(np.float32(np.float32(eps) ** 2))
+    n_dev = dd.n_dev
+    for hint in (0, _lib.JOIN_SPARSE, _lib.JOIN_LOW_OUTPUT):
+        got = engine.to_host(engine.join_device(dd, es, flags=hint))
+        assert _same(ref, got), hint
+    rows, cols = (128, min(n_dev, 1152)), (256, n_dev)
+    ref = _tc_variant(hd, eps, rows, cols, FASTED_CTA_GROUP=1, FASTED_RESIDENT=0)
+    got = engine.to_host(engine.join_device(dd, es, rows=rows, cols=cols))
+    assert _same(ref, got)
+
+
+def test_product_cta_pair_form_matches_single_cta_at_scale():
+    """The product's streaming CTA-pair form is chosen only for >= 2^36
+    examined pairs with the LOW_OUTPUT hint: run it at that size (256K x 576)
+    and compare with libfasted_exp.so's single-CTA streaming kernel."""
+    n, d = 262144, 576
+    hd = F.to_half(F.generate_synthetic(n, d, seed=3))
+    cal = F.calibrate_epsilon_device(hd, 4.0, sample_blocks=8)
+    L = _lib.load()
+    name = L.fasted_join_kernel_name(hd.d_padded, n, n, _lib.JOIN_LOW_OUTPUT).decode()
+    assert "join_tc_kernel<2>" in name, name
+    dd = engine.upload(hd, 0)
+    es = float(np.float32(np.float32(cal.epsilon) ** 2))
+    ref = _tc_variant(hd, cal.epsilon, FASTED_CTA_GROUP=1)
+    assert len(ref[0]) > n
+    for hint in (_lib.JOIN_LOW_OUTPUT, _lib.JOIN_LOW_OUTPUT | _lib.JOIN_SPARSE):
+        got = engine.to_host(engine.join_device(dd, es, flags=hint))
+        assert _same(ref, got), hint
+
+
+def test_product_library_has_no_knobs():
+    """No environment variable reaches libfasted.so, and the diagnostic flag
+    bits are rejected there (they exist only in libfasted_exp.so)."""
+    blob = open(_lib.LIB_PATH, "rb").read()
+    assert b"FASTED_" not in blob and b"getenv" not in blob
+    hd = F.to_half(F.generate_synthetic(500, 32, seed=1))
+    dd = engine.upload(hd, 0)
+    cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+    for bad in (256, 512, 1 << 16, 1 << 20):
+        with pytest.raises(F.ArgumentError):
+            engine.join_raw(dd, 1.0, _lib.JOIN_COUNT | bad, (0, dd.n_dev), (0, dd.n_dev), None,
+                            0, cnt, torch.cuda.current_stream().cuda_stream)
 
 
 @pytest.mark.parametrize("n,d,eps,seg", [(3000, 128, 3.7, 64), (2999, 100, 3.3, 3),
@@ -376,28 +534,30 @@ def test_resident_kernel_bit_identical_to_streaming(n, d, eps, seg):
 
 @pytest.mark.parametrize("n,d,eps", [(3000, 128, 3.7), (2999, 100, 3.3), (4000, 64, 2.9),
                                      (2000, 512, 8.6), (1500, 384, 7.7)])
-def test_resident_hit_warps_symmetric_and_count(n, d, eps, monkeypatch):
+def test_resident_hit_warps_symmetric_and_count(n, d, eps):
     """Hit warps (FASTED_RES_HIT=2): the symmetric schedule and the
     count-only join give what the epilogue-warp form gives."""
     hd = F.to_half(F.generate_synthetic(n, d, seed=n * 3 + d))
     es = float(np.float32(np.float32(eps) ** 2))
     dd = engine.upload(hd, 0)
+    X = _lib.load_experimental()
     out = {}
     for hit in ("0", "2"):
-        monkeypatch.setenv("FASTED_RES_HIT", hit)
-        engine._count_memo.clear()
-        rs = F.self_join(hd, eps, symmetric=True)
-        cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
-        engine.join_raw(dd, es, _lib.JOIN_TC | _lib.JOIN_COUNT, (0, dd.n_dev), (0, dd.n_dev),
-                        None, 0, cnt, torch.cuda.current_stream().cuda_stream)
-        out[hit] = (rs, int(cnt[0]))
+        with _env(FASTED_RES_HIT=hit):
+            rs = engine.to_host(engine.join_device(dd, es, flags=_lib.JOIN_SYMMETRIC, lib=X))
+            cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
+            engine.join_raw(dd, es, _lib.JOIN_TC | _lib.JOIN_COUNT, (0, dd.n_dev),
+                            (0, dd.n_dev), None, 0, cnt, torch.cuda.current_stream().cuda_stream,
+                            X)
+            out[hit] = (rs, int(cnt[0]))
     (ra, ca), (rb, cb) = out["0"], out["2"]
     # (the full count may exceed the symmetric set by a pair whose D_ij and
     # D_ji straddle the boundary in the last bit; compare like with like)
-    assert ca == cb > n and len(ra) == len(rb) > n and abs(ca - len(ra)) <= 4
-    for x, y in zip((ra.i, ra.j, ra.dist_sq), (rb.i, rb.j, rb.dist_sq)):
-        assert np.array_equal(np.asarray(x).view(np.uint32), np.asarray(y).view(np.uint32))
-    engine._count_memo.clear()
+    assert ca == cb > n and len(ra[0]) == len(rb[0]) > n and abs(ca - len(ra[0])) <= 4
+    assert _same(ra, rb)
+    # the product library's symmetric schedule gives the same records
+    prod = F.self_join(hd, eps, symmetric=True)
+    assert _same(ra, (prod.i, prod.j, prod.dist_sq))
 
 
 @pytest.mark.parametrize("n,d,eps", [(3000, 512, 8.6), (2999, 300, 6.8), (1100, 960, 12.0),
@@ -432,7 +592,7 @@ def test_stream_join_pipeline_matches_single_shot(budget, monkeypatch):
     dd = engine.upload(hd, 0)
     es = float(np.float32(np.float32(3.2) ** 2))
     ref = engine.to_host(engine.join_device(dd, es))
-    engine._count_memo.clear()
+    dd.memo.clear()
     if budget == 3000:
         monkeypatch.setattr(engine, "_estimate_capacity", lambda *a, **k: 10)
         monkeypatch.setattr(engine, "hole_slack", lambda dev: 0)
@@ -447,7 +607,6 @@ def test_stream_join_pipeline_matches_single_shot(budget, monkeypatch):
         assert nch > 1
     if budget == 3000:
         assert reruns >= 1
-    engine._count_memo.clear()
 
 
 @pytest.mark.parametrize("exact", [False, True])
@@ -491,7 +650,7 @@ def test_segmented_upload_pipeline_matches_resident(monkeypatch):
     if hasattr(hd, "device_cache"):
         hd.device_cache.clear()
     for segments in (8, 3):
-        engine._count_memo.clear()
+        hd.count_memo.clear()
         dd = engine.upload_segmented(hd, 0, segments=segments)
         assert dd.ready is not None and len(dd.ready) == segments
         segs = engine.column_segments(dd, (0, dd.n_dev), dd.n_dev // 4 // 128 * 128)
@@ -503,7 +662,6 @@ def test_segmented_upload_pipeline_matches_resident(monkeypatch):
         got = host.arrays()
         for x, y in zip(ref, got):
             assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), segments
-    engine._count_memo.clear()
 
 
 def test_device_calibration_hits_target_on_full_data(golden_meta):
@@ -526,25 +684,21 @@ def test_device_calibration_hits_target_on_full_data(golden_meta):
 
 @pytest.mark.parametrize("n,d,eps", [(3000, 64, 2.6), (2999, 128, 3.9), (1500, 300, 6.8),
                                      (2100, 960, 12.0)])
-@pytest.mark.parametrize("env", [{}, {"FASTED_CTA_GROUP": "1"}, {"FASTED_CTA_GROUP": "2",
-                                                                  "FASTED_RESIDENT": "0"}])
+@pytest.mark.parametrize("env", [None, {"FASTED_CTA_GROUP": "1"}, {"FASTED_CTA_GROUP": "2",
+                                                                    "FASTED_RESIDENT": "0"}])
 def test_symmetric_join(oracle, n, d, eps, env):
     """FASTED_JOIN_SYMMETRIC (upper tiles + mirrored records) on every kernel
-    form: the pair set is exactly symmetric with equal dist_sq both ways,
+    form (the product library, and libfasted_exp.so's forced streaming
+    forms): the pair set is exactly symmetric with equal dist_sq both ways,
     equals the full join outside the 1e-3 band, and passes the band contract
     against the reference oracle."""
     hd = F.to_half(F.generate_synthetic(n, d, seed=n + 3 * d))
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
+    if env is None:
         full = F.self_join(hd, eps)
         sym = F.self_join(hd, eps, symmetric=True)
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
+    else:
+        full = F.make_result_set(*_tc_variant(hd, eps, **env), n, eps)
+        sym = F.make_result_set(*_tc_variant(hd, eps, flags=_lib.JOIN_SYMMETRIC, **env), n, eps)
     assert len(sym) > n
     # exact symmetry: (i, j, d) present <=> (j, i, d) present
     key = (sym.i.astype(np.uint64) << np.uint64(32)) | sym.j.astype(np.uint64)
@@ -607,11 +761,7 @@ def test_c4_full_size_tc_vs_exact(oracle):
     rep = _band_ok(oracle, hd, rs, ref.i, ref.j, ref.dist_sq, eps)
     print("C4 band report:", rep)
     assert rep.ok, rep
-    for rb in (0, 7812):
-        oi, oj, od = oracle.join(hd.values, hd.norms, n, eps, rows=(rb * 128, rb * 128 + 128))
-        sel = (ref.i > rb * 128) & (ref.i <= rb * 128 + 128)
-        assert np.array_equal(oi, ref.i[sel]) and np.array_equal(oj, ref.j[sel])
-        assert np.array_equal(od.view(np.uint32), ref.dist_sq[sel].view(np.uint32))
+    _exact_and_tc_vs_oracle_blocks(oracle, hd, n, eps, ref, rs)
 
 
 def test_cta_pair_low_output_form_matches_single_cta():
@@ -703,15 +853,7 @@ def test_tmem_a_kernel_bit_identical(n, d, eps):
     ts = _tc_variant(hd, eps, rows, cols, FASTED_TS=1, FASTED_SEG_TILES=3)
     for x, y in zip(ref, ts):
         assert np.array_equal(x.view(np.uint32), y.view(np.uint32))
-    old = os.environ.get("FASTED_TS")
-    os.environ["FASTED_TS"] = "1"
-    try:
-        sym = F.self_join(hd, eps, symmetric=True)
-    finally:
-        if old is None:
-            os.environ.pop("FASTED_TS", None)
-        else:
-            os.environ["FASTED_TS"] = old
+    sym = F.make_result_set(*_tc_variant(hd, eps, flags=_lib.JOIN_SYMMETRIC, FASTED_TS=1), n, eps)
     full = F.self_join(hd, eps)
     key = lambda r: set(zip(r.i.tolist(), r.j.tolist()))
     assert len(key(sym) ^ key(full)) <= max(2, len(full) // 10000)

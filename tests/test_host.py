@@ -44,6 +44,25 @@ def test_library_host_calls_without_gpu():
     assert L.fasted_quantize(None, 1, 1, None, 1, 8, None, None, None) == _lib.ERR_ARGUMENT
 
 
+def test_product_library_is_configuration_free():
+    """libfasted.so reads no FASTED_* environment and has no diagnostic flags
+    (the only getenv calls are the static CUDA runtime's own); any flag bit
+    outside the public set
+    is an ArgumentError before any device work.  libfasted_exp.so (the
+    experiment build) exports the same ABI."""
+    blob = open(_lib.LIB_PATH, "rb").read()
+    assert b"FASTED_" not in blob
+    L = _lib.load()
+    for bad in (64, 256, 512, 1024, 1 << 16, 1 << 18):
+        assert L.fasted_join(None, None, 1, 128, 16, 0, 128, 0, 128, 1.0, bad, None, 0,
+                             None, None) == _lib.ERR_ARGUMENT
+        assert b"unknown flag" in L.fasted_last_error()
+    X = _lib.load_experimental()
+    for s in _lib.EXPORTS:
+        assert hasattr(X, s), s
+    assert b"FASTED_CTA_GROUP" in open(_lib.EXP_LIB_PATH, "rb").read()
+
+
 def test_library_is_sm100a_only():
     out = os.popen(f"cuobjdump -lelf {_lib.LIB_PATH} 2>/dev/null").read()
     if not out:
@@ -275,13 +294,15 @@ def test_plan_row_chunks():
 def test_kernel_selection_rule_is_host_side(monkeypatch):
     """fasted_join_kernel_name applies the launch's selection rule without a
     GPU: resident pair for d_pad <= 512, the CTA pair for large low-output
-    joins, multicast clusters otherwise, the exact kernel for mode exact."""
+    joins, multicast clusters otherwise, the exact kernel for mode exact.
+    The product library reads no environment: the experiment build's
+    overrides, set here, change nothing."""
     L = _lib.load()
-    for k in ("FASTED_RES_HIT", "FASTED_MC_HIT", "FASTED_STREAM_HIT", "FASTED_STREAM_EPI",
-              "FASTED_RES_MAXD",
-              "FASTED_RES_EPI", "FASTED_MC_EPI",
-              "FASTED_CTA_GROUP", "FASTED_MC", "FASTED_RESIDENT"):
-        monkeypatch.delenv(k, raising=False)
+    for k, v in (("FASTED_RES_HIT", "0"), ("FASTED_MC_HIT", "0"), ("FASTED_STREAM_HIT", "0"),
+                 ("FASTED_STREAM_EPI", "8"), ("FASTED_RES_MAXD", "64"), ("FASTED_RES_EPI", "8"),
+                 ("FASTED_MC_EPI", "8"), ("FASTED_CTA_GROUP", "1"), ("FASTED_MC", "0"),
+                 ("FASTED_RESIDENT", "0"), ("FASTED_TS", "1")):
+        monkeypatch.setenv(k, v)
 
     def name(d, r, c, f):
         return L.fasted_join_kernel_name(d, r, c, f).decode()
