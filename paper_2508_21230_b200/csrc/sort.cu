@@ -10,16 +10,22 @@
 //   4. per-row ordering by j (j values of a row are distinct):
 //        - rows <= SHORT_MAX records: one warp per row, rank by comparison
 //          against the row staged in shared memory;
-//        - rows <= MID_MAX (then <= BIG_MAX): one CTA per row, bitonic sort
-//          of (j << 32 | d) keys in shared memory (O(len log^2 len)) -- the
-//          high-selectivity case (S ~ 1000-4000 at 5M x 384, where central
-//          points of uniform data have several times the mean neighbour
-//          count);
-//        - longer rows: one CTA per row splits the row into ~len/4096
-//          column buckets (shared-memory counts, scatter in place), then
-//          bitonic-sorts each bucket in shared memory; a row whose buckets
-//          overflow (adversarially clustered j) falls back to a bitmap of the
-//          column range with prefix popcounts, O(n_cols/32 + len).
+//        - rows <= RANK_MAX: one CTA per row, a bucketed rank sort in shared
+//          memory (rank_sort_segment): ~len/4 buckets over the row's
+//          [j_min, j_max] by a monotone float map, counts + scan + scatter,
+//          then each element's rank inside its bucket by comparison -- about
+//          a dozen shared-memory operations per record instead of the
+//          ~300 of a bitonic network (the high-selectivity case: S ~ 1000-4000
+//          at 5M x 384, where central points of uniform data have several
+//          times the mean neighbour count);
+//        - longer rows: one CTA per row splits the row into column
+//          super-buckets of <= RANK_MAX (shared-memory counts, scatter in
+//          place), then rank-sorts each;
+//        - fallbacks, for adversarially clustered j: a bucket above
+//          RANK_BUCKET_MAX sends the row to a bitonic sort of (j << 32 | d)
+//          keys in shared memory (O(len log^2 len)); a super-bucket above
+//          RANK_MAX sends it to a bitmap of the column range with prefix
+//          popcounts, O(n_cols/32 + len).
 //          (This was the path for every row > 1024 before: at S = 4096 it
 //          cleared and scanned a 625 KB bitmap per row, 3.1 s for 2.56e9
 //          records; profiles/round1/c5_sweep_session2.jsonl.)
@@ -32,8 +38,10 @@ constexpr int SCAN_ITEMS = 4;
 constexpr int SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 constexpr int SHORT_MAX = 256;
 constexpr int SHORT_WARPS = 4;
-constexpr int MID_MAX = 8192;                  // keys per CTA bitonic sort (64 KB smem)
-constexpr int BIG_MAX = 16384;                 // second tier: 128 KB smem, one CTA per SM
+constexpr int MID_MAX = 4096;                  // rank sort, small tier (~37 KB smem, 6 CTAs/SM)
+constexpr int BIG_MAX = 16384;                 // rank sort, large tier (~148 KB smem)
+constexpr int RANK_THREADS = 256;
+constexpr int RANK_BUCKET_MAX = 64;            // a fuller bucket: bitonic fallback
 constexpr int MID_THREADS = 512;
 constexpr int LONG_BLOCKS = 32;
 constexpr int LONG_THREADS = 512;
@@ -214,8 +222,8 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
         if (len == 0) continue;
         if (len > SHORT_MAX) {
             if (lane == 0) {
-                if (len <= MID_MAX) mid_rows[atomicAdd(mid_count, 1u)] = (uint32_t)r;
-                else if (len <= BIG_MAX) big_rows[atomicAdd(big_count, 1u)] = (uint32_t)r;
+                if (len <= (uint32_t)MID_MAX) mid_rows[atomicAdd(mid_count, 1u)] = (uint32_t)r;
+                else if (len <= (uint32_t)BIG_MAX) big_rows[atomicAdd(big_count, 1u)] = (uint32_t)r;
                 else long_rows[atomicAdd(long_count, 1u)] = (uint32_t)r;
             }
             continue;
@@ -231,54 +239,6 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
             od[s0 + rank] = td[s0 + e];
         }
         __syncwarp();
-    }
-}
-
-// One CTA per mid-length row: bitonic sort of 64-bit (j << 32 | d bits)
-// keys in shared memory (padding with all-ones keys to the next power of 2);
-// j is unique within a row, so key order is j order.
-template <int KEYS>
-__global__ void __launch_bounds__(MID_THREADS)
-mid_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
-                const unsigned long long* __restrict__ offsets, int64_t row_begin,
-                const uint32_t* __restrict__ mid_rows, const uint32_t* __restrict__ mid_count,
-                uint32_t* __restrict__ oi, uint32_t* __restrict__ oj, float* __restrict__ od) {
-    extern __shared__ unsigned long long key[];   // KEYS entries (dynamic shared memory)
-    const uint32_t nm = *mid_count;
-    for (uint32_t mi = blockIdx.x; mi < nm; mi += gridDim.x) {
-        const int64_t r = mid_rows[mi];
-        const unsigned long long s0 = offsets[r];
-        const uint32_t len = (uint32_t)(offsets[r + 1] - s0);
-        uint32_t n = 1;
-        while (n < len) n <<= 1;
-        for (uint32_t e = threadIdx.x; e < n; e += MID_THREADS)
-            key[e] = e < len ? ((unsigned long long)tj[s0 + e] << 32) |
-                                   (unsigned long long)__float_as_uint(td[s0 + e])
-                             : ~0ull;
-        __syncthreads();
-        for (uint32_t k = 2; k <= n; k <<= 1) {
-            for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-                for (uint32_t t = threadIdx.x; t < (n >> 1); t += MID_THREADS) {
-                    const uint32_t i = ((t & ~(jj - 1)) << 1) | (t & (jj - 1));
-                    const uint32_t l = i + jj;
-                    const unsigned long long a = key[i], b = key[l];
-                    const bool up = (i & k) == 0;
-                    if ((a > b) == up) {
-                        key[i] = b;
-                        key[l] = a;
-                    }
-                }
-                __syncthreads();
-            }
-        }
-        const uint32_t row1 = (uint32_t)(row_begin + r + 1);
-        for (uint32_t e = threadIdx.x; e < len; e += MID_THREADS) {
-            const unsigned long long v = key[e];
-            oi[s0 + e] = row1;
-            oj[s0 + e] = (uint32_t)(v >> 32);
-            od[s0 + e] = __uint_as_float((uint32_t)v);
-        }
-        __syncthreads();
     }
 }
 
@@ -300,19 +260,203 @@ __device__ __forceinline__ void block_bitonic(unsigned long long* key, uint32_t 
     }
 }
 
-constexpr int BUCKETS_MAX = 1024;
+// Shared memory of one bucketed rank sort of up to CAP records: bucketed
+// copies of j and d (bj then bd: together the 8-byte key array of the
+// bitonic fallback), bucket offsets and cursors.
+template <int CAP>
+struct RankSmem {
+    static constexpr int NB = CAP / 8;   // <= 8 records per bucket on average
+    uint32_t bj[CAP];
+    float bd[CAP];
+    uint32_t off[NB + 1];
+    uint32_t cur[NB];
+    uint32_t red[64];
+    uint32_t flag;
+    static constexpr size_t BYTES = ((sizeof(uint32_t) * (2 * CAP + 2 * NB + 1 + 64 + 1)) + 15) &
+                                    ~(size_t)15;
+};
 
-// One CTA per long row (> BIG_MAX records): column buckets, then a
-// shared-memory bitonic sort per bucket.  The row's final slots in
-// out_j/out_d double as the scatter scratch.
-__global__ void __launch_bounds__(MID_THREADS)
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Block-wide exclusive scan of a[0..n) in place (n <= 8 * blockDim.x);
+// a[n] = total.  Returns the largest a[k] before the scan.
+__device__ uint32_t block_scan_excl(uint32_t* a, uint32_t n, uint32_t* red) {
+    const uint32_t per = (n + blockDim.x - 1) / blockDim.x;
+    const uint32_t b0 = threadIdx.x * per;
+    uint32_t sum = 0, mx = 0;
+    for (uint32_t k = 0; k < per; k++)
+        if (b0 + k < n) {
+            sum += a[b0 + k];
+            mx = max(mx, a[b0 + k]);
+        }
+    const uint32_t incl = warp_inclusive_scan(sum);
+    mx = warp_max_u32(mx);
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 31) red[w] = incl;
+    if ((threadIdx.x & 31) == 0) red[32 + w] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const uint32_t t = threadIdx.x < (uint32_t)nw ? red[threadIdx.x] : 0u;
+        const uint32_t m = threadIdx.x < (uint32_t)nw ? red[32 + threadIdx.x] : 0u;
+        const uint32_t ti = warp_inclusive_scan(t);
+        const uint32_t mm = warp_max_u32(m);
+        red[threadIdx.x] = ti - t;
+        if (threadIdx.x == 0) red[32] = mm;
+    }
+    __syncthreads();
+    uint32_t run = red[w] + incl - sum;
+    for (uint32_t k = 0; k < per; k++)
+        if (b0 + k < n) {
+            const uint32_t v = a[b0 + k];
+            a[b0 + k] = run;
+            run += v;
+        }
+    if (threadIdx.x == blockDim.x - 1) a[n] = run;
+    const uint32_t res = red[32];
+    __syncthreads();
+    return res;
+}
+
+// Canonical order of one row segment of L records (distinct j): reads
+// (sj, sd), writes (dj, dd) and, if di, the row id -- dst may alias src.
+// Buckets: a monotone map of [j_min, j_max] onto nb ~ L/4 buckets (a float
+// product: rounding is monotone, so bucket order is j order); counts, scan,
+// scatter into shared memory, then each record's rank inside its bucket by
+// comparison.  Returns false (nothing written) if some bucket holds more
+// than RANK_BUCKET_MAX records (clustered j): the caller sorts otherwise.
+template <int CAP>
+__device__ bool rank_sort_segment(const uint32_t* sj, const float* sd, uint32_t L, uint32_t* dj,
+                                  float* dd, uint32_t* di, uint32_t row1, RankSmem<CAP>& S) {
+    uint32_t mn = 0xffffffffu, mx = 0u;
+    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
+        const uint32_t j = sj[e];
+        mn = min(mn, j);
+        mx = max(mx, j);
+    }
+    mn = warp_min_u32(mn);
+    mx = warp_max_u32(mx);
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        S.red[w] = mn;
+        S.red[32 + w] = mx;
+    }
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const uint32_t a = threadIdx.x < (uint32_t)nw ? S.red[threadIdx.x] : 0xffffffffu;
+        const uint32_t b = threadIdx.x < (uint32_t)nw ? S.red[32 + threadIdx.x] : 0u;
+        const uint32_t am = warp_min_u32(a), bm = warp_max_u32(b);
+        if (threadIdx.x == 0) {
+            S.red[0] = am;
+            S.red[1] = bm;
+        }
+    }
+    __syncthreads();
+    mn = S.red[0];
+    mx = S.red[1];
+    __syncthreads();
+    uint32_t nb = 1;
+    while (nb < (uint32_t)RankSmem<CAP>::NB && nb * 4u < L) nb <<= 1;
+    const float scale = (float)nb / ((float)(mx - mn) + 1.0f);
+    auto bucket = [&](uint32_t j) {
+        const uint32_t b = (uint32_t)((float)(j - mn) * scale);
+        return b < nb ? b : nb - 1u;
+    };
+    for (uint32_t b = threadIdx.x; b <= nb; b += blockDim.x) S.off[b] = 0u;
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) atomicAdd(&S.off[bucket(sj[e])], 1u);
+    __syncthreads();
+    const uint32_t fullest = block_scan_excl(S.off, nb, S.red);
+    if (fullest > (uint32_t)RANK_BUCKET_MAX) return false;   // block-uniform
+    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) S.cur[b] = S.off[b];
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
+        const uint32_t j = sj[e];
+        const uint32_t p = atomicAdd(&S.cur[bucket(j)], 1u);
+        S.bj[p] = j;
+        S.bd[p] = sd[e];
+    }
+    __syncthreads();   // every read of (sj, sd) done: dst may alias src
+    for (uint32_t x = threadIdx.x; x < L; x += blockDim.x) {
+        const uint32_t j = S.bj[x];
+        const uint32_t b = bucket(j);
+        const uint32_t lo = S.off[b], hi = S.off[b + 1];
+        uint32_t rank = 0;
+        for (uint32_t y = lo; y < hi; y++) rank += S.bj[y] < j;
+        dj[lo + rank] = j;
+        dd[lo + rank] = S.bd[x];
+        if (di) di[lo + rank] = row1;
+    }
+    __syncthreads();
+    return true;
+}
+
+// Bitonic fallback for a segment of L <= CAP records (dst may alias src):
+// (j << 32 | d bits) keys in the rank sort's shared memory.
+template <int CAP>
+__device__ void bitonic_segment(const uint32_t* sj, const float* sd, uint32_t L, uint32_t* dj,
+                                float* dd, uint32_t* di, uint32_t row1, RankSmem<CAP>& S) {
+    unsigned long long* key = reinterpret_cast<unsigned long long*>(S.bj);
+    uint32_t n = 1;
+    while (n < L) n <<= 1;
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
+        key[e] = e < L ? ((unsigned long long)sj[e] << 32) | (unsigned long long)__float_as_uint(sd[e])
+                       : ~0ull;
+    __syncthreads();
+    block_bitonic(key, n);
+    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
+        const unsigned long long v = key[e];
+        dj[e] = (uint32_t)(v >> 32);
+        dd[e] = __uint_as_float((uint32_t)v);
+        if (di) di[e] = row1;
+    }
+    __syncthreads();
+}
+
+// One CTA per listed row (SHORT_MAX < len <= CAP): rank sort, bitonic if a
+// bucket overflows.
+template <int CAP>
+__global__ void __launch_bounds__(RANK_THREADS)
+rank_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
+                 const unsigned long long* __restrict__ offsets, int64_t row_begin,
+                 const uint32_t* __restrict__ rows, const uint32_t* __restrict__ nrows,
+                 uint32_t* __restrict__ oi, uint32_t* __restrict__ oj, float* __restrict__ od) {
+    extern __shared__ __align__(16) uint8_t rank_raw[];
+    RankSmem<CAP>& S = *reinterpret_cast<RankSmem<CAP>*>(rank_raw);
+    const uint32_t nm = *nrows;
+    for (uint32_t mi = blockIdx.x; mi < nm; mi += gridDim.x) {
+        const int64_t r = rows[mi];
+        const unsigned long long s0 = offsets[r];
+        const uint32_t len = (uint32_t)(offsets[r + 1] - s0);
+        const uint32_t row1 = (uint32_t)(row_begin + r + 1);
+        if (!rank_sort_segment<CAP>(tj + s0, td + s0, len, oj + s0, od + s0, oi + s0, row1, S))
+            bitonic_segment<CAP>(tj + s0, td + s0, len, oj + s0, od + s0, oi + s0, row1, S);
+    }
+}
+
+constexpr int BUCKETS_MAX = 1024;
+constexpr uint32_t SUPER_TARGET = BIG_MAX / 2;   // expected records per column super-bucket
+
+// One CTA per long row (> BIG_MAX records): column super-buckets (counts,
+// scatter in place into the row's final slots of out_j/out_d), then a rank
+// sort of each, in place.
+__global__ void __launch_bounds__(RANK_THREADS)
 bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
                    const unsigned long long* __restrict__ offsets, int64_t row_begin,
                    int64_t n_cols, const uint32_t* __restrict__ long_rows,
                    const uint32_t* __restrict__ long_count, uint32_t* __restrict__ fb_rows,
                    uint32_t* __restrict__ fb_count, uint32_t* __restrict__ oi,
                    uint32_t* __restrict__ oj, float* __restrict__ od) {
-    extern __shared__ unsigned long long key[];   // BIG_MAX entries
+    extern __shared__ __align__(16) uint8_t rank_raw[];
+    RankSmem<BIG_MAX>& S = *reinterpret_cast<RankSmem<BIG_MAX>*>(rank_raw);
     __shared__ uint32_t cnt[BUCKETS_MAX], boff[BUCKETS_MAX + 1], cur[BUCKETS_MAX];
     __shared__ uint32_t overflow;
     const uint32_t nl = *long_count;
@@ -321,13 +465,13 @@ bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td
         const unsigned long long s0 = offsets[r];
         const uint32_t len = (uint32_t)(offsets[r + 1] - s0);
         uint32_t nb = 2;
-        while (nb < BUCKETS_MAX && (uint64_t)nb * 4096u < len) nb <<= 1;
-        const uint64_t bw = ((uint64_t)n_cols + nb - 1) / nb;   // columns per bucket
+        while (nb < BUCKETS_MAX && (uint64_t)nb * SUPER_TARGET < len) nb <<= 1;
+        const uint32_t bw = (uint32_t)(((uint64_t)n_cols + nb - 1) / nb);   // columns per bucket
         for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) cnt[b] = 0;
         if (threadIdx.x == 0) overflow = 0;
         __syncthreads();
         for (uint32_t e = threadIdx.x; e < len; e += blockDim.x)
-            atomicAdd(&cnt[(uint32_t)((tj[s0 + e] - 1) / bw)], 1u);
+            atomicAdd(&cnt[(tj[s0 + e] - 1u) / bw], 1u);
         __syncthreads();
         if (threadIdx.x == 0) {   // nb <= 1024: a serial scan is cheap next to the row
             uint32_t run = 0;
@@ -347,7 +491,7 @@ bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td
         }
         for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
             const uint32_t j = tj[s0 + e];
-            const uint32_t pos = atomicAdd(&cur[(uint32_t)((j - 1) / bw)], 1u);
+            const uint32_t pos = atomicAdd(&cur[(j - 1u) / bw], 1u);
             oj[s0 + pos] = j;
             od[s0 + pos] = td[s0 + e];
         }
@@ -356,21 +500,10 @@ bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td
         for (uint32_t b = 0; b < nb; b++) {
             const uint32_t b0 = boff[b], bl = boff[b + 1] - b0;
             if (bl == 0) continue;
-            uint32_t n = 1;
-            while (n < bl) n <<= 1;
-            for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
-                key[e] = e < bl ? ((unsigned long long)oj[s0 + b0 + e] << 32) |
-                                      (unsigned long long)__float_as_uint(od[s0 + b0 + e])
-                                : ~0ull;
-            __syncthreads();
-            block_bitonic(key, n);
-            for (uint32_t e = threadIdx.x; e < bl; e += blockDim.x) {
-                const unsigned long long v = key[e];
-                oi[s0 + b0 + e] = row1;
-                oj[s0 + b0 + e] = (uint32_t)(v >> 32);
-                od[s0 + b0 + e] = __uint_as_float((uint32_t)v);
-            }
-            __syncthreads();
+            uint32_t* sj = oj + s0 + b0;
+            float* sd = od + s0 + b0;
+            if (!rank_sort_segment<BIG_MAX>(sj, sd, bl, sj, sd, oi + s0 + b0, row1, S))
+                bitonic_segment<BIG_MAX>(sj, sd, bl, sj, sd, oi + s0 + b0, row1, S);
         }
     }
 }
@@ -491,34 +624,31 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
                                                   ws.long_count, ws.mid_rows, ws.mid_count,
                                                   ws.big_rows, ws.big_count);
     FASTED_CHECK_LAUNCH("short_rows_kernel");
-    static PerDeviceOnce mid_once;
+    static PerDeviceOnce rank_once;
     {
-        cudaError_t e = mid_once.run([&] {
-            cudaError_t r = cudaFuncSetAttribute(mid_rows_kernel<MID_MAX>,
+        cudaError_t e = rank_once.run([&] {
+            cudaError_t r = cudaFuncSetAttribute(rank_rows_kernel<MID_MAX>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 MID_MAX * 8);
+                                                 (int)RankSmem<MID_MAX>::BYTES);
             if (r == cudaSuccess)
-                r = cudaFuncSetAttribute(mid_rows_kernel<BIG_MAX>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, BIG_MAX * 8);
+                r = cudaFuncSetAttribute(rank_rows_kernel<BIG_MAX>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)RankSmem<BIG_MAX>::BYTES);
+            if (r == cudaSuccess)
+                r = cudaFuncSetAttribute(bucket_rows_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)RankSmem<BIG_MAX>::BYTES);
             return r;
         });
-        if (e != cudaSuccess) return cuda_status(e, "mid_rows_kernel attribute");
+        if (e != cudaSuccess) return cuda_status(e, "rank sort attributes");
     }
-    mid_rows_kernel<MID_MAX><<<(unsigned)(sms * 3), MID_THREADS, MID_MAX * 8, s>>>(
+    rank_rows_kernel<MID_MAX><<<(unsigned)(sms * 6), RANK_THREADS, RankSmem<MID_MAX>::BYTES, s>>>(
         tmp_j, tmp_d, ws.offsets, row_begin, ws.mid_rows, ws.mid_count, out_i, out_j, out_d);
-    FASTED_CHECK_LAUNCH("mid_rows_kernel");
-    mid_rows_kernel<BIG_MAX><<<(unsigned)sms, MID_THREADS, BIG_MAX * 8, s>>>(
+    FASTED_CHECK_LAUNCH("rank_rows_kernel<4096>");
+    rank_rows_kernel<BIG_MAX><<<(unsigned)sms, RANK_THREADS, RankSmem<BIG_MAX>::BYTES, s>>>(
         tmp_j, tmp_d, ws.offsets, row_begin, ws.big_rows, ws.big_count, out_i, out_j, out_d);
-    FASTED_CHECK_LAUNCH("mid_rows_kernel");
-    static PerDeviceOnce bucket_once;
-    {
-        cudaError_t e = bucket_once.run([&] {
-            return cudaFuncSetAttribute(bucket_rows_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, BIG_MAX * 8);
-        });
-        if (e != cudaSuccess) return cuda_status(e, "bucket_rows_kernel attribute");
-    }
-    bucket_rows_kernel<<<(unsigned)sms, MID_THREADS, BIG_MAX * 8, s>>>(
+    FASTED_CHECK_LAUNCH("rank_rows_kernel<16384>");
+    bucket_rows_kernel<<<(unsigned)sms, RANK_THREADS, RankSmem<BIG_MAX>::BYTES, s>>>(
         tmp_j, tmp_d, ws.offsets, row_begin, n_cols, ws.long_rows, ws.long_count, ws.fb_rows,
         ws.fb_count, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("bucket_rows_kernel");

@@ -97,8 +97,19 @@ def main():
                     dd, es, jflags, rows, (0, dd.n_dev), rec, cap, cnt, sp)))
         slots = int(cnt[1].item()) * engine.RECORD_CHUNK
         assert int(cnt[0].item()) == pairs
-        sort_ms = timed(lambda: engine._sort_records(dd, rec, slots, pairs, rows, stream,
-                                                    timed=False))
+        dev = "cuda"
+        sout = (torch.empty(max(pairs, 1), dtype=torch.int32, device=dev),
+                torch.empty(max(pairs, 1), dtype=torch.int32, device=dev),
+                torch.empty(max(pairs, 1), dtype=torch.float32, device=dev))
+        stmp = (torch.empty(max(pairs, 1), dtype=torch.int32, device=dev),
+                torch.empty(max(pairs, 1), dtype=torch.float32, device=dev))
+        sws = torch.empty(L.fasted_sort_workspace_bytes(rows[1] - rows[0], dd.n_dev),
+                          dtype=torch.uint8, device=dev)
+        sort = lambda: engine._sort_records(dd, rec, slots, pairs, rows, stream, out=sout,
+                                            timed=False, tmp=stmp, ws=sws)
+        sort()   # first call: attributes, caches
+        sort_ms = timed(sort)
+        del sout, stmp, sws
         del rec
         torch.cuda.empty_cache()
         jm, cm = min(join_ms), min(count_ms)
