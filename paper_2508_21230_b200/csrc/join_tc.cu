@@ -1562,6 +1562,7 @@ struct ResSched {
     int stages;               // B ring stages
     uint32_t a_buf_bytes;     // one A buffer: nkb k-blocks + augment rows, 1024-aligned
     int64_t units;            // row_tiles * nsegs
+    int lanes;                // units in flight: CTA pairs (CTAs) launched
 };
 
 // Records per staging buffer in the resident kernel (tight shared memory):
@@ -1587,10 +1588,25 @@ struct ResCfg {
     static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1024-aligned");
 };
 
+// Unit order: rounds of `lanes` row tiles.  Inside a round, lane (pair) p
+// keeps row tile round * lanes + p and sweeps the column segments in order,
+// all lanes on the same segment at the same time -- so co-running pairs share
+// each B panel in L2 (as a segment-major order would), each pair's A panel
+// stays the same for a whole round, and the record stream is row-coherent:
+// a row's records are produced within one round, not spread over the whole
+// launch (the canonical-order scatter then writes each row's segment while it
+// is still in L2).  A last, partial round of m row tiles is spread over all
+// lanes (unit v -> row tile v % m, segment v / m).
 __device__ __forceinline__ void res_unit(const ResSched& s, int64_t u, int& rt, int& ct0,
                                          int& ct1) {
-    const int64_t g = u / s.row_tiles;
-    rt = (int)(u - g * s.row_tiles);
+    const int64_t per_round = (int64_t)s.lanes * s.nsegs;
+    const int64_t R = u / per_round;
+    const int64_t v = u - R * per_round;
+    const int64_t rt0 = R * s.lanes;
+    const int64_t left = (int64_t)s.row_tiles - rt0;
+    const int64_t m = left < s.lanes ? left : s.lanes;
+    const int64_t g = v / m;
+    rt = (int)(rt0 + (v - g * m));
     ct0 = (int)((int64_t)s.col_tiles * g / s.nsegs);
     ct1 = (int)((int64_t)s.col_tiles * (g + 1) / s.nsegs);
 }
@@ -2379,6 +2395,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     const int64_t slots = sm_count_current() / CG;
     const int64_t work = sch.units < slots ? sch.units : slots;
     if (work <= 0) return cudaSuccess;
+    sch.lanes = (int)work;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * CG));
     cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI + NHIT) * 32);
@@ -2485,6 +2502,7 @@ static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUte
     const int64_t slots = sm_count_current() / 2;
     const int64_t work = sch.units < slots ? sch.units : slots;
     if (work <= 0) return cudaSuccess;
+    sch.lanes = (int)work;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * 2));
     cfg.blockDim = dim3(TS_THREADS);

@@ -40,7 +40,8 @@ constexpr int SHORT_MAX = 256;
 constexpr int SHORT_WARPS = 4;
 constexpr int MID_MAX = 4096;                  // rank sort, small tier (~37 KB smem, 6 CTAs/SM)
 constexpr int BIG_MAX = 16384;                 // rank sort, large tier (~148 KB smem)
-constexpr int RANK_THREADS = 256;
+constexpr int RANK_THREADS = 256;              // small tier (several CTAs per SM)
+constexpr int BIG_THREADS = 1024;              // large tier and long rows (one CTA per SM)
 constexpr int RANK_BUCKET_MAX = 64;            // a fuller bucket: bitonic fallback
 constexpr int MID_THREADS = 512;
 constexpr int LONG_BLOCKS = 32;
@@ -423,8 +424,8 @@ __device__ void bitonic_segment(const uint32_t* sj, const float* sd, uint32_t L,
 
 // One CTA per listed row (SHORT_MAX < len <= CAP): rank sort, bitonic if a
 // bucket overflows.
-template <int CAP>
-__global__ void __launch_bounds__(RANK_THREADS)
+template <int CAP, int THREADS>
+__global__ void __launch_bounds__(THREADS)
 rank_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
                  const unsigned long long* __restrict__ offsets, int64_t row_begin,
                  const uint32_t* __restrict__ rows, const uint32_t* __restrict__ nrows,
@@ -448,7 +449,7 @@ constexpr uint32_t SUPER_TARGET = BIG_MAX / 2;   // expected records per column 
 // One CTA per long row (> BIG_MAX records): column super-buckets (counts,
 // scatter in place into the row's final slots of out_j/out_d), then a rank
 // sort of each, in place.
-__global__ void __launch_bounds__(RANK_THREADS)
+__global__ void __launch_bounds__(BIG_THREADS)
 bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
                    const unsigned long long* __restrict__ offsets, int64_t row_begin,
                    int64_t n_cols, const uint32_t* __restrict__ long_rows,
@@ -627,11 +628,11 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
     static PerDeviceOnce rank_once;
     {
         cudaError_t e = rank_once.run([&] {
-            cudaError_t r = cudaFuncSetAttribute(rank_rows_kernel<MID_MAX>,
+            cudaError_t r = cudaFuncSetAttribute(rank_rows_kernel<MID_MAX, RANK_THREADS>,
                                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)RankSmem<MID_MAX>::BYTES);
             if (r == cudaSuccess)
-                r = cudaFuncSetAttribute(rank_rows_kernel<BIG_MAX>,
+                r = cudaFuncSetAttribute(rank_rows_kernel<BIG_MAX, BIG_THREADS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)RankSmem<BIG_MAX>::BYTES);
             if (r == cudaSuccess)
@@ -642,13 +643,13 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
         });
         if (e != cudaSuccess) return cuda_status(e, "rank sort attributes");
     }
-    rank_rows_kernel<MID_MAX><<<(unsigned)(sms * 6), RANK_THREADS, RankSmem<MID_MAX>::BYTES, s>>>(
+    rank_rows_kernel<MID_MAX, RANK_THREADS><<<(unsigned)(sms * 6), RANK_THREADS, RankSmem<MID_MAX>::BYTES, s>>>(
         tmp_j, tmp_d, ws.offsets, row_begin, ws.mid_rows, ws.mid_count, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("rank_rows_kernel<4096>");
-    rank_rows_kernel<BIG_MAX><<<(unsigned)sms, RANK_THREADS, RankSmem<BIG_MAX>::BYTES, s>>>(
+    rank_rows_kernel<BIG_MAX, BIG_THREADS><<<(unsigned)sms, BIG_THREADS, RankSmem<BIG_MAX>::BYTES, s>>>(
         tmp_j, tmp_d, ws.offsets, row_begin, ws.big_rows, ws.big_count, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("rank_rows_kernel<16384>");
-    bucket_rows_kernel<<<(unsigned)sms, RANK_THREADS, RankSmem<BIG_MAX>::BYTES, s>>>(
+    bucket_rows_kernel<<<(unsigned)sms, BIG_THREADS, RankSmem<BIG_MAX>::BYTES, s>>>(
         tmp_j, tmp_d, ws.offsets, row_begin, n_cols, ws.long_rows, ws.long_count, ws.fb_rows,
         ws.fb_count, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("bucket_rows_kernel");

@@ -63,7 +63,7 @@ def main():
             hbm = float(json.load(f)["hbm_gbs"])
     except Exception:
         pass
-    peak_burst, peak_sus, _ = load_peaks()
+    peak_burst, peak_sus, _, _ = load_peaks()
     cnt = torch.zeros(2, dtype=torch.int64, device="cuda")
     flops = 2.0 * nrows * N * D
     for (label, eps), extra in [(le, x) for le in SWEEP for x in extras]:
