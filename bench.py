@@ -31,9 +31,7 @@ import hashlib
 import json
 import os
 import statistics
-import subprocess
 import sys
-import threading
 import time
 from concurrent.futures import ThreadPoolExecutor
 
@@ -41,6 +39,9 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+
+from paper_2508_21230_b200.measure import (ClockSampler, load_peaks,  # noqa: E402
+                                          tensor_roofline, timed_launches)
 
 METRIC = "ε-self-join TFLOPS, % of FP16 TC peak at 1–8 B200; pair accuracy vs FP64"
 
@@ -58,78 +59,6 @@ C5_SWEEP = [("S0 (eps 0: self pairs only)", 0.0), ("S16", 6.896041752764515),
 SEED = 12345
 C1_PAIRS = 1199444
 C1_SHA256 = None   # read from tests/golden/reference_meta.json when present
-LONG_LAUNCH_MS = 100.0   # launches longer than this are rated against the sustained peak
-SM_COUNT = 148
-FLOP_PER_CLK_SM = 8192   # dense FP16 tcgen05 rate per SM per clock
-
-
-def load_peaks():
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            p = json.load(f)
-        return (float(p["bf16_tflops"]), float(p.get("bf16_tflops_sustained", 0) or 0),
-                float(p.get("hbm_gbs", 0) or 6540.5), "measured")
-    except Exception:
-        return 1590.0, 1400.0, 6540.5, "fallback (B200_PROFILING.md)"
-
-
-class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
-
-    def __init__(self, device: int):
-        self.device = device
-        self.proc = None
-        self.lines = []
-
-    def __enter__(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except Exception:
-            self.proc = None
-        return self
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-
-    def summary(self):
-        sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
-                "reasons": sorted(reasons), "samples": len(sm)}
-
-
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -246,35 +175,6 @@ def run_reference(args):
 
 
 # ── GPU helpers ─────────────────────────────────────────────────────────
-
-
-def timed_launches(stream, fn, reps):
-    """Per-launch CUDA-event times (ms) of `reps` back-to-back calls."""
-    import torch
-
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(reps + 1)]
-    ev[0].record(stream)
-    for r in range(reps):
-        fn()
-        ev[r + 1].record(stream)
-    ev[-1].synchronize()
-    return [ev[r].elapsed_time(ev[r + 1]) for r in range(reps)]
-
-
-def tensor_roofline(flops, launch_ms, clocks, peaks):
-    peak_burst, peak_sus, _, src = peaks
-    long = launch_ms > LONG_LAUNCH_MS and peak_sus
-    peak = peak_sus if long else peak_burst
-    achieved = flops / (launch_ms / 1e3) / 1e12
-    out = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-           "frac": achieved / peak,
-           "peak_source": f"{src} " + ("bf16_tflops_sustained (launch > 100 ms)" if long
-                                       else "bf16_tflops burst (launch <= 100 ms)")}
-    mhz = clocks.get("sm_mhz") if clocks else None
-    if mhz:
-        at_clock = FLOP_PER_CLK_SM * SM_COUNT * mhz * 1e6 / 1e12
-        out["frac_of_tensor_rate_at_median_clock"] = achieved / at_clock
-    return out
 
 
 def device_synthetic(n, d, seed, device, chunk_rows=131072):
@@ -543,10 +443,18 @@ def main():
 
     rank, world, local = dist_env()
     if world > 1:
+        # one rank per GPU; FASTED_BENCH_DIST_BACKEND=gloo lets the test suite
+        # run two ranks on one GPU (NCCL refuses a shared device) -- the
+        # process group carries only bookkeeping (max time, summed counts)
+        local = local % torch.cuda.device_count()
         torch.cuda.set_device(local)
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        backend = os.environ.get("FASTED_BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(backend)
     device = torch.cuda.current_device()
     _lib.require_device(device)
     name, n, d, eps = WORKLOADS[args.workload]

@@ -16,43 +16,66 @@ import numpy as np
 
 from . import _lib, engine
 from .analysis import distance_error_stats, overlap_accuracy
+from .errors import ArgumentError
 from .tiling import ResultSet
 
-__all__ = ["fp64_truth_rows", "sample_row_blocks", "join_row_blocks", "accuracy_vs_fp64"]
+__all__ = ["fp64_truth_rows", "brute_force_fp64", "sample_row_blocks", "join_row_blocks", "accuracy_vs_fp64"]
 
 
-def fp64_truth_rows(values: np.ndarray, rows, epsilon: float, device: int = 0):
+def fp64_truth_rows(values: np.ndarray, rows, epsilon: float, device: int = 0,
+                    chunk_rows: int = 8192):
     """FP64 truth pairs (1-based i, j, float64 dist_sq) for the 0-based
-    query `rows`, canonical order."""
+    query `rows` (None: every point), canonical order.  The FP32 matrix is
+    uploaded once; queries run in chunks of `chunk_rows`, each chunk's
+    record buffer grown to its exact count and rerun if it overflowed."""
     import torch
 
+    if not np.isfinite(epsilon) or epsilon < 0:
+        raise ArgumentError(f"epsilon must be finite and >= 0, got {epsilon}")
     _lib.require_device(device)
     L = _lib.load()
-    rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
     vals = np.ascontiguousarray(values, dtype=np.float32)
     n, d = vals.shape
+    rows = (np.arange(n, dtype=np.int64) if rows is None
+            else np.ascontiguousarray(np.asarray(rows, dtype=np.int64)))
     dev = f"cuda:{device}"
+    parts = []
     with torch.cuda.device(device):
         stream = torch.cuda.current_stream().cuda_stream
         x = torch.from_numpy(vals).to(dev)
-        q = torch.from_numpy(rows).to(dev)
         cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-        cap = max(len(rows) * 512, 1024)
-        while True:
-            rec = torch.empty((cap, 4), dtype=torch.int32, device=dev)
-            _lib.check(L.fasted_fp64_rows(x.data_ptr(), n, d, q.data_ptr(), len(rows),
-                                          float(epsilon), rec.data_ptr(), cap, cnt.data_ptr(),
-                                          stream), "fasted_fp64_rows")
-            count = engine.read_counts(cnt)[0]
-            if count <= cap:
-                break
-            cap = count
-        raw = rec[:count].cpu().numpy()
+        cap = max(min(len(rows), chunk_rows) * 512, 1024)
+        rec = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+        for c0 in range(0, len(rows), chunk_rows):
+            q = torch.from_numpy(rows[c0:c0 + chunk_rows]).to(dev)
+            while True:
+                _lib.check(L.fasted_fp64_rows(x.data_ptr(), n, d, q.data_ptr(), q.numel(),
+                                              float(epsilon), rec.data_ptr(), cap,
+                                              cnt.data_ptr(), stream), "fasted_fp64_rows")
+                count = engine.read_counts(cnt)[0]
+                if count <= cap:
+                    break
+                cap = count + count // 4
+                rec = torch.empty((cap, 4), dtype=torch.int32, device=dev)
+            parts.append(rec[:count].cpu().numpy())
+    raw = np.concatenate(parts) if parts else np.empty((0, 4), np.int32)
     i = raw[:, 0].view(np.uint32).copy()
     j = raw[:, 1].view(np.uint32).copy()
     d2 = raw[:, 2:4].copy().view(np.float64).reshape(-1)
     order = np.lexsort((j, i))
     return i[order], j[order], d2[order]
+
+
+def brute_force_fp64(ds, epsilon: float, device: int = 0, rows=None) -> ResultSet:
+    """Drop-in for the reference's ``brute_force_fp64`` (oracle.py:43-64):
+    every ordered pair (self-pairs included) with FP64 distance <= epsilon,
+    direct subtract-square form in ascending k on the original FP32 values,
+    threshold sqrt(d2) <= epsilon, float64 dist_sq, canonical order --
+    computed by ``fasted_fp64_rows`` on the GPU (csrc/fp64.cu).  `rows`
+    (0-based) restricts the query points (the truth of a row sample)."""
+    values = getattr(ds, "values", ds)
+    i, j, d2 = fp64_truth_rows(values, rows, epsilon, device)
+    return ResultSet(i, j, d2, n=int(values.shape[0]), epsilon=float(epsilon))
 
 
 def sample_row_blocks(n: int, blocks: int = 8, seed: int = 0, block: int = 128) -> np.ndarray:

@@ -33,13 +33,17 @@ enum {
     // epilogue hit-search A/B (results stay valid): always per-lane masks /
     // always transposed rows
     FASTED_JOIN_DIAG_RARE_LM = 131072,
-    FASTED_JOIN_DIAG_RARE_ROWS = 262144
+    FASTED_JOIN_DIAG_RARE_ROWS = 262144,
+    // attribution of the augment step (results NOT valid): skip the
+    // kind::tf32 augment MMA / issue it as a kind::f16 MMA instead
+    FASTED_JOIN_DIAG_NOAUG = 524288,
+    FASTED_JOIN_DIAG_AUGF16 = 1048576
 };
 constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA | FASTED_JOIN_DIAG_LOADONLY |
     FASTED_JOIN_DIAG_NOSLOW | FASTED_JOIN_DIAG_SPIN | FASTED_JOIN_DIAG_LDX64 |
     FASTED_JOIN_DIAG_AEVL | FASTED_JOIN_DIAG_TRACE | FASTED_JOIN_DIAG_RARE_LM |
-    FASTED_JOIN_DIAG_RARE_ROWS;
+    FASTED_JOIN_DIAG_RARE_ROWS | FASTED_JOIN_DIAG_NOAUG | FASTED_JOIN_DIAG_AUGF16;
 
 inline int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -67,7 +71,9 @@ enum {
     FASTED_JOIN_DIAG_AEVL = 0,
     FASTED_JOIN_DIAG_TRACE = 0,
     FASTED_JOIN_DIAG_RARE_LM = 0,
-    FASTED_JOIN_DIAG_RARE_ROWS = 0
+    FASTED_JOIN_DIAG_RARE_ROWS = 0,
+    FASTED_JOIN_DIAG_NOAUG = 0,
+    FASTED_JOIN_DIAG_AUGF16 = 0
 };
 
 #endif

@@ -1812,9 +1812,14 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                                 mma_f16<CG>(dtm, ad + koff, bd + koff, (kb | kk) != 0 ? 1u : 0u,
                                             C::IDESC_F16);
                             }
-                            if (kb == sch.nkb - 1)
-                                mma_tf32<CG>(dtm, sw32_desc(abuf + a_aug_off),
-                                             sw32_desc(st + C::B_BYTES), C::IDESC_TF32);
+                            if (kb == sch.nkb - 1) {
+                                if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_AUGF16)
+                                    mma_f16<CG>(dtm, sw32_desc(abuf + a_aug_off),
+                                                sw32_desc(st + C::B_BYTES), 1u, C::IDESC_F16);
+                                else if (!(FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOAUG))
+                                    mma_tf32<CG>(dtm, sw32_desc(abuf + a_aug_off),
+                                                 sw32_desc(st + C::B_BYTES), C::IDESC_TF32);
+                            }
                         }
                         mma_commit<CG>(empty_bar(s));
                         }

@@ -336,3 +336,26 @@ def test_form_hints_thresholds():
     shard, cols = (0, 625_024), (0, 5_000_064)
     assert engine.form_hints(2_516_311_890, shard, cols) == 0                              # C5 S4096
     assert engine.form_hints(160_000_000, shard, cols) == _lib.JOIN_SPARSE                  # C5 S256
+
+
+def test_overlap_vectorised_equals_reference_loop():
+    """analysis.overlap_accuracy (vectorised) == the reference's per-point set
+    loop (analysis.py:127-147) bit for bit, incl. empty-on-one/both-sides
+    points and a point sample."""
+    rng = np.random.default_rng(11)
+    n = 300
+    for trial in range(4):
+        def rand_rs(m):
+            i = rng.integers(1, n - 20, m)       # points n-19..n have no pairs anywhere
+            j = rng.integers(1, n + 1, m)
+            key = np.unique((i.astype(np.uint64) << np.uint64(32)) | j.astype(np.uint64))
+            return F.make_result_set((key >> np.uint64(32)).astype(np.uint32),
+                                     (key & np.uint64(0xFFFFFFFF)).astype(np.uint32),
+                                     np.zeros(len(key), np.float32), n, 1.0)
+        a, b = rand_rs(2000 + 300 * trial), rand_rs(1800)
+        assert F.overlap_accuracy(a, b) == F.analysis.overlap_accuracy_sets(a, b)
+        pts = rng.choice(np.arange(1, n + 1), 50, replace=False)
+        assert F.overlap_accuracy(a, b, points=pts) == \
+            F.analysis.overlap_accuracy_sets(a, b, points=pts)
+    empty = F.make_result_set([], [], np.zeros(0, np.float32), n, 1.0)
+    assert F.overlap_accuracy(empty, empty) == 1.0
