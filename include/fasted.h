@@ -21,6 +21,7 @@
  * Reference interfaces replaced (paths under /root/reference/pkg/src/mpjoin):
  *   fasted_quantize  : dataset.to_half            dataset.py:164-193
  *                      + _kernel.squared_norms_rz _kernel.py:79-93
+ *   fasted_quantize_async : the same, stream-ordered (device overflow word)
  *   fasted_norms     : dataset.compute_squared_norms dataset.py:159-161
  *   fasted_join      : tiling.self_join's sweep   tiling.py:307-344
  *                      (work queue + compute_block_tile tiling.py:199-285
@@ -103,6 +104,17 @@ int fasted_device_check(int device);
 int fasted_quantize(const float* x, int64_t n, int64_t d, uint16_t* values16,
                     int64_t n_pad, int64_t d_pad, float* norms,
                     int64_t* first_overflow_host, void* stream);
+
+/*
+ * fasted_quantize without the synchronisation (same kernel, same bits): the
+ * overflow index is atomicMin'ed into the DEVICE word *first_overflow_dev,
+ * which the caller sets to ~0 before the call and reads after the stream
+ * reaches it (~0: no overflow).  For pipelines that quantise in chunks and
+ * check once (bench.py's 5M x 384 generation, the per-kernel timing).
+ */
+int fasted_quantize_async(const float* x, int64_t n, int64_t d, uint16_t* values16,
+                          int64_t n_pad, int64_t d_pad, float* norms,
+                          unsigned long long* first_overflow_dev, void* stream);
 
 /* RZ squared norms of an existing FP16 [n_pad, d_pad] matrix. */
 int fasted_norms(const uint16_t* values16, int64_t n_pad, int64_t d_pad, float* norms,

@@ -29,7 +29,8 @@ JOIN_SPARSE = 32
 # Every symbol include/fasted.h declares (tests check the .so exports them).
 EXPORTS = (
     "fasted_abi_version", "fasted_strerror", "fasted_last_error", "fasted_device_check",
-    "fasted_device_info", "fasted_join_kernel_name", "fasted_quantize", "fasted_norms", "fasted_join",
+    "fasted_device_info", "fasted_join_kernel_name", "fasted_quantize", "fasted_quantize_async",
+    "fasted_norms", "fasted_join",
     "fasted_sort_workspace_bytes", "fasted_sort_pairs", "fasted_fp64_rows",
 )
 
@@ -71,6 +72,9 @@ def _load(path):
         L.fasted_device_info.argtypes = [ctypes.POINTER(ci), ctypes.c_char_p, ci]
         L.fasted_quantize.restype = ci
         L.fasted_quantize.argtypes = [p, i64, i64, p, i64, i64, p, ctypes.POINTER(i64), p]
+        if hasattr(L, "fasted_quantize_async"):   # (older experiment builds lack it)
+            L.fasted_quantize_async.restype = ci
+            L.fasted_quantize_async.argtypes = [p, i64, i64, p, i64, i64, p, p, p]
         L.fasted_norms.restype = ci
         L.fasted_norms.argtypes = [p, i64, i64, p, p]
         L.fasted_join.restype = ci

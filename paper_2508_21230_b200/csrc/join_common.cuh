@@ -28,10 +28,17 @@ struct JoinArgs {
 // committed}, then [t][w][8] per epilogue warp {tfull passed, TMEM loads
 // landed, tempty arrived, tile done, slice vote done, rare chunk: hit masks
 // built, rare chunk: records appended, 1 if a rare chunk ran}.
+// Then, with hit warps, [h][e][4] per hit warp h < TRACE_HIT_WARPS and
+// queue entry e < TRACE_HIT_ENTRIES {wait for the entry started, entry
+// visible, entry done, kind | records << 8}.
 constexpr int TRACE_TILES = 256;
 constexpr int TRACE_EPI_WARPS = 16;
-constexpr unsigned long long TRACE_WORDS =
+constexpr int TRACE_HIT_WARPS = 2;
+constexpr int TRACE_HIT_ENTRIES = 512;
+constexpr unsigned long long TRACE_HIT_BASE =
     (unsigned long long)TRACE_TILES * (2 + 8 * TRACE_EPI_WARPS);
+constexpr unsigned long long TRACE_WORDS =
+    TRACE_HIT_BASE + (unsigned long long)TRACE_HIT_WARPS * TRACE_HIT_ENTRIES * 4;
 
 // ((-2 a) + s_i) + s_j in FP32 round-to-nearest, clamped at 0
 // (mma.py:143-157).  -2a is exact, so the first step is one RN FMA.

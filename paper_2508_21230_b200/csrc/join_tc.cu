@@ -805,6 +805,30 @@ __device__ __forceinline__ void st_release_shared(uint32_t addr, uint32_t v) {
 }
 enum { HIT_ROW = 0, HIT_SELF = 1, HIT_END = 2 };
 
+// This CTA's shared::cta address as a shared::cluster address (st.async
+// takes the latter; in a non-cluster launch the CTA is rank 0 of 1).
+__device__ __forceinline__ uint32_t cluster_addr(uint32_t cta_addr) {
+    uint32_t rank, r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(cta_addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                 : "memory");
+}
+
+// 16-byte asynchronous store into shared::cluster memory; its completion
+// counts 16 bytes on the mbarrier `bar` (shared::cluster address).
+__device__ __forceinline__ void st_async_v4(uint32_t addr, uint4 v, uint32_t bar) {
+    asm volatile(
+        "st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, "
+        "[%5];" ::"r"(addr),
+        "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "r"(bar)
+        : "memory");
+}
+
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
     uint4 v;
     asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
@@ -823,27 +847,31 @@ __device__ __forceinline__ void hit_put(uint32_t reg, int q, uint32_t idx, uint3
     using H = HitQ<NHIT>;
     const uint32_t slot = idx % H::Q;
     if (idx >= (uint32_t)H::Q) {
-        // at most one lap ahead of the hit warp (the head counter), then the
-        // slot's empty barrier for the previous lap (all 32 consumer lanes
-        // arrive after their reads; with the lap bounded its parity is
-        // unambiguous)
+        // the slot's previous lap (entry idx - Q) must be consumed: the hit
+        // warp publishes its head counter (release, after all 32 lanes read
+        // the entry) and this acquire orders the refill after those reads
         if (ld_acquire_shared(H::head(reg, q)) + H::Q <= idx) {
             const uint64_t t0 = global_timer();
             while (ld_acquire_shared(H::head(reg, q)) + H::Q <= idx) {
-                __nanosleep(64);
+                __nanosleep(32);
                 if (global_timer() - t0 > 20000000000ull) __trap();
             }
         }
-        mbar_wait(H::full(reg, q, slot) + 8u, ((idx / H::Q) & 1u) ^ 1u);
     }
+    // The entry goes in with st.async (async proxy, completion counted in
+    // bytes on the slot's full barrier): the consumer's wait returns once
+    // the bytes landed, and the hand-off is the TMA-style one -- no generic
+    // shared-memory store for a generic load on another warp to race with.
+    const uint32_t full = cluster_addr(H::full(reg, q, slot));
+    mbar_arrive_expect_tx(H::full(reg, q, slot), with_data ? 144u : 16u);
     if (with_data) {
-        const uint32_t d = H::data(reg, q, slot);
+        const uint32_t d = cluster_addr(H::data(reg, q, slot));
 #pragma unroll
         for (int k = 0; k < 8; k++)
-            st_shared_v4(d + 16u * k, make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
+            st_async_v4(d + 16u * k, make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]),
+                        full);
     }
-    st_shared_v4(H::meta(reg, q, slot), make_uint4(kind, i, jb, mask));
-    mbar_arrive(H::full(reg, q, slot));
+    st_async_v4(cluster_addr(H::meta(reg, q, slot)), make_uint4(kind, i, jb, mask), full);
 }
 
 // Hand one 32-column chunk's candidate rows (and the diagonal's self pairs)
@@ -881,18 +909,20 @@ __device__ __forceinline__ void hit_push(uint32_t reg, uint8_t* smem_raw, uint32
 
 // The resident epilogue tile with hit warps: drain, release, slice test, and
 // on a candidate only the hand-off.
-template <int CG, int TBN, int NSPLIT, int NHIT>
+template <int CG, int TBN, int NSPLIT, int NHIT, bool TRACE = false>
 __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg, uint8_t* smem_raw,
                                                  uint32_t raw, int hq, uint32_t tcol,
                                                  uint32_t tfull, uint32_t aph, uint32_t tempty,
                                                  bool local_release, bool spin, int dflags,
                                                  int nchunks, bool fast, int jb, int i, int iw,
-                                                 bool row_ok, uint32_t lane) {
+                                                 bool row_ok, uint32_t lane,
+                                                 unsigned long long* tr = nullptr) {
     constexpr int HALF = TBN / NSPLIT;
     constexpr int NCH = HALF / 32;
     static_assert(NCH == 2, "hit-warp epilogue: 64 columns per warp");
     mbar_wait2(tfull, aph, spin);
     tc_fence_after();
+    if (TRACE && tr && lane == 0) tr[0] = clock64();
     uint32_t r0[32], r1[32];
     if (nchunks > 0) tmem_ld32(tcol, r0);
     if (nchunks > 1) tmem_ld32(tcol + 32u, r1);
@@ -900,30 +930,37 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
         tmem_ld_wait(r0);
         tmem_ld_wait(r1);
     }
+    if (TRACE && tr && lane == 0) tr[1] = clock_after(r0[0] ^ r0[31] ^ r1[31]);
     tc_fence_before();
     __syncwarp();
     if (lane == 0) {
         if (local_release) mbar_arrive_relaxed(tempty);
         else mbar_arrive_cluster(tempty);
+        if (TRACE && tr) tr[2] = clock64();
     }
     if (dflags & FASTED_JOIN_DIAG_LOADONLY) return;
     if (fast) {
         const uint32_t all = and_tree32(r0) & and_tree32(r1);
-        if (!__any_sync(0xffffffffu, (int)all >= 0)) return;
+        const bool any = __any_sync(0xffffffffu, (int)all >= 0);
+        if (TRACE && tr && lane == 0) {
+            tr[4] = clock64();
+            tr[7] = any ? 1ull : 0ull;
+        }
+        if (!any) return;
     }
     if (dflags & FASTED_JOIN_DIAG_NOSLOW) return;
+    if (TRACE && tr && lane == 0) tr[5] = clock64();
     if (nchunks > 0) hit_push<NHIT>(reg, smem_raw, raw, hq, r0, jb, i, iw, row_ok, lane);
     if (nchunks > 1) hit_push<NHIT>(reg, smem_raw, raw, hq, r1, jb + 32, i, iw, row_ok, lane);
+    if (TRACE && tr && lane == 0) tr[6] = clock64();
 }
 
 // Queue barriers and counters (thread 0, before the CTA-wide barrier).
 template <int NHIT>
 __device__ __forceinline__ void hit_init(uint32_t reg, uint8_t* smem_raw, uint32_t raw) {
     for (int q = 0; q < NHIT; q++) {
-        for (uint32_t sl = 0; sl < (uint32_t)HitQ<NHIT>::Q; sl++) {
+        for (uint32_t sl = 0; sl < (uint32_t)HitQ<NHIT>::Q; sl++)
             mbar_init(HitQ<NHIT>::full(reg, q, sl), 1);
-            mbar_init(HitQ<NHIT>::full(reg, q, sl) + 8u, 32);   // empty
-        }
         *reinterpret_cast<volatile uint32_t*>(smem_raw + (HitQ<NHIT>::tail(reg, q) - raw)) = 0u;
         *reinterpret_cast<volatile uint32_t*>(smem_raw + (HitQ<NHIT>::head(reg, q) - raw)) = 0u;
     }
@@ -944,16 +981,24 @@ __device__ __forceinline__ void hit_end(uint32_t reg, uint8_t* smem_raw, uint32_
 
 // A hit warp's whole life: pop queue hq in order until `producers` END
 // entries, test each row transposed, write the records.
-template <int NHIT>
+template <int NHIT, bool TRACE = false>
 __device__ __forceinline__ void hit_warp_loop(const JoinArgs& a, uint32_t reg, int hq,
                                               int producers, int lane, bool spin) {
     using H = HitQ<NHIT>;
     StagedWriter<H::HWS> wr;
     writer_init(wr, reg + (uint32_t)hq * 2u * H::HWS * 16u);
+    unsigned long long* trh =
+        (TRACE && a.trace && blockIdx.x == 0 && hq < TRACE_HIT_WARPS)
+            ? a.trace + TRACE_HIT_BASE + (unsigned long long)hq * TRACE_HIT_ENTRIES * 4
+            : nullptr;
     int ends = 0;
     for (uint32_t idx = 0; ends < producers; idx++) {
         const uint32_t sl = idx % H::Q;
+        unsigned long long* te = (TRACE && trh && idx < (uint32_t)TRACE_HIT_ENTRIES)
+                                     ? trh + 4u * idx : nullptr;
+        if (TRACE && te && lane == 0) te[0] = clock64();
         mbar_wait2(H::full(reg, hq, sl), (idx / H::Q) & 1u, spin);
+        if (TRACE && te && lane == 0) te[1] = clock64();
         const uint4 m = ld_shared_v4(H::meta(reg, hq, sl));
         if (m.x == HIT_ROW) {
             const uint32_t v = ld_shared_u32(H::data(reg, hq, sl) + 4u * (uint32_t)lane);
@@ -973,9 +1018,12 @@ __device__ __forceinline__ void hit_warp_loop(const JoinArgs& a, uint32_t reg, i
         } else {
             ends++;
         }
-        mbar_arrive(H::full(reg, hq, sl) + 8u);   // this lane is done with the slot
-        __syncwarp();
+        __syncwarp();   // every lane's reads of the slot are done
         if (lane == 0) st_release_shared(H::head(reg, hq), idx + 1u);
+        if (TRACE && te && lane == 0) {
+            te[2] = clock64();
+            te[3] = (unsigned long long)m.x;
+        }
     }
     writer_finish(wr, a);
 }
@@ -1840,8 +1888,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         __syncwarp();
     } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
         // ---------------- hit warp
-        hit_warp_loop<NHIT>(a, bars + C::BAR_REGION, warp - FIRST_EPI_WARP - NEPI, NEPI / NHIT,
-                            lane, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
+        hit_warp_loop<NHIT, TRACE>(a, bars + C::BAR_REGION, warp - FIRST_EPI_WARP - NEPI,
+                                   NEPI / NHIT, lane, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
     } else {
         // ---------------- epilogue
         constexpr int NSPLIT = NEPI / 4;
@@ -1900,11 +1948,11 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                     tr = a.trace + 2 * TRACE_TILES +
                          8 * (lt * TRACE_EPI_WARPS + (warp - FIRST_EPI_WARP));
                 if constexpr (NHIT > 0)
-                    res_epi_tile_hit<CG, TBN, NSPLIT, NHIT>(
+                    res_epi_tile_hit<CG, TBN, NSPLIT, NHIT, TRACE>(
                         a, bars + C::BAR_REGION, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT,
                         tcol0 + buf * TBN, tfull0 + 8u * buf, aph, buf ? release1 : release0,
                         local_release, spin, dflags, nchunks, fast, jb, i, iw, row_ok,
-                        (uint32_t)lane);
+                        (uint32_t)lane, tr);
                 else
                     res_epi_tile<CG, TBN, NSPLIT, TRACE>(
                         a, wr, tcol0 + buf * TBN, tfull0 + 8u * buf, aph,
@@ -2356,7 +2404,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     using C = ResCfg<CG, TBN>;
     constexpr int SMEM_MAX = 227 * 1024;
 #ifdef FASTED_EXPERIMENTS
-    constexpr bool CAN_TRACE = CG == 2 && TBN == 256 && NEPI == 16 && NHIT == 0;
+    constexpr bool CAN_TRACE = CG == 2 && TBN == 256 && NEPI == 16;
 #else
     constexpr bool CAN_TRACE = false;   // the clock64 timeline exists in libfasted_exp.so only
 #endif
@@ -2365,7 +2413,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     PerDeviceOnce* once = &attr_once;
     if constexpr (CAN_TRACE) {
         if (a.trace) {
-            kern = join_tc_res_kernel<CG, TBN, NEPI, true, 0>;
+            kern = join_tc_res_kernel<CG, TBN, NEPI, true, NHIT>;
             once = &attr_once_trace;
         }
     }

@@ -199,6 +199,45 @@ norms_kernel(const __half* __restrict__ v16, int64_t n_pad, int64_t d_pad,
 
 using namespace fasted;
 
+// Stream-ordered quantise: no allocation, no synchronisation.  The caller
+// initialises *first_overflow_dev to ~0 (all ones) before the launch; the
+// kernel atomicMin's the flat index of every overflowing value into it.
+extern "C" int fasted_quantize_async(const float* x, int64_t n, int64_t d, uint16_t* values16,
+                                     int64_t n_pad, int64_t d_pad, float* norms,
+                                     unsigned long long* first_overflow_dev, void* stream) {
+    if (!x || !values16 || !norms || !first_overflow_dev || n < 1 || d < 1 || n_pad < n ||
+        d_pad < d || (d_pad % 8) != 0) {
+        set_error("fasted_quantize: bad arguments (n=%lld d=%lld n_pad=%lld d_pad=%lld)",
+                  (long long)n, (long long)d, (long long)n_pad, (long long)d_pad);
+        return FASTED_ERR_ARGUMENT;
+    }
+    cudaStream_t s = as_stream(stream);
+    const int64_t blocks = (n_pad + QROWS - 1) / QROWS;
+    // TMA form: 16-byte row pitch and base, 16-byte aligned output rows
+    const bool tma = (d % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
+                     (reinterpret_cast<uintptr_t>(values16) & 15u) == 0 && n <= 0x7fffffffLL;
+    CUtensorMap map;
+    if (tma && encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, (uint64_t)d, (uint64_t)n,
+                         (uint64_t)d * 4, QCOLS, QROWS, CU_TENSOR_MAP_SWIZZLE_128B) == FASTED_OK) {
+        static PerDeviceOnce attr_once;
+        cudaError_t e = attr_once.run([&] {
+            return cudaFuncSetAttribute(quantize_tma_kernel,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
+        });
+        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(quantize)");
+        quantize_tma_kernel<<<(unsigned)blocks, QROWS, QSMEM, s>>>(
+            map, n, d, reinterpret_cast<__half*>(values16), n_pad, d_pad, norms,
+            first_overflow_dev);
+        FASTED_CHECK_LAUNCH("quantize_tma_kernel");
+    } else {
+        quantize_kernel<<<(unsigned)blocks, QROWS, 0, s>>>(
+            x, n, d, reinterpret_cast<__half*>(values16), n_pad, d_pad, norms,
+            first_overflow_dev);
+        FASTED_CHECK_LAUNCH("quantize_kernel");
+    }
+    return FASTED_OK;
+}
+
 extern "C" int fasted_quantize(const float* x, int64_t n, int64_t d, uint16_t* values16,
                                int64_t n_pad, int64_t d_pad, float* norms,
                                int64_t* first_overflow_host, void* stream) {
@@ -214,26 +253,10 @@ extern "C" int fasted_quantize(const float* x, int64_t n, int64_t d, uint16_t* v
     cudaError_t e = cudaMallocAsync(&flag, sizeof(unsigned long long), s);
     if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(overflow flag)");
     cudaMemsetAsync(flag, 0xff, sizeof(unsigned long long), s);
-    const int64_t blocks = (n_pad + QROWS - 1) / QROWS;
-    // TMA form: 16-byte row pitch and base, 16-byte aligned output rows
-    const bool tma = (d % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 15u) == 0 &&
-                     (reinterpret_cast<uintptr_t>(values16) & 15u) == 0 && n <= 0x7fffffffLL;
-    CUtensorMap map;
-    if (tma && encode_2d(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, (uint64_t)d, (uint64_t)n,
-                         (uint64_t)d * 4, QCOLS, QROWS, CU_TENSOR_MAP_SWIZZLE_128B) == FASTED_OK) {
-        static PerDeviceOnce attr_once;
-        e = attr_once.run([&] {
-            return cudaFuncSetAttribute(quantize_tma_kernel,
-                                        cudaFuncAttributeMaxDynamicSharedMemorySize, QSMEM);
-        });
-        if (e != cudaSuccess) return cuda_status(e, "cudaFuncSetAttribute(quantize)");
-        quantize_tma_kernel<<<(unsigned)blocks, QROWS, QSMEM, s>>>(
-            map, n, d, reinterpret_cast<__half*>(values16), n_pad, d_pad, norms, flag);
-        FASTED_CHECK_LAUNCH("quantize_tma_kernel");
-    } else {
-        quantize_kernel<<<(unsigned)blocks, QROWS, 0, s>>>(
-            x, n, d, reinterpret_cast<__half*>(values16), n_pad, d_pad, norms, flag);
-        FASTED_CHECK_LAUNCH("quantize_kernel");
+    const int st = fasted_quantize_async(x, n, d, values16, n_pad, d_pad, norms, flag, stream);
+    if (st != FASTED_OK) {
+        cudaFreeAsync(flag, s);
+        return st;
     }
     unsigned long long h = ~0ull;
     cudaMemcpyAsync(&h, flag, sizeof(h), cudaMemcpyDeviceToHost, s);

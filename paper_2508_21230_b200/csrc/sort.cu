@@ -355,6 +355,7 @@ __device__ bool rank_sort_segment(const uint32_t* sj, const float* sd, uint32_t 
         const uint32_t a = threadIdx.x < (uint32_t)nw ? S.red[threadIdx.x] : 0xffffffffu;
         const uint32_t b = threadIdx.x < (uint32_t)nw ? S.red[32 + threadIdx.x] : 0u;
         const uint32_t am = warp_min_u32(a), bm = warp_max_u32(b);
+        __syncwarp();   // every lane's read of red[lane] before lane 0 overwrites red[0..1]
         if (threadIdx.x == 0) {
             S.red[0] = am;
             S.red[1] = bm;

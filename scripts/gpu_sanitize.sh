@@ -8,7 +8,9 @@ cat > /tmp/san.py <<'PY'
 import sys, os, numpy as np
 sys.path.insert(0, os.getcwd())
 import paper_2508_21230_b200 as F
-from paper_2508_21230_b200 import engine
+from paper_2508_21230_b200 import _lib, engine
+# the FASTED_* overrides below exist only in the experiment build
+_lib.LIB_PATH = _lib.EXP_LIB_PATH
 for n, d, eps in ((2000, 200, 5.4), (1500, 520, 8.6), (3000, 64, 2.6), (1500, 384, 7.7),
                   (1000, 512, 8.6)):
     hd = F.to_half(F.generate_synthetic(n, d, seed=n))

@@ -22,7 +22,8 @@ _lib.LIB_PATH = os.path.abspath(os.environ.get("FASTED_LIB", _lib.EXP_LIB_PATH))
 
 TRACE = 65536
 TT, NW = 256, 16
-WORDS = TT * (2 + 8 * NW)
+HW, HE = 2, 512                       # hit warps traced, entries each
+WORDS = TT * (2 + 8 * NW) + HW * HE * 4
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "C3"
 rows = int(sys.argv[2]) if len(sys.argv) > 2 else 148 * 256 * 2
@@ -49,7 +50,8 @@ for fl in extra:
     ms = e0.elapsed_time(e1)
     tr = rec.view(torch.int64).flatten()[-WORDS:].cpu().numpy().astype(np.int64)
     mma = tr[:2 * TT].reshape(TT, 2)
-    epi = tr[2 * TT:].reshape(TT, NW, 8)
+    epi = tr[2 * TT:TT * (2 + 8 * NW)].reshape(TT, NW, 8)
+    hit = tr[TT * (2 + 8 * NW):].reshape(HW, HE, 4)
     lo = 16
     t0 = mma[lo:, 0]
     period = np.diff(t0)
@@ -95,6 +97,24 @@ for fl in extra:
         print(f"  arrived -> tile done (rare)  {q(e[:, 3] - e[:, 2])}")
         nr = epi[lo:][~rare]
         print(f"  arrived -> tile done (none)  {q(nr[:, 3] - nr[:, 2])}")
+    # which epilogue warps see tfull late: per warp (warp index 2 + w, SMSP
+    # (2 + w) % 4) the median over tiles of (its tfull stamp - the earliest)
+    late = np.median(tf - tf.min(axis=1, keepdims=True), axis=0)
+    print("tfull lateness per epi warp (median cycles after the first warp):")
+    print("  " + " ".join(f"w{2 + w}:{late[w]:.0f}" for w in range(NW)))
+    if hit[:, :, 2].any():
+        for h in range(HW):
+            e = hit[h]
+            e = e[(e[:, 2] > 0) & (e[:, 1] > 0)]
+            if len(e) < 32:
+                continue
+            e = e[16:]
+            span = e[-1, 2] - e[0, 0]
+            busy = (e[:, 2] - e[:, 1]).sum()
+            print(f"hit warp {h}: {len(e)} entries over {span} cycles "
+                  f"({span / len(e):.0f} cycles per entry), busy {100.0 * busy / span:.0f}%")
+            print(f"  wait for entry               {q(e[:, 1] - e[:, 0])}")
+            print(f"  process entry                {q(e[:, 2] - e[:, 1])}")
     print("tiles 40..47 (cycles rel. MMA start of tile 40):")
     base = mma[40, 0]
     for t in range(40, 48):

@@ -162,7 +162,7 @@ def test_bench_command_sweep(tmp_path):
                                                           (8192, 64), (8192, 200)]
     for r in rows:
         assert float(r["distance_tflops"]) > 0 and int(r["pairs"]) >= int(r["n"])
-        assert r["kernel"].startswith("join_tc")
+        assert "join_tc" in r["kernel"]
         assert int(r["d_padded"]) % 16 == 0
     man = json.loads((tmp_path / "b.json").read_text())
     assert len(man["runs"]) == 4

@@ -64,7 +64,7 @@ def test_two_process_shards_equal_single_process():
 
     import paper_2508_21230_b200 as F
 
-    n, d, eps = 20000, 96, 2.55
+    n, d, eps = 20000, 128, 3.8
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
