@@ -37,13 +37,25 @@ enum {
     // attribution of the augment step (results NOT valid): skip the
     // kind::tf32 augment MMA / issue it as a kind::f16 MMA instead
     FASTED_JOIN_DIAG_NOAUG = 524288,
-    FASTED_JOIN_DIAG_AUGF16 = 1048576
+    FASTED_JOIN_DIAG_AUGF16 = 1048576,
+    // hit-warp attribution (results NOT valid): producers push the entry's
+    // metadata only / hit warps consume entries without testing or writing
+    FASTED_JOIN_DIAG_HITMETA = 2097152,
+    FASTED_JOIN_DIAG_HITSKIP = 4194304,
+    // resident kernel: the producer arrives on the B stages' full barriers
+    // without loading them (MMA + handshakes alone; results NOT valid)
+    FASTED_JOIN_DIAG_NOTMA = 8388608,
+    // resident CTA pair: the peer CTA's epilogue warps do not release the
+    // accumulator (tempty counts the leader's warps only; results NOT valid)
+    FASTED_JOIN_DIAG_NOREMOTE = 16777216
 };
 constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA | FASTED_JOIN_DIAG_LOADONLY |
     FASTED_JOIN_DIAG_NOSLOW | FASTED_JOIN_DIAG_SPIN | FASTED_JOIN_DIAG_LDX64 |
     FASTED_JOIN_DIAG_AEVL | FASTED_JOIN_DIAG_TRACE | FASTED_JOIN_DIAG_RARE_LM |
-    FASTED_JOIN_DIAG_RARE_ROWS | FASTED_JOIN_DIAG_NOAUG | FASTED_JOIN_DIAG_AUGF16;
+    FASTED_JOIN_DIAG_RARE_ROWS | FASTED_JOIN_DIAG_NOAUG | FASTED_JOIN_DIAG_AUGF16 |
+    FASTED_JOIN_DIAG_HITMETA | FASTED_JOIN_DIAG_HITSKIP | FASTED_JOIN_DIAG_NOTMA |
+    FASTED_JOIN_DIAG_NOREMOTE;
 
 inline int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -73,7 +85,11 @@ enum {
     FASTED_JOIN_DIAG_RARE_LM = 0,
     FASTED_JOIN_DIAG_RARE_ROWS = 0,
     FASTED_JOIN_DIAG_NOAUG = 0,
-    FASTED_JOIN_DIAG_AUGF16 = 0
+    FASTED_JOIN_DIAG_AUGF16 = 0,
+    FASTED_JOIN_DIAG_HITMETA = 0,
+    FASTED_JOIN_DIAG_HITSKIP = 0,
+    FASTED_JOIN_DIAG_NOTMA = 0,
+    FASTED_JOIN_DIAG_NOREMOTE = 0
 };
 
 #endif

@@ -726,7 +726,7 @@ __device__ __forceinline__ void res_epi_tile(const JoinArgs& a, W& wr, uint32_t 
     __syncwarp();
     if (lane == 0) {
         if (local_release) mbar_arrive_relaxed(tempty);
-        else mbar_arrive_cluster(tempty);
+        else if (!(dflags & FASTED_JOIN_DIAG_NOREMOTE)) mbar_arrive_cluster(tempty);
         if (TRACE && tr) tr[2] = clock64();
     }
     if (dflags & FASTED_JOIN_DIAG_LOADONLY) return;
@@ -814,8 +814,13 @@ __device__ __forceinline__ uint32_t cluster_addr(uint32_t cta_addr) {
     return r;
 }
 
+// Relaxed: the entry's bytes travel with st.async and complete the phase
+// through complete_tx, so the arrive orders nothing -- a (default) release
+// arrive would first wait for this thread's earlier memory operations, e.g.
+// a CTA-pair epilogue warp's remote accumulator-release arrive (DSMEM).
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+    asm volatile("mbarrier.arrive.expect_tx.relaxed.cta.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                 "r"(bytes)
                  : "memory");
 }
 
@@ -879,7 +884,7 @@ __device__ __forceinline__ void hit_put(uint32_t reg, int q, uint32_t idx, uint3
 template <int NHIT>
 __device__ __forceinline__ void hit_push(uint32_t reg, uint8_t* smem_raw, uint32_t raw, int q,
                                          const uint32_t (&r)[32], int jb, int i, int iw,
-                                         bool row_ok, uint32_t lane) {
+                                         bool row_ok, uint32_t lane, int dflags = 0) {
     const bool diag = (jb < iw + 32) && (iw < jb + 32);
     uint32_t rows, selfmask = 0u;
     if (!diag) {
@@ -900,7 +905,7 @@ __device__ __forceinline__ void hit_push(uint32_t reg, uint8_t* smem_raw, uint32
     b0 = __shfl_sync(0xffffffffu, b0, 0);
     if ((rows >> lane) & 1u)
         hit_put<NHIT>(reg, q, b0 + (uint32_t)__popc(rows & lanemask_lt()), HIT_ROW, (uint32_t)i,
-                      (uint32_t)jb, 0u, r, true);
+                      (uint32_t)jb, 0u, r, !(dflags & FASTED_JOIN_DIAG_HITMETA));
     if (selfmask && lane == 0)
         hit_put<NHIT>(reg, q, b0 + (uint32_t)__popc(rows), HIT_SELF, (uint32_t)iw, (uint32_t)jb,
                       selfmask, r, false);
@@ -935,7 +940,7 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
     __syncwarp();
     if (lane == 0) {
         if (local_release) mbar_arrive_relaxed(tempty);
-        else mbar_arrive_cluster(tempty);
+        else if (!(dflags & FASTED_JOIN_DIAG_NOREMOTE)) mbar_arrive_cluster(tempty);
         if (TRACE && tr) tr[2] = clock64();
     }
     if (dflags & FASTED_JOIN_DIAG_LOADONLY) return;
@@ -950,8 +955,9 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
     }
     if (dflags & FASTED_JOIN_DIAG_NOSLOW) return;
     if (TRACE && tr && lane == 0) tr[5] = clock64();
-    if (nchunks > 0) hit_push<NHIT>(reg, smem_raw, raw, hq, r0, jb, i, iw, row_ok, lane);
-    if (nchunks > 1) hit_push<NHIT>(reg, smem_raw, raw, hq, r1, jb + 32, i, iw, row_ok, lane);
+    if (nchunks > 0) hit_push<NHIT>(reg, smem_raw, raw, hq, r0, jb, i, iw, row_ok, lane, dflags);
+    if (nchunks > 1)
+        hit_push<NHIT>(reg, smem_raw, raw, hq, r1, jb + 32, i, iw, row_ok, lane, dflags);
     if (TRACE && tr && lane == 0) tr[6] = clock64();
 }
 
@@ -1000,7 +1006,8 @@ __device__ __forceinline__ void hit_warp_loop(const JoinArgs& a, uint32_t reg, i
         mbar_wait2(H::full(reg, hq, sl), (idx / H::Q) & 1u, spin);
         if (TRACE && te && lane == 0) te[1] = clock64();
         const uint4 m = ld_shared_v4(H::meta(reg, hq, sl));
-        if (m.x == HIT_ROW) {
+        if ((FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_HITSKIP) && m.x != HIT_END) {
+        } else if (m.x == HIT_ROW) {
             const uint32_t v = ld_shared_u32(H::data(reg, hq, sl) + 4u * (uint32_t)lane);
             const int64_t is = (int64_t)m.y, j = (int64_t)m.z + lane;
             const bool hit = (int)v >= 0 && j < a.n_logical && j != is && (!a.symmetric || j > is);
@@ -1713,7 +1720,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         }
         for (int b = 0; b < NACC; b++) {
             mbar_init(tfull_bar(b), 1);
-            mbar_init(tempty_bar(b), NEPI * CG);
+            mbar_init(tempty_bar(b),
+                      (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOREMOTE) ? NEPI : NEPI * CG);
         }
         for (int b = 0; b < 2; b++) {
             mbar_init(afull_bar(b), 1);
@@ -1800,7 +1808,10 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                         const uint32_t st = sB + (uint32_t)s * C::STAGE_BYTES;
                         const uint32_t box_bytes =
                             C::BBOX * (BK * 2 + (last ? AUG_ROW_BYTES : 0));
-                        if (elect_one()) {
+                        const bool el = elect_one();
+                        if ((FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOTMA) != 0) {
+                            if (el && (CG == 1 || leader)) mbar_arrive(fb);
+                        } else if (el) {
                             if (CG == 1 || leader)
                                 mbar_expect_tx(fb, (uint32_t)nbox_pair * box_bytes);
                             for (int x = 0; x < nbox; x++) {

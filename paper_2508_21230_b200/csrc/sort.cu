@@ -43,6 +43,9 @@ constexpr int BIG_MAX = 16384;                 // rank sort, large tier (~148 KB
 constexpr int RANK_THREADS = 256;              // small tier (several CTAs per SM)
 constexpr int BIG_THREADS = 1024;              // large tier and long rows (one CTA per SM)
 constexpr int RANK_BUCKET_MAX = 64;            // a fuller bucket: bitonic fallback
+constexpr int RANK_PER = 16;                   // records per thread held in registers
+static_assert(MID_MAX == RANK_THREADS * RANK_PER && BIG_MAX == BIG_THREADS * RANK_PER,
+              "each rank-sort tier holds one row segment in registers");
 constexpr int MID_THREADS = 512;
 constexpr int LONG_BLOCKS = 32;
 constexpr int LONG_THREADS = 512;
@@ -93,11 +96,40 @@ static size_t carve(void* base, int64_t n_rows, int64_t n_cols, SortWs* ws) {
     return off;
 }
 
+// The record array is read twice, once per pass, as a stream: its loads
+// carry an L2 evict_first policy so the 10s of GB flowing through L2 do not
+// evict the working sets the passes write into (the per-row counters and
+// cursors, and the row segments' partially written sectors -- with default
+// loads the scatter wrote 1.8x and read 1.4x the payload: sectors evicted
+// half-filled and merged in DRAM; profiles/round2/sort_launches_c5_s4096_r2.csv).
+__device__ __forceinline__ uint64_t stream_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;"
+                 : "=r"(v)
+                 : "l"(p), "l"(pol));
+    return v;
+}
+
 __global__ void hist_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
                             uint32_t* __restrict__ counts) {
+    const uint64_t pol = stream_policy();
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < count;
          p += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = rec[p].x;
+        const uint32_t i = ld_stream_u32(reinterpret_cast<const uint32_t*>(rec + p), pol);
         if (i) atomicAdd(&counts[i - 1 - row_begin], 1u);   // i == 0: unused slot
     }
 }
@@ -194,9 +226,10 @@ __global__ void scatter_kernel(const uint4* __restrict__ rec, uint64_t count, in
                                const unsigned long long* __restrict__ offsets,
                                uint32_t* __restrict__ cursor, uint32_t* __restrict__ tj,
                                float* __restrict__ td) {
+    const uint64_t pol = stream_policy();
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < count;
          p += (uint64_t)gridDim.x * blockDim.x) {
-        const uint4 v = rec[p];
+        const uint4 v = ld_stream_u4(rec + p, pol);
         if (v.x == 0) continue;
         const int64_t r = (int64_t)v.x - 1 - row_begin;
         const unsigned long long pos = offsets[r] + atomicAdd(&cursor[r], 1u);
@@ -337,11 +370,22 @@ __device__ uint32_t block_scan_excl(uint32_t* a, uint32_t n, uint32_t* red) {
 template <int CAP>
 __device__ bool rank_sort_segment(const uint32_t* sj, const float* sd, uint32_t L, uint32_t* dj,
                                   float* dd, uint32_t* di, uint32_t row1, RankSmem<CAP>& S) {
+    // the row is read from global memory ONCE, into registers (element
+    // threadIdx.x + k * blockDim.x in slot k; every launch of a CAP tier
+    // has CAP / blockDim.x == RANK_PER), then min/max, bucket counts and the
+    // bucket scatter all work from the registers
+    uint32_t vj[RANK_PER];
+    float vd[RANK_PER];
     uint32_t mn = 0xffffffffu, mx = 0u;
-    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
-        const uint32_t j = sj[e];
-        mn = min(mn, j);
-        mx = max(mx, j);
+#pragma unroll
+    for (int k = 0; k < RANK_PER; k++) {
+        const uint32_t e = threadIdx.x + (uint32_t)k * blockDim.x;
+        vj[k] = e < L ? sj[e] : 0u;
+        vd[k] = e < L ? sd[e] : 0.0f;
+        if (e < L) {
+            mn = min(mn, vj[k]);
+            mx = max(mx, vj[k]);
+        }
     }
     mn = warp_min_u32(mn);
     mx = warp_max_u32(mx);
@@ -374,17 +418,21 @@ __device__ bool rank_sort_segment(const uint32_t* sj, const float* sd, uint32_t 
     };
     for (uint32_t b = threadIdx.x; b <= nb; b += blockDim.x) S.off[b] = 0u;
     __syncthreads();
-    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) atomicAdd(&S.off[bucket(sj[e])], 1u);
+#pragma unroll
+    for (int k = 0; k < RANK_PER; k++)
+        if (threadIdx.x + (uint32_t)k * blockDim.x < L) atomicAdd(&S.off[bucket(vj[k])], 1u);
     __syncthreads();
     const uint32_t fullest = block_scan_excl(S.off, nb, S.red);
     if (fullest > (uint32_t)RANK_BUCKET_MAX) return false;   // block-uniform
     for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) S.cur[b] = S.off[b];
     __syncthreads();
-    for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
-        const uint32_t j = sj[e];
-        const uint32_t p = atomicAdd(&S.cur[bucket(j)], 1u);
-        S.bj[p] = j;
-        S.bd[p] = sd[e];
+#pragma unroll
+    for (int k = 0; k < RANK_PER; k++) {
+        if (threadIdx.x + (uint32_t)k * blockDim.x < L) {
+            const uint32_t p = atomicAdd(&S.cur[bucket(vj[k])], 1u);
+            S.bj[p] = vj[k];
+            S.bd[p] = vd[k];
+        }
     }
     __syncthreads();   // every read of (sj, sd) done: dst may alias src
     for (uint32_t x = threadIdx.x; x < L; x += blockDim.x) {
