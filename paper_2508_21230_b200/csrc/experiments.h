@@ -47,7 +47,10 @@ enum {
     FASTED_JOIN_DIAG_NOTMA = 8388608,
     // resident CTA pair: the peer CTA's epilogue warps do not release the
     // accumulator (tempty counts the leader's warps only; results NOT valid)
-    FASTED_JOIN_DIAG_NOREMOTE = 16777216
+    FASTED_JOIN_DIAG_NOREMOTE = 16777216,
+    // hit warps: candidate rows with <= 3 hits travel as (mask, values)
+    // instead of all 32 words (results stay valid; A/B of the packing)
+    FASTED_JOIN_DIAG_HITPACK = 33554432
 };
 constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA | FASTED_JOIN_DIAG_LOADONLY |
@@ -55,7 +58,7 @@ constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_AEVL | FASTED_JOIN_DIAG_TRACE | FASTED_JOIN_DIAG_RARE_LM |
     FASTED_JOIN_DIAG_RARE_ROWS | FASTED_JOIN_DIAG_NOAUG | FASTED_JOIN_DIAG_AUGF16 |
     FASTED_JOIN_DIAG_HITMETA | FASTED_JOIN_DIAG_HITSKIP | FASTED_JOIN_DIAG_NOTMA |
-    FASTED_JOIN_DIAG_NOREMOTE;
+    FASTED_JOIN_DIAG_NOREMOTE | FASTED_JOIN_DIAG_HITPACK;
 
 inline int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -89,7 +92,8 @@ enum {
     FASTED_JOIN_DIAG_HITMETA = 0,
     FASTED_JOIN_DIAG_HITSKIP = 0,
     FASTED_JOIN_DIAG_NOTMA = 0,
-    FASTED_JOIN_DIAG_NOREMOTE = 0
+    FASTED_JOIN_DIAG_NOREMOTE = 0,
+    FASTED_JOIN_DIAG_HITPACK = 0
 };
 
 #endif

@@ -843,52 +843,67 @@ __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
     return v;
 }
 
-// One queue entry, written by one thread: wait until the slot's previous
-// lap was consumed, fill it, publish it (release arrive).
+// Wait until entry idx's slot is free: its previous lap (entry idx - Q) was
+// consumed.  The hit warp publishes its head counter (release, after all 32
+// lanes read the entry) and this acquire orders the refill after those
+// reads; `head_seen` caches the last reading (a lower bound of the head).
 template <int NHIT>
-__device__ __forceinline__ void hit_put(uint32_t reg, int q, uint32_t idx, uint32_t kind,
-                                        uint32_t i, uint32_t jb, uint32_t mask,
-                                        const uint32_t (&r)[32], bool with_data) {
+__device__ __forceinline__ void hit_slot_wait(uint32_t reg, int q, uint32_t idx,
+                                              uint32_t& head_seen) {
     using H = HitQ<NHIT>;
-    const uint32_t slot = idx % H::Q;
-    if (idx >= (uint32_t)H::Q) {
-        // the slot's previous lap (entry idx - Q) must be consumed: the hit
-        // warp publishes its head counter (release, after all 32 lanes read
-        // the entry) and this acquire orders the refill after those reads
-        if (ld_acquire_shared(H::head(reg, q)) + H::Q <= idx) {
+    if (head_seen + H::Q <= idx) {
+        head_seen = ld_acquire_shared(H::head(reg, q));
+        if (head_seen + H::Q <= idx) {
             const uint64_t t0 = global_timer();
-            while (ld_acquire_shared(H::head(reg, q)) + H::Q <= idx) {
+            while ((head_seen = ld_acquire_shared(H::head(reg, q))) + H::Q <= idx) {
                 __nanosleep(32);
                 if (global_timer() - t0 > 20000000000ull) __trap();
             }
         }
     }
+}
+
+// One queue entry, written by one thread: wait until the slot's previous
+// lap was consumed, fill it, publish it.  `creg`: the queue region's
+// shared::cluster address (mapped once per warp); `head_seen`: this
+// thread's last reading of the hit warp's head counter -- a lower bound of
+// it, so the counter is read again only when it cannot prove the slot free.
+template <int NHIT>
+__device__ __forceinline__ void hit_put(uint32_t reg, uint32_t creg, int q, uint32_t idx,
+                                        uint32_t kind, uint32_t i, uint32_t jb, uint32_t mask,
+                                        const uint32_t (&r)[32], bool with_data,
+                                        uint32_t& head_seen) {
+    using H = HitQ<NHIT>;
+    const uint32_t slot = idx % H::Q;
+    hit_slot_wait<NHIT>(reg, q, idx, head_seen);
     // The entry goes in with st.async (async proxy, completion counted in
     // bytes on the slot's full barrier): the consumer's wait returns once
     // the bytes landed, and the hand-off is the TMA-style one -- no generic
     // shared-memory store for a generic load on another warp to race with.
-    const uint32_t full = cluster_addr(H::full(reg, q, slot));
+    const uint32_t full = creg + (H::full(reg, q, slot) - reg);
     mbar_arrive_expect_tx(H::full(reg, q, slot), with_data ? 144u : 16u);
     if (with_data) {
-        const uint32_t d = cluster_addr(H::data(reg, q, slot));
+        const uint32_t d = creg + (H::data(reg, q, slot) - reg);
 #pragma unroll
         for (int k = 0; k < 8; k++)
             st_async_v4(d + 16u * k, make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]),
                         full);
     }
-    st_async_v4(cluster_addr(H::meta(reg, q, slot)), make_uint4(kind, i, jb, mask), full);
+    st_async_v4(creg + (H::meta(reg, q, slot) - reg), make_uint4(kind, i, jb, mask), full);
 }
 
 // Hand one 32-column chunk's candidate rows (and the diagonal's self pairs)
 // to hit warp q.  Warp-collective.
 template <int NHIT>
-__device__ __forceinline__ void hit_push(uint32_t reg, uint8_t* smem_raw, uint32_t raw, int q,
-                                         const uint32_t (&r)[32], int jb, int i, int iw,
-                                         bool row_ok, uint32_t lane, int dflags = 0) {
+__device__ __forceinline__ void hit_push(uint32_t reg, uint32_t creg, uint8_t* smem_raw,
+                                         uint32_t raw, int q, const uint32_t (&r)[32],
+                                         uint32_t and_r, int jb, int i, int iw, bool row_ok,
+                                         uint32_t lane, uint32_t& head_seen, int dflags = 0,
+                                         unsigned long long* trp = nullptr) {
     const bool diag = (jb < iw + 32) && (iw < jb + 32);
     uint32_t rows, selfmask = 0u;
     if (!diag) {
-        rows = __ballot_sync(0xffffffffu, (int)and_tree32(r) >= 0 && row_ok);
+        rows = __ballot_sync(0xffffffffu, (int)and_r >= 0 && row_ok);
     } else {
         // every row meets its own column here: candidates other than the self column
         uint32_t lm = hit_mask32(r);
@@ -903,19 +918,28 @@ __device__ __forceinline__ void hit_push(uint32_t reg, uint8_t* smem_raw, uint32
     if (lane == 0)
         b0 = atomicAdd(reinterpret_cast<unsigned*>(smem_raw + (HitQ<NHIT>::tail(reg, q) - raw)), k);
     b0 = __shfl_sync(0xffffffffu, b0, 0);
+    if (trp && lane == 0) trp[0] = clock64();
+    // each candidate lane hands its row over (eight 16-byte st.async + the
+    // metadata).  Measured alternatives, both slower at 1M x 128: the row
+    // transposed across the warp by 32 shuffles and stored with one
+    // warp-wide st.async (~1700 vs ~850 cycles per row), and (mask, <= 3
+    // hit values) picked by select trees (35.5 vs 32.4 ms per shard).
     if ((rows >> lane) & 1u)
-        hit_put<NHIT>(reg, q, b0 + (uint32_t)__popc(rows & lanemask_lt()), HIT_ROW, (uint32_t)i,
-                      (uint32_t)jb, 0u, r, !(dflags & FASTED_JOIN_DIAG_HITMETA));
+        hit_put<NHIT>(reg, creg, q, b0 + (uint32_t)__popc(rows & lanemask_lt()), HIT_ROW,
+                      (uint32_t)i, (uint32_t)jb, 0u, r, !(dflags & FASTED_JOIN_DIAG_HITMETA),
+                      head_seen);
     if (selfmask && lane == 0)
-        hit_put<NHIT>(reg, q, b0 + (uint32_t)__popc(rows), HIT_SELF, (uint32_t)iw, (uint32_t)jb,
-                      selfmask, r, false);
+        hit_put<NHIT>(reg, creg, q, b0 + (uint32_t)__popc(rows), HIT_SELF, (uint32_t)iw,
+                      (uint32_t)jb, selfmask, r, false, head_seen);
+    if (trp && lane == 0) trp[3] = clock_after(head_seen);
     __syncwarp();
 }
 
 // The resident epilogue tile with hit warps: drain, release, slice test, and
 // on a candidate only the hand-off.
 template <int CG, int TBN, int NSPLIT, int NHIT, bool TRACE = false>
-__device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg, uint8_t* smem_raw,
+__device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg, uint32_t creg,
+                                                 uint32_t& head_seen, uint8_t* smem_raw,
                                                  uint32_t raw, int hq, uint32_t tcol,
                                                  uint32_t tfull, uint32_t aph, uint32_t tempty,
                                                  bool local_release, bool spin, int dflags,
@@ -944,9 +968,9 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
         if (TRACE && tr) tr[2] = clock64();
     }
     if (dflags & FASTED_JOIN_DIAG_LOADONLY) return;
+    const uint32_t and0 = and_tree32(r0), and1 = and_tree32(r1);
     if (fast) {
-        const uint32_t all = and_tree32(r0) & and_tree32(r1);
-        const bool any = __any_sync(0xffffffffu, (int)all >= 0);
+        const bool any = __any_sync(0xffffffffu, (int)(and0 & and1) >= 0);
         if (TRACE && tr && lane == 0) {
             tr[4] = clock64();
             tr[7] = any ? 1ull : 0ull;
@@ -955,9 +979,12 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
     }
     if (dflags & FASTED_JOIN_DIAG_NOSLOW) return;
     if (TRACE && tr && lane == 0) tr[5] = clock64();
-    if (nchunks > 0) hit_push<NHIT>(reg, smem_raw, raw, hq, r0, jb, i, iw, row_ok, lane, dflags);
+    if (nchunks > 0)
+        hit_push<NHIT>(reg, creg, smem_raw, raw, hq, r0, and0, jb, i, iw, row_ok, lane, head_seen,
+                       dflags, (TRACE && tr) ? tr + 4 : nullptr);
     if (nchunks > 1)
-        hit_push<NHIT>(reg, smem_raw, raw, hq, r1, jb + 32, i, iw, row_ok, lane, dflags);
+        hit_push<NHIT>(reg, creg, smem_raw, raw, hq, r1, and1, jb + 32, i, iw, row_ok, lane,
+                       head_seen, dflags);
     if (TRACE && tr && lane == 0) tr[6] = clock64();
 }
 
@@ -980,7 +1007,9 @@ __device__ __forceinline__ void hit_end(uint32_t reg, uint8_t* smem_raw, uint32_
         const uint32_t idx = atomicAdd(
             reinterpret_cast<unsigned*>(smem_raw + (HitQ<NHIT>::tail(reg, hq) - raw)), 1u);
         uint32_t none[32];
-        hit_put<NHIT>(reg, hq, idx, HIT_END, 0u, 0u, 0u, none, false);
+        uint32_t head_seen = 0u;
+        hit_put<NHIT>(reg, cluster_addr(reg), hq, idx, HIT_END, 0u, 0u, 0u, none, false,
+                      head_seen);
     }
     __syncwarp();
 }
@@ -1038,7 +1067,7 @@ __device__ __forceinline__ void hit_warp_loop(const JoinArgs& a, uint32_t reg, i
 // epilogue_tile with hit warps (streaming/multicast kernels): drain,
 // release, slice test, hand candidate rows over.
 template <int CG, int TBN, int NSPLIT, int NHIT>
-__device__ __forceinline__ void epilogue_tile_hit(const JoinArgs& a, uint32_t reg,
+__device__ __forceinline__ void epilogue_tile_hit(const JoinArgs& a, uint32_t reg, uint32_t creg, uint32_t& head_seen,
                                                   uint8_t* smem_raw, uint32_t raw, int hq,
                                                   uint32_t tmem_base, uint32_t tempty,
                                                   int64_t row0, int64_t col0, int buf,
@@ -1071,16 +1100,17 @@ __device__ __forceinline__ void epilogue_tile_hit(const JoinArgs& a, uint32_t re
     }
     if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_LOADONLY) return;
     const int64_t jb = col0 + h * HALF;
+    const uint32_t and0 = and_tree32(r0), and1 = and_tree32(r1);
     if (nchunks == NCH && !((jb < iw + 32) && (iw < jb + HALF))) {
-        const uint32_t all = and_tree32(r0) & and_tree32(r1);
-        if (!__any_sync(0xffffffffu, (int)all >= 0)) return;
+        if (!__any_sync(0xffffffffu, (int)(and0 & and1) >= 0)) return;
     }
     if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOSLOW) return;
     if (nchunks > 0)
-        hit_push<NHIT>(reg, smem_raw, raw, hq, r0, (int)jb, (int)i, (int)iw, row_ok, (uint32_t)lane);
+        hit_push<NHIT>(reg, creg, smem_raw, raw, hq, r0, and0, (int)jb, (int)i, (int)iw, row_ok,
+                       (uint32_t)lane, head_seen);
     if (nchunks > 1)
-        hit_push<NHIT>(reg, smem_raw, raw, hq, r1, (int)jb + 32, (int)i, (int)iw, row_ok,
-                       (uint32_t)lane);
+        hit_push<NHIT>(reg, creg, smem_raw, raw, hq, r1, and1, (int)jb + 32, (int)i, (int)iw,
+                       row_ok, (uint32_t)lane, head_seen);
 }
 
 template <int CG, bool DIAG, int NEPI = NUM_EPI_WARPS, int NHIT = 0>
@@ -1302,6 +1332,8 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         StagedWriter<WST> wr;
         if constexpr (NHIT == 0)
             writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
+        const uint32_t hit_creg = NHIT > 0 ? cluster_addr(bars + BAR_BYTES) : 0u;
+        uint32_t head_seen = 0u;
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -1333,7 +1365,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             }
             if constexpr (NHIT > 0)
                 epilogue_tile_hit<CG, BN, NEPI / 4, NHIT>(
-                    a, bars + BAR_BYTES, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, tmem_base,
+                    a, bars + BAR_BYTES, hit_creg, head_seen, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, tmem_base,
                     tempty_bar(buf), row0, col0, buf, aph, q, h, lane, leader, tfull_bar(buf));
             else
                 epilogue_tile<CG, BN, NEPI / 4>(a, wr, tmem_base, tempty_bar(buf), row0, col0, buf,
@@ -1552,6 +1584,8 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         StagedWriter<WST> wr;
         if constexpr (NHIT == 0)
             writer_init(wr, bars + BAR_BYTES + (uint32_t)(warp - FIRST_EPI_WARP) * 2 * WST * 16);
+        const uint32_t hit_creg = NHIT > 0 ? cluster_addr(bars + BAR_BYTES) : 0u;
+        uint32_t head_seen = 0u;
         int lt = 0;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++lt) {
             int rt, ct;
@@ -1565,7 +1599,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const int buf = lt & 1;
             if constexpr (NHIT > 0)
                 epilogue_tile_hit<1, BN, NEPI / 4, NHIT>(
-                    a, bars + BAR_BYTES, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, tmem_base,
+                    a, bars + BAR_BYTES, hit_creg, head_seen, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, tmem_base,
                     tempty_bar(buf), row0, col0, buf, (uint32_t)(lt >> 1) & 1u, q, h, lane, true,
                     tfull_bar(buf));
             else
@@ -1928,6 +1962,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         // this warp's first column in tile 0 of the range
         const int jbase = (int)a.col_begin + h * HALF;
         const int col_end = (int)a.col_end;
+        const uint32_t hit_creg = NHIT > 0 ? cluster_addr(bars + C::BAR_REGION) : 0u;
+        uint32_t head_seen = 0u;
         int lt = 0;
         uint32_t buf = 0, aph = 0;
         for (int u = (int)unit0; u < (int)sch.units; u += (int)ustep) {
@@ -1960,7 +1996,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                          8 * (lt * TRACE_EPI_WARPS + (warp - FIRST_EPI_WARP));
                 if constexpr (NHIT > 0)
                     res_epi_tile_hit<CG, TBN, NSPLIT, NHIT, TRACE>(
-                        a, bars + C::BAR_REGION, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT,
+                        a, bars + C::BAR_REGION, hit_creg, head_seen, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT,
                         tcol0 + buf * TBN, tfull0 + 8u * buf, aph, buf ? release1 : release0,
                         local_release, spin, dflags, nchunks, fast, jb, i, iw, row_ok,
                         (uint32_t)lane, tr);

@@ -85,7 +85,8 @@ for fl in extra:
     print(f"epi: arrived -> tile done      {q(math)}")
     print(f"epi: tile done -> next tfull   {q(idle)}")
     print(f"last arrive -> MMA past tempty {q(wake)}")
-    rare = epi[lo:, :, 7] == 1
+    rare = epi[lo:, :, 7] >= 1
+    pushed = epi[lo:, :, 7] > 1     # hit-warp build: [4] after the tail atomic, [7] after the puts
     vote = epi[lo:, :, 4] - epi[lo:, :, 2]
     print(f"epi: arrived -> slice vote     {q(vote)}")
     if rare.any():
@@ -95,6 +96,13 @@ for fl in extra:
         print(f"  row loop (records appended)  {q(e[:, 6] - e[:, 5])}")
         print(f"  appended -> tile done        {q(e[:, 3] - e[:, 6])}")
         print(f"  arrived -> tile done (rare)  {q(e[:, 3] - e[:, 2])}")
+        if pushed.any():
+            e2 = epi[lo:][pushed]
+            e2 = e2[(e2[:, 4] > e2[:, 5]) & (e2[:, 7] > e2[:, 4]) & (e2[:, 6] >= e2[:, 7])]
+            if len(e2):
+                print(f"  push: start -> tail atomic   {q(e2[:, 4] - e2[:, 5])}")
+                print(f"  push: tail atomic -> puts    {q(e2[:, 7] - e2[:, 4])}")
+                print(f"  push: puts -> push end       {q(e2[:, 6] - e2[:, 7])}")
         nr = epi[lo:][~rare]
         print(f"  arrived -> tile done (none)  {q(nr[:, 3] - nr[:, 2])}")
     # which epilogue warps see tfull late: per warp (warp index 2 + w, SMSP

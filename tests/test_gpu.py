@@ -933,3 +933,29 @@ def test_c5_rows_at_full_column_range(oracle):
                              lambda i, j: oracle.pair_d2(hd.values, hd.norms, i, j))
         print("C5 row block", rb, rep)
         assert rep.ok, rep
+
+
+def test_engine_stats_fields():
+    """EngineStats (tiling.py:125-151) is filled from device measurements:
+    the H2D stage time is the copy's CUDA-event time (a host dataset with no
+    device copy must pay it: > 0 and at least the bytes at ~60 GB/s cannot be
+    faster than ~1/100 of a second here), kernel time below the wall time,
+    the FMA count is n_pad^2 d_pad, per-device phase reports present; a
+    dataset already resident (to_half's device cache) stages nothing."""
+    hd = F.to_half(F.generate_synthetic(40000, 256, seed=5), pin_host=True)
+    host = F.HalfDataset(hd.n_logical, hd.d_logical, hd.values, hd.norms)   # no device cache
+    st = F.EngineStats()
+    rs = F.self_join(host, 5.2, stats_out=st)
+    nbytes = hd.values.nbytes + hd.norms.nbytes
+    assert st.stage_seconds > 0 and nbytes / st.stage_seconds < 80e9, (st.stage_seconds, nbytes)
+    assert 0 < st.kernel_wall_seconds < st.wall_seconds
+    n_dev = -(-hd.n_padded // 128) * 128
+    assert st.fma_ops == n_dev * n_dev * hd.d_padded and st.tiles > 0
+    dev0 = st.per_device[0]
+    for k in ("chunks", "reruns", "sort_ms", "d2h_ms"):
+        assert k in dev0, dev0.keys()
+    assert dev0["d2h_ms"] > 0 and dev0["sort_ms"] >= 0
+    st2 = F.EngineStats()
+    rs2 = F.self_join(hd, 5.2, stats_out=st2)      # resident: nothing to stage
+    assert st2.stage_seconds == 0.0
+    assert rs.same_pairs(rs2)
