@@ -50,7 +50,11 @@ enum {
     FASTED_JOIN_DIAG_NOREMOTE = 16777216,
     // hit warps: candidate rows with <= 3 hits travel as (mask, values)
     // instead of all 32 words (results stay valid; A/B of the packing)
-    FASTED_JOIN_DIAG_HITPACK = 33554432
+    FASTED_JOIN_DIAG_HITPACK = 33554432,
+    // hit warps: queue entries written with generic shared stores and a
+    // release arrive on the slot's full barrier instead of st.async +
+    // complete_tx (results stay valid; A/B of the hand-off)
+    FASTED_JOIN_DIAG_GENERICQ = 67108864
 };
 constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA | FASTED_JOIN_DIAG_LOADONLY |
@@ -58,7 +62,7 @@ constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_AEVL | FASTED_JOIN_DIAG_TRACE | FASTED_JOIN_DIAG_RARE_LM |
     FASTED_JOIN_DIAG_RARE_ROWS | FASTED_JOIN_DIAG_NOAUG | FASTED_JOIN_DIAG_AUGF16 |
     FASTED_JOIN_DIAG_HITMETA | FASTED_JOIN_DIAG_HITSKIP | FASTED_JOIN_DIAG_NOTMA |
-    FASTED_JOIN_DIAG_NOREMOTE | FASTED_JOIN_DIAG_HITPACK;
+    FASTED_JOIN_DIAG_NOREMOTE | FASTED_JOIN_DIAG_HITPACK | FASTED_JOIN_DIAG_GENERICQ;
 
 inline int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -93,7 +97,8 @@ enum {
     FASTED_JOIN_DIAG_HITSKIP = 0,
     FASTED_JOIN_DIAG_NOTMA = 0,
     FASTED_JOIN_DIAG_NOREMOTE = 0,
-    FASTED_JOIN_DIAG_HITPACK = 0
+    FASTED_JOIN_DIAG_HITPACK = 0,
+    FASTED_JOIN_DIAG_GENERICQ = 0
 };
 
 #endif

@@ -181,6 +181,43 @@ __device__ __forceinline__ void mbar_wait2(uint32_t bar, uint32_t parity, bool s
     }
 }
 
+// Non-blocking phase test (mbarrier.test_wait: never suspends).
+__device__ __forceinline__ bool mbar_test_only(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+
+// The epilogue's accumulator wait.  sleep_ns == 0: mbar_wait2 (try_wait
+// with a suspend hint).  Otherwise a failed test sleeps sleep_ns in
+// __nanosleep: a try_wait-suspended warp is woken by other barrier traffic
+// every ~100 cycles and re-polls (ncu at 1M x 128: ~9 polls, ~70 issued
+// instructions per warp per tile), taking issue slots from the warps on
+// its SM sub-partition that are still working on the previous tile.
+__device__ __forceinline__ void epi_wait(uint32_t bar, uint32_t parity, bool spin,
+                                         uint32_t sleep_ns) {
+    if (sleep_ns == 0u) {
+        mbar_wait2(bar, parity, spin);
+        return;
+    }
+    if (mbar_test_only(bar, parity)) return;
+    const uint64_t t0 = global_timer();
+    uint32_t polls = 0;
+    while (!mbar_test_only(bar, parity)) {
+        __nanosleep(sleep_ns);
+        if (++polls == 64u) {
+            polls = 0;
+            if (global_timer() - t0 > 20000000000ull) __trap();
+        }
+    }
+}
+
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
@@ -697,14 +734,14 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
 template <int CG, int TBN, int NSPLIT, bool TRACE, typename W>
 __device__ __forceinline__ void res_epi_tile(const JoinArgs& a, W& wr, uint32_t tcol,
                                              uint32_t tfull, uint32_t aph, uint32_t tempty,
-                                             bool local_release, bool spin, int dflags,
-                                             int nchunks, bool fast, int64_t jb, int64_t i,
-                                             int64_t iw, bool row_ok, int lane,
+                                             bool local_release, bool spin, uint32_t sleep_ns,
+                                             int dflags, int nchunks, bool fast, int64_t jb,
+                                             int64_t i, int64_t iw, bool row_ok, int lane,
                                              unsigned long long* tr) {
     constexpr int HALF = TBN / NSPLIT;
     constexpr int NCH = HALF / 32;
     static_assert(NCH == 1 || NCH == 2 || NCH == 4, "a warp covers 32, 64 or 128 columns");
-    mbar_wait2(tfull, aph, spin);
+    epi_wait(tfull, aph, spin, sleep_ns);
     tc_fence_after();
     if (TRACE && tr && lane == 0) tr[0] = clock64();
     uint32_t r0[32], r1[32], r2[32], r3[32];
@@ -764,7 +801,10 @@ __device__ __forceinline__ void res_epi_tile(const JoinArgs& a, W& wr, uint32_t 
 // the entry with the slot's full mbarrier.
 template <int NHIT>
 struct HitQ {
-    static constexpr int Q = 16;                    // slots per queue
+#ifndef FASTED_HITQ_SLOTS
+#define FASTED_HITQ_SLOTS 16
+#endif
+    static constexpr int Q = FASTED_HITQ_SLOTS;     // slots per queue
     static constexpr int HWS = 64;                  // records per staging buffer (hit warp)
     static constexpr int WRITER_BYTES = NHIT * 2 * HWS * 16;
     static constexpr int DATA_BYTES = NHIT * Q * 128;
@@ -872,10 +912,26 @@ template <int NHIT>
 __device__ __forceinline__ void hit_put(uint32_t reg, uint32_t creg, int q, uint32_t idx,
                                         uint32_t kind, uint32_t i, uint32_t jb, uint32_t mask,
                                         const uint32_t (&r)[32], bool with_data,
-                                        uint32_t& head_seen) {
+                                        uint32_t& head_seen, bool generic = false,
+                                        unsigned long long* trs = nullptr) {
     using H = HitQ<NHIT>;
     const uint32_t slot = idx % H::Q;
     hit_slot_wait<NHIT>(reg, q, idx, head_seen);
+#ifdef FASTED_TRACE_SLOT
+    if (trs) trs[2] = clock_after(head_seen);   // slot known free (trace experiment)
+#endif
+    if (generic) {   // FASTED_JOIN_DIAG_GENERICQ: plain stores + a release arrive
+        if (with_data) {
+            const uint32_t d = H::data(reg, q, slot);
+#pragma unroll
+            for (int k = 0; k < 8; k++)
+                st_shared_v4(d + 16u * k,
+                             make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]));
+        }
+        st_shared_v4(H::meta(reg, q, slot), make_uint4(kind, i, jb, mask));
+        mbar_arrive(H::full(reg, q, slot));
+        return;
+    }
     // The entry goes in with st.async (async proxy, completion counted in
     // bytes on the slot's full barrier): the consumer's wait returns once
     // the bytes landed, and the hand-off is the TMA-style one -- no generic
@@ -927,10 +983,11 @@ __device__ __forceinline__ void hit_push(uint32_t reg, uint32_t creg, uint8_t* s
     if ((rows >> lane) & 1u)
         hit_put<NHIT>(reg, creg, q, b0 + (uint32_t)__popc(rows & lanemask_lt()), HIT_ROW,
                       (uint32_t)i, (uint32_t)jb, 0u, r, !(dflags & FASTED_JOIN_DIAG_HITMETA),
-                      head_seen);
+                      head_seen, (dflags & FASTED_JOIN_DIAG_GENERICQ) != 0, trp);
     if (selfmask && lane == 0)
         hit_put<NHIT>(reg, creg, q, b0 + (uint32_t)__popc(rows), HIT_SELF, (uint32_t)iw,
-                      (uint32_t)jb, selfmask, r, false, head_seen);
+                      (uint32_t)jb, selfmask, r, false, head_seen,
+                      (dflags & FASTED_JOIN_DIAG_GENERICQ) != 0);
     if (trp && lane == 0) trp[3] = clock_after(head_seen);
     __syncwarp();
 }
@@ -942,14 +999,14 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
                                                  uint32_t& head_seen, uint8_t* smem_raw,
                                                  uint32_t raw, int hq, uint32_t tcol,
                                                  uint32_t tfull, uint32_t aph, uint32_t tempty,
-                                                 bool local_release, bool spin, int dflags,
-                                                 int nchunks, bool fast, int jb, int i, int iw,
-                                                 bool row_ok, uint32_t lane,
-                                                 unsigned long long* tr = nullptr) {
+                                                 bool local_release, bool spin,
+                                                 uint32_t sleep_ns, int dflags, int nchunks,
+                                                 bool fast, int jb, int i, int iw, bool row_ok,
+                                                 uint32_t lane, unsigned long long* tr = nullptr) {
     constexpr int HALF = TBN / NSPLIT;
     constexpr int NCH = HALF / 32;
     static_assert(NCH == 2, "hit-warp epilogue: 64 columns per warp");
-    mbar_wait2(tfull, aph, spin);
+    epi_wait(tfull, aph, spin, sleep_ns);
     tc_fence_after();
     if (TRACE && tr && lane == 0) tr[0] = clock64();
     uint32_t r0[32], r1[32];
@@ -985,7 +1042,9 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
     if (nchunks > 1)
         hit_push<NHIT>(reg, creg, smem_raw, raw, hq, r1, and1, jb + 32, i, iw, row_ok, lane,
                        head_seen, dflags);
+#ifndef FASTED_TRACE_SLOT
     if (TRACE && tr && lane == 0) tr[6] = clock64();
+#endif
 }
 
 // Queue barriers and counters (thread 0, before the CTA-wide barrier).
@@ -1652,6 +1711,7 @@ struct ResSched {
     uint32_t a_buf_bytes;     // one A buffer: nkb k-blocks + augment rows, 1024-aligned
     int64_t units;            // row_tiles * nsegs
     int lanes;                // units in flight: CTA pairs (CTAs) launched
+    uint32_t epi_sleep_ns;    // epilogue accumulator wait backoff (0: suspend hint)
 };
 
 // Records per staging buffer in the resident kernel (tight shared memory):
@@ -1953,7 +2013,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         const uint32_t tcol0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * HALF);
         const bool local_release = CG == 1 || leader;
         const uint32_t release0 = local_release ? tempty_bar(0) : mapa_shared(tempty_bar(0), 0);
-        const uint32_t release1 = local_release ? tempty_bar(1) : mapa_shared(tempty_bar(1), 0);
+        // the two accumulator-release barriers are adjacent (tempty_bar(1) =
+        // tempty_bar(0) + 8), in the cluster window too: no per-buffer select
         const uint32_t tfull0 = tfull_bar(0);
         const int dflags = FASTED_DFLAGS(a);
         const bool spin = (dflags & FASTED_JOIN_DIAG_SPIN) != 0;
@@ -1997,14 +2058,14 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                 if constexpr (NHIT > 0)
                     res_epi_tile_hit<CG, TBN, NSPLIT, NHIT, TRACE>(
                         a, bars + C::BAR_REGION, hit_creg, head_seen, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT,
-                        tcol0 + buf * TBN, tfull0 + 8u * buf, aph, buf ? release1 : release0,
-                        local_release, spin, dflags, nchunks, fast, jb, i, iw, row_ok,
-                        (uint32_t)lane, tr);
+                        tcol0 + buf * TBN, tfull0 + 8u * buf, aph, release0 + 8u * buf,
+                        local_release, spin, sch.epi_sleep_ns, dflags, nchunks, fast, jb, i, iw,
+                        row_ok, (uint32_t)lane, tr);
                 else
                     res_epi_tile<CG, TBN, NSPLIT, TRACE>(
                         a, wr, tcol0 + buf * TBN, tfull0 + 8u * buf, aph,
-                        buf ? release1 : release0, local_release, spin, dflags, nchunks, fast, jb,
-                        i, iw, row_ok, lane, tr);
+                        release0 + 8u * buf, local_release, spin, sch.epi_sleep_ns, dflags,
+                        nchunks, fast, jb, i, iw, row_ok, lane, tr);
                 if (TRACE && tr && lane == 0) tr[3] = clock64();
                 buf ^= 1u;
                 aph ^= buf ^ 1u;   // phase flips after buffer 1
@@ -2486,6 +2547,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     sch.col_tiles = (int)((a.col_end - a.col_begin + TBN - 1) / TBN);
     // a segment of ~16K columns per unit: the A panel load is amortised over
     // many tiles and the units stay small enough to balance
+    sch.epi_sleep_ns = (uint32_t)FASTED_KNOB("FASTED_EPI_SLEEP_NS", 0);
     int seg = FASTED_KNOB("FASTED_SEG_TILES", 16384 / TBN);
     if (seg < 1) seg = 1;
     sch.nsegs = (sch.col_tiles + seg - 1) / seg;
@@ -2585,6 +2647,7 @@ static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUte
         if (e != cudaSuccess) return e;
     }
     ResSched sch;
+    sch.epi_sleep_ns = 0u;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.na = 2;
     sch.a_buf_bytes = 0;

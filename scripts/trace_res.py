@@ -103,6 +103,11 @@ for fl in extra:
                 print(f"  push: start -> tail atomic   {q(e2[:, 4] - e2[:, 5])}")
                 print(f"  push: tail atomic -> puts    {q(e2[:, 7] - e2[:, 4])}")
                 print(f"  push: puts -> push end       {q(e2[:, 6] - e2[:, 7])}")
+            if os.environ.get("TRACE_SLOT"):   # libfasted_exp_slot.so: [6] = slot known free
+                e3 = epi[lo:][pushed]
+                e3 = e3[(e3[:, 6] >= e3[:, 4]) & (e3[:, 7] >= e3[:, 6])]
+                print(f"  push: tail atomic -> slot ok {q(e3[:, 6] - e3[:, 4])}")
+                print(f"  push: slot ok -> puts issued {q(e3[:, 7] - e3[:, 6])}")
         nr = epi[lo:][~rare]
         print(f"  arrived -> tile done (none)  {q(nr[:, 3] - nr[:, 2])}")
     # which epilogue warps see tfull late: per warp (warp index 2 + w, SMSP
