@@ -122,6 +122,7 @@ template <int STAGE>
 struct StagedWriter {
     static_assert(WRITER_CHUNK % STAGE == 0, "chunk must hold whole staging buffers");
     static constexpr uint32_t kStage = STAGE;
+    static constexpr bool kDirect = false;
     unsigned long long base;    // first slot of the current chunk (~0: none open)
     uint32_t flushed;           // staging buffers shipped into the current chunk
     uint32_t fill;              // records in the current staging buffer
@@ -236,6 +237,69 @@ __device__ __forceinline__ void writer_finish(StagedWriter<STAGE>& w, const Join
         }
         if (lane_id() == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
         __syncwarp();
+    }
+    if (lane_id() == 0 && w.total) atomicAdd(a.count, w.total);
+}
+
+// Direct pair writer (the resident kernel's sparse-output form): PairWriter's
+// chunk protocol, each record one 16-byte global store with an L2
+// evict_first hint straight from the epilogue warp's registers -- no shared
+// memory on the hit path.  The shared-memory staging and hand-off round trips
+// wait behind the tensor core's operand reads from the same shared memory
+// (profiles/round2/c3_session3_epilogue_analysis.txt); at ~1 pair per 10^4
+// examined the uncoalesced stores cost nothing measurable in bandwidth.
+struct DirectWriter {
+    static constexpr bool kDirect = true;
+    unsigned long long base;   // first slot of the current chunk
+    uint32_t fill;             // slots used in it (WRITER_CHUNK = none open)
+    unsigned long long total;  // pairs found by this warp
+    uint64_t policy;           // L2 evict_first for the record stream
+};
+
+__device__ __forceinline__ void writer_init(DirectWriter& w) {
+    w.base = 0;
+    w.fill = WRITER_CHUNK;
+    w.total = 0;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(w.policy));
+}
+
+__device__ __forceinline__ void st_global_v4_hint(uint4* p, uint4 v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;"
+                 ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w), "l"(pol)
+                 : "memory");
+}
+
+// Warp collective (same contract as the other writers).
+__device__ __forceinline__ void writer_append(DirectWriter& w, const JoinArgs& a, uint32_t ballot,
+                                              bool mine, uint32_t i1, uint32_t j1, float d2) {
+    const uint32_t n = __popc(ballot);
+    w.total += n;
+    if (a.count_only || n == 0) return;
+    const uint32_t room = WRITER_CHUNK - w.fill;
+    unsigned long long next = 0;
+    if (n > room) {
+        unsigned long long c = 0;
+        if (lane_id() == 0) c = atomicAdd(a.count + 1, 1ull);
+        next = __shfl_sync(0xffffffffu, c, 0) * WRITER_CHUNK;
+    }
+    if (mine) {
+        const uint32_t r = __popc(ballot & lanemask_lt());
+        const unsigned long long slot = r < room ? w.base + w.fill + r : next + (r - room);
+        if (slot < a.capacity)
+            st_global_v4_hint(a.out + slot, make_uint4(i1, j1, __float_as_uint(d2), 0u), w.policy);
+    }
+    if (n > room) {
+        w.base = next;
+        w.fill = n - room;
+    } else {
+        w.fill += n;
+    }
+}
+
+__device__ __forceinline__ void writer_finish(DirectWriter& w, const JoinArgs& a) {
+    if (!a.count_only) {
+        for (uint32_t s = w.fill + lane_id(); s < WRITER_CHUNK; s += 32)
+            if (w.base + s < a.capacity) a.out[w.base + s] = make_uint4(0u, 0u, 0u, 0u);
     }
     if (lane_id() == 0 && w.total) atomicAdd(a.count, w.total);
 }

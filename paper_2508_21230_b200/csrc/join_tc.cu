@@ -52,6 +52,8 @@
 #include <cudaTypedefs.h>
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "join_common.cuh"
 
@@ -576,7 +578,8 @@ template <typename W>
 __device__ __forceinline__ void epi_chunk_res(const JoinArgs& a, W& wr, const uint32_t (&r)[32],
                                               int64_t jb, int64_t i, int64_t iw, bool row_ok,
                                               unsigned long long* tr = nullptr) {
-    const uint32_t stash = wr.sbuf + 2u * W::kStage * 16u;
+    uint32_t stash = 0u;
+    if constexpr (!W::kDirect) stash = wr.sbuf + 2u * W::kStage * 16u;
     // common path: is any D >= 0 (sign bit clear)?  A balanced AND tree.
     const uint32_t acc = and_tree32(r);
     const bool diag = (jb < iw + 32) && (iw < jb + 32);   // warp-uniform
@@ -596,8 +599,8 @@ __device__ __forceinline__ void epi_chunk_res(const JoinArgs& a, W& wr, const ui
     // masks, all rows at once (serialising rows measured 20% slower at
     // 60K x 512, where a 32 x 32 chunk holds ~1 pair; A/B flags force either).
     const bool multi = (rows & (rows - 1u)) != 0u;
-    if (((FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_RARE_LM) || multi) &&
-        !(FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_RARE_ROWS)) {
+    if (W::kDirect || (((FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_RARE_LM) || multi) &&
+                       !(FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_RARE_ROWS))) {
         // per-lane hit masks: all candidate rows at once
         uint32_t lm = hit_mask32(r);
         const int64_t valid = a.n_logical - jb;
@@ -1774,8 +1777,11 @@ __device__ __forceinline__ void res_unit_sym(const ResSched& s, const JoinArgs& 
     }
 }
 
+// NHIT > 0: hit warps own the rare path; NHIT == 0: staged writers in the
+// epilogue warps; NHIT == -1: DirectWriter (registers -> global) in the
+// epilogue warps, the per-lane hit-mask search, no shared memory on the hit path.
 template <int CG, int TBN, int NEPI, bool TRACE = false, int NHIT = 0>
-__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI + NHIT) * 32, 1)
+__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI + (NHIT > 0 ? NHIT : 0)) * 32, 1)
 join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                    const __grid_constant__ CUtensorMap tmap_xb,
                    const __grid_constant__ CUtensorMap tmap_aug_a,
@@ -1993,8 +1999,10 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         __syncwarp();
     } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
         // ---------------- hit warp
-        hit_warp_loop<NHIT, TRACE>(a, bars + C::BAR_REGION, warp - FIRST_EPI_WARP - NEPI,
-                                   NEPI / NHIT, lane, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
+        if constexpr (NHIT > 0)
+            hit_warp_loop<NHIT, TRACE>(a, bars + C::BAR_REGION, warp - FIRST_EPI_WARP - NEPI,
+                                       NEPI / NHIT, lane,
+                                       (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
     } else {
         // ---------------- epilogue
         constexpr int NSPLIT = NEPI / 4;
@@ -2003,12 +2011,15 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         const int q = warp & 3;                       // TMEM lane quarter
         const int h = (warp - FIRST_EPI_WARP) >> 2;   // column group (NEPI / 4 of them)
         constexpr int RWS = RES_WSTAGE_TOTAL / (2 * NEPI) * 2;   // 16 (NEPI 16) / 32 (NEPI 8)
-        StagedWriter<RWS> wr;
+        using EpiWriter = std::conditional_t<(NHIT < 0), DirectWriter, StagedWriter<RWS>>;
+        EpiWriter wr;
         // per warp: two staging buffers, then the 128-byte row stash (no
         // writers here when hit warps write the records)
         if constexpr (NHIT == 0)
             writer_init(wr, bars + C::BAR_REGION +
                                 (uint32_t)(warp - FIRST_EPI_WARP) * (2 * RWS * 16 + EPI_STASH_BYTES));
+        else if constexpr (NHIT < 0)
+            writer_init(wr);
         static_assert(NACC == 2, "lean epilogue assumes two accumulators");
         const uint32_t tcol0 = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * HALF);
         const bool local_release = CG == 1 || leader;
@@ -2535,9 +2546,10 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     ResSched sch;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.a_buf_bytes = (uint32_t)((sch.nkb * A_BYTES + BM * AUG_ROW_BYTES + 1023) & ~1023);
-    const int wstage = NHIT > 0 ? HitQ<NHIT>::BYTES
-                                : NEPI * (2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16 +
-                                          EPI_STASH_BYTES);
+    const int wstage = NHIT > 0    ? HitQ<(NHIT > 0 ? NHIT : 1)>::BYTES
+                       : NHIT == 0 ? NEPI * (2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16 +
+                                             EPI_STASH_BYTES)
+                                   : 0;
     const int budget = SMEM_MAX - 1024 - C::BAR_REGION - wstage;
     sch.na = 2 * (int)sch.a_buf_bytes <= 80 * 1024 ? 2 : 1;
     sch.stages = (budget - sch.na * (int)sch.a_buf_bytes) / C::STAGE_BYTES;
@@ -2560,7 +2572,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     sch.lanes = (int)work;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * CG));
-    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI + NHIT) * 32);
+    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI + (NHIT > 0 ? NHIT : 0)) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -2814,6 +2826,8 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
             e = launch_res<1, 256, 8>(mx, mxb, ma, mbb, a, s);
         else if (FASTED_KNOB("FASTED_RES_EPI", 16) != 16)
             e = launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
+        else if (FASTED_KNOB("FASTED_RES_DIRECT", 0) != 0)
+            e = launch_res<2, 256, 16, -1>(mx, mxb, ma, mbb, a, s);
         else
 #endif
             e = res_hit(a.sparse != 0) ? launch_res<2, 256, 16, 2>(mx, mxb, ma, mbb, a, s)

@@ -124,13 +124,38 @@ __device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p, uint64_t po
     return v;
 }
 
-__global__ void hist_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
-                            uint32_t* __restrict__ counts) {
+// Records per thread in flight (hist / scatter): SORT_ILP independent
+// coalesced loads (and cursor atomics) before any result is used.
+constexpr int SORT_ILP = 4;
+
+__device__ __forceinline__ uint32_t sort_lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__global__ void __launch_bounds__(256)
+hist_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
+            uint32_t* __restrict__ counts) {
     const uint64_t pol = stream_policy();
-    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < count;
-         p += (uint64_t)gridDim.x * blockDim.x) {
-        const uint32_t i = ld_stream_u32(reinterpret_cast<const uint32_t*>(rec + p), pol);
-        if (i) atomicAdd(&counts[i - 1 - row_begin], 1u);   // i == 0: unused slot
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    // warp-uniform trip count (the match below needs the whole warp)
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+         p - (threadIdx.x & 31) < count; p += stride * SORT_ILP) {
+        uint32_t iv[SORT_ILP];
+#pragma unroll
+        for (int k = 0; k < SORT_ILP; k++) {
+            const uint64_t q = p + (uint64_t)k * stride;
+            iv[k] = q < count ? ld_stream_u32(reinterpret_cast<const uint32_t*>(rec + q), pol) : 0u;
+        }
+        // lanes holding the same row add once (a warp reads 32 consecutive
+        // records: one join warp's staging buffer, a few rows repeated)
+#pragma unroll
+        for (int k = 0; k < SORT_ILP; k++) {   // i == 0: unused slot
+            const uint32_t g = __match_any_sync(0xffffffffu, iv[k]);
+            if (iv[k] && (g & sort_lanemask_lt()) == 0u)
+                atomicAdd(&counts[iv[k] - 1 - row_begin], (uint32_t)__popc(g));
+        }
     }
 }
 
@@ -222,19 +247,42 @@ __global__ void scan_add_kernel(unsigned long long* __restrict__ offsets, int64_
     if (idx == 0) offsets[n] = bsum[(n + SCAN_TILE - 1) / SCAN_TILE];
 }
 
-__global__ void scatter_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
-                               const unsigned long long* __restrict__ offsets,
-                               uint32_t* __restrict__ cursor, uint32_t* __restrict__ tj,
-                               float* __restrict__ td) {
+__global__ void __launch_bounds__(256)
+scatter_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
+               const unsigned long long* __restrict__ offsets, uint32_t* __restrict__ cursor,
+               uint32_t* __restrict__ tj, float* __restrict__ td) {
     const uint64_t pol = stream_policy();
-    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < count;
-         p += (uint64_t)gridDim.x * blockDim.x) {
-        const uint4 v = ld_stream_u4(rec + p, pol);
-        if (v.x == 0) continue;
-        const int64_t r = (int64_t)v.x - 1 - row_begin;
-        const unsigned long long pos = offsets[r] + atomicAdd(&cursor[r], 1u);
-        tj[pos] = v.y;
-        td[pos] = __uint_as_float(v.z);
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+         p - (threadIdx.x & 31) < count; p += stride * SORT_ILP) {
+        uint4 v[SORT_ILP];
+#pragma unroll
+        for (int k = 0; k < SORT_ILP; k++) {
+            const uint64_t q = p + (uint64_t)k * stride;
+            v[k] = q < count ? ld_stream_u4(rec + q, pol) : make_uint4(0u, 0u, 0u, 0u);
+        }
+        // one cursor atomic per distinct row of the warp's 32 records; each
+        // lane takes the next slot after its lower lanes of the same row
+        uint32_t c[SORT_ILP], g[SORT_ILP];
+#pragma unroll
+        for (int k = 0; k < SORT_ILP; k++) {
+            g[k] = __match_any_sync(0xffffffffu, v[k].x);
+            const bool lead = v[k].x && (g[k] & sort_lanemask_lt()) == 0u;
+            c[k] = lead ? atomicAdd(&cursor[(int64_t)v[k].x - 1 - row_begin],
+                                    (uint32_t)__popc(g[k]))
+                        : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < SORT_ILP; k++)
+            c[k] = __shfl_sync(0xffffffffu, c[k], __ffs(g[k]) - 1) +
+                   (uint32_t)__popc(g[k] & sort_lanemask_lt());
+#pragma unroll
+        for (int k = 0; k < SORT_ILP; k++) {
+            if (v[k].x == 0) continue;
+            const unsigned long long pos = offsets[(int64_t)v[k].x - 1 - row_begin] + c[k];
+            tj[pos] = v[k].y;
+            td[pos] = __uint_as_float(v[k].z);
+        }
     }
 }
 
@@ -651,9 +699,10 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
     cudaMemsetAsync(ws.big_count, 0, 4, s);
     cudaMemsetAsync(ws.fb_count, 0, 4, s);
     const int sms = sm_count_current();
-    const unsigned rec_grid = (unsigned)((count + 255) / 256 < (uint64_t)sms * 16
-                                             ? (count + 255) / 256
-                                             : (uint64_t)sms * 16);
+    // one resident wave (8 x 256 threads per SM), SORT_ILP records per thread in flight
+    const uint64_t rec_blocks = (count + 256 * SORT_ILP - 1) / (256 * SORT_ILP);
+    const unsigned rec_grid =
+        (unsigned)(rec_blocks < (uint64_t)sms * 8 ? rec_blocks : (uint64_t)sms * 8);
     hist_kernel<<<rec_grid, 256, 0, s>>>(rec, count, row_begin, ws.counts);
     FASTED_CHECK_LAUNCH("hist_kernel");
     const int64_t nsb = (n_rows + SCAN_TILE - 1) / SCAN_TILE;
