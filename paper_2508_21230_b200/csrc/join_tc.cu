@@ -92,6 +92,15 @@ struct Cfg {
     static constexpr uint32_t IDESC_TF32 = IDESC_F16 | (2u << 7) | (2u << 10);
 };
 
+// Which pipeline warps wait for their mbarriers by a test_wait spin instead
+// of a try_wait suspend: 1 the MMA warp (accumulator release, operand
+// stages), 2 the TMA producer (stage release), 4 the hit warps.  A suspended
+// try_wait can resume well after the phase completes; alternating launches
+// (profiles/round2/mbarrier_spin_ab.txt): C4 1391 vs 1573 ms, C5 shard
+// S~256 1561 vs 2101 ms, S~16 1542 vs 1760 ms with 3; C3 and C2 unchanged;
+// the hit warps (4) do not gain.
+constexpr int MMA_SPIN_DEFAULT = 3;
+
 struct Sched {
     int row_tiles;
     int col_tiles;
@@ -99,6 +108,7 @@ struct Sched {
     int nkb;
     int64_t total;
     int diag;   // 1: Gram-diagonal pre-pass (tiles (r, r), no augment step)
+    int mma_spin = MMA_SPIN_DEFAULT;   // MMA_SPIN_DEFAULT bits (FASTED_MMA_SPIN in experiments)
 };
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -214,6 +224,21 @@ __device__ __forceinline__ void epi_wait(uint32_t bar, uint32_t parity, bool spi
     while (!mbar_test_only(bar, parity)) {
         __nanosleep(sleep_ns);
         if (++polls == 64u) {
+            polls = 0;
+            if (global_timer() - t0 > 20000000000ull) __trap();
+        }
+    }
+}
+
+// Pure spin on mbarrier.test_wait (never suspends): the MMA and TMA-producer
+// warps' waits (MMA_SPIN_DEFAULT) -- a suspended try_wait may resume well
+// after the phase completes.
+__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+    if (mbar_test_only(bar, parity)) return;
+    const uint64_t t0 = global_timer();
+    uint32_t polls = 0;
+    while (!mbar_test_only(bar, parity)) {
+        if (++polls == 1024u) {
             polls = 0;
             if (global_timer() - t0 > 20000000000ull) __trap();
         }
@@ -1094,7 +1119,7 @@ __device__ __forceinline__ void hit_warp_loop(const JoinArgs& a, uint32_t reg, i
         unsigned long long* te = (TRACE && trh && idx < (uint32_t)TRACE_HIT_ENTRIES)
                                      ? trh + 4u * idx : nullptr;
         if (TRACE && te && lane == 0) te[0] = clock64();
-        mbar_wait2(H::full(reg, hq, sl), (idx / H::Q) & 1u, spin);
+        if (spin) mbar_spin(H::full(reg, hq, sl), (idx / H::Q) & 1u); else mbar_wait(H::full(reg, hq, sl), (idx / H::Q) & 1u);
         if (TRACE && te && lane == 0) te[1] = clock64();
         const uint4 m = ld_shared_v4(H::meta(reg, hq, sl));
         if ((FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_HITSKIP) && m.x != HIT_END) {
@@ -1267,7 +1292,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 const int my_a = (int)(row0 + 128 * rank);
                 const bool a_mine = rank == 0 || a_hi;
                 for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
-                    mbar_wait(empty_bar(s), ph ^ 1u);
+                    if (sch.mma_spin & 2) mbar_spin(empty_bar(s), ph ^ 1u); else mbar_wait(empty_bar(s), ph ^ 1u);
                     const uint32_t fb = full_bar(s);
                     if (elect_one()) {
                     if (kb < sch.nkb) {
@@ -1345,11 +1370,13 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 }
                 const int buf = lt & 1;
                 const uint32_t aph = (uint32_t)(lt >> 1) & 1u;
-                mbar_wait(tempty_bar(buf), aph ^ 1u);
+                if (sch.mma_spin & 1) mbar_spin(tempty_bar(buf), aph ^ 1u);
+                else mbar_wait(tempty_bar(buf), aph ^ 1u);
                 tc_fence_after();
                 const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
                 for (int kb = 0; kb < sch.nkb + (DIAG ? 0 : 1); kb++) {
-                    mbar_wait(full_bar(s), ph);
+                    if (sch.mma_spin & 1) mbar_spin(full_bar(s), ph);
+                    else mbar_wait(full_bar(s), ph);
                     tc_fence_after();
                     if (elect_one()) {
                     if (!no_mma) {
@@ -1382,7 +1409,7 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
     } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
         // ---------------- hit warp
         hit_warp_loop<NHIT>(a, bars + BAR_BYTES, warp - FIRST_EPI_WARP - NEPI, NEPI / NHIT, lane,
-                            (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
+                            (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0 || (sch.mma_spin & 4));
     } else {
         // ---------------- epilogue
         const int q = warp & 3;          // TMEM lane quarter this warp may access
@@ -1562,7 +1589,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             const int row0 = (int)(a.row_begin + ((int64_t)rt * 2 + cr) * BM);
             const int colh = (int)(a.col_begin + (int64_t)ct * BN + 128 * cr);
             for (int kb = 0; kb < sch.nkb + 1; kb++) {
-                mbar_wait(empty_bar(s), ph ^ 1u);
+                if (sch.mma_spin & 2) mbar_spin(empty_bar(s), ph ^ 1u); else mbar_wait(empty_bar(s), ph ^ 1u);
                 const uint32_t fb = full_bar(s);
                 if (elect_one()) {
                     if (kb < sch.nkb) {
@@ -1602,12 +1629,15 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 }
             }
             const int buf = lt & 1;
-            mbar_wait2(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u,
-                       (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
+            if (sch.mma_spin & 1)
+                mbar_spin(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u);
+            else
+                mbar_wait2(tempty_bar(buf), ((uint32_t)(lt >> 1) & 1u) ^ 1u,
+                           (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
             tc_fence_after();
             const uint32_t dtm = tmem_base + (uint32_t)(buf * BN);
             for (int kb = 0; kb < sch.nkb + 1; kb++) {
-                mbar_wait(full_bar(s), ph);
+                if (sch.mma_spin & 1) mbar_spin(full_bar(s), ph); else mbar_wait(full_bar(s), ph);
                 tc_fence_after();
                 const uint64_t ad = sw128_desc(sA + s * A_BYTES);
                 const uint64_t bd = sw128_desc(sB + s * B_BYTES);
@@ -1637,7 +1667,7 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
     } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
         // ---------------- hit warp
         hit_warp_loop<NHIT>(a, bars + BAR_BYTES, warp - FIRST_EPI_WARP - NEPI, NEPI / NHIT, lane,
-                            (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
+                            (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0 || (sch.mma_spin & 4));
     } else {
         // ---------------- epilogue
         const int q = warp & 3;
@@ -1715,6 +1745,7 @@ struct ResSched {
     int64_t units;            // row_tiles * nsegs
     int lanes;                // units in flight: CTA pairs (CTAs) launched
     uint32_t epi_sleep_ns;    // epilogue accumulator wait backoff (0: suspend hint)
+    int mma_spin = MMA_SPIN_DEFAULT;   // MMA_SPIN_DEFAULT bits (FASTED_MMA_SPIN in experiments)
 };
 
 // Records per staging buffer in the resident kernel (tight shared memory):
@@ -1903,7 +1934,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                     }
                     for (int kb = 0; kb < sch.nkb; kb++) {
                         const bool last = kb == sch.nkb - 1;
-                        mbar_wait(empty_bar(s), ph ^ 1u);
+                        if (sch.mma_spin & 2) mbar_spin(empty_bar(s), ph ^ 1u); else mbar_wait(empty_bar(s), ph ^ 1u);
                         const uint32_t fb = full_bar(s);
                         const uint32_t st = sB + (uint32_t)s * C::STAGE_BYTES;
                         const uint32_t box_bytes =
@@ -1948,8 +1979,11 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                 const uint32_t abuf = sAb + (uint32_t)ab * sch.a_buf_bytes;
                 for (int ct = ct0; ct < ct1; ct++, ++lt) {
                     const int buf = lt % NACC;
-                    mbar_wait2(tempty_bar(buf), ((uint32_t)(lt / NACC) & 1u) ^ 1u,
-                               (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
+                    if (sch.mma_spin & 1)
+                        mbar_spin(tempty_bar(buf), ((uint32_t)(lt / NACC) & 1u) ^ 1u);
+                    else
+                        mbar_wait2(tempty_bar(buf), ((uint32_t)(lt / NACC) & 1u) ^ 1u,
+                                   (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
                     tc_fence_after();
                     unsigned long long* tr =
                         (TRACE && a.trace && blockIdx.x == 0 && lt < TRACE_TILES)
@@ -1958,7 +1992,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                     if (TRACE && tr && lane == 0) tr[0] = clock64();
                     const uint32_t dtm = tmem_base + (uint32_t)(buf * TBN);
                     for (int kb = 0; kb < sch.nkb; kb++) {
-                        mbar_wait(full_bar(s), ph);
+                        if (sch.mma_spin & 1) mbar_spin(full_bar(s), ph);
+                        else mbar_wait(full_bar(s), ph);
                         tc_fence_after();
                         const uint32_t st = sB + (uint32_t)s * C::STAGE_BYTES;
                         if (elect_one()) {
@@ -2002,7 +2037,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         if constexpr (NHIT > 0)
             hit_warp_loop<NHIT, TRACE>(a, bars + C::BAR_REGION, warp - FIRST_EPI_WARP - NEPI,
                                        NEPI / NHIT, lane,
-                                       (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
+                                       (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0 ||
+                                           (sch.mma_spin & 4));
     } else {
         // ---------------- epilogue
         constexpr int NSPLIT = NEPI / 4;
@@ -2487,6 +2523,7 @@ static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const
     }
     Sched sch;
     sch.diag = 0;
+    sch.mma_spin = FASTED_KNOB("FASTED_MMA_SPIN", MMA_SPIN_DEFAULT);
     sch.row_tiles = (int)((a.row_end - a.row_begin + 2 * BM - 1) / (2 * BM));   // super-rows
     sch.col_tiles = (int)((a.col_end - a.col_begin + BN - 1) / BN);
     // 8192-row groups (measured at 1M x 960: 1374 TFLOPS vs 1305 for 4096 and
@@ -2560,6 +2597,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     // a segment of ~16K columns per unit: the A panel load is amortised over
     // many tiles and the units stay small enough to balance
     sch.epi_sleep_ns = (uint32_t)FASTED_KNOB("FASTED_EPI_SLEEP_NS", 0);
+    sch.mma_spin = FASTED_KNOB("FASTED_MMA_SPIN", MMA_SPIN_DEFAULT);
     int seg = FASTED_KNOB("FASTED_SEG_TILES", 16384 / TBN);
     if (seg < 1) seg = 1;
     sch.nsegs = (sch.col_tiles + seg - 1) / seg;
@@ -2660,6 +2698,7 @@ static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUte
     }
     ResSched sch;
     sch.epi_sleep_ns = 0u;
+    sch.mma_spin = 0;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.na = 2;
     sch.a_buf_bytes = 0;
@@ -2778,6 +2817,7 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         sd.nkb = (int)((a.d_pad + BK - 1) / BK);
         sd.total = sd.row_tiles;
         sd.diag = 1;
+        sd.mma_spin = FASTED_KNOB("FASTED_MMA_SPIN", MMA_SPIN_DEFAULT);
         e = launch_variant<1, true>(mx, ma, mb, ad, sd, s);
         if (e == cudaSuccess) e = cudaGetLastError();
         if (e != cudaSuccess) {
@@ -2856,6 +2896,7 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     }
     Sched sch;
     sch.diag = 0;
+    sch.mma_spin = FASTED_KNOB("FASTED_MMA_SPIN", MMA_SPIN_DEFAULT);
     const int tile_m = BM * cg;
     sch.row_tiles = (int)((a.row_end - a.row_begin + tile_m - 1) / tile_m);
     sch.col_tiles = (int)((a.col_end - a.col_begin + BN - 1) / BN);
