@@ -54,7 +54,9 @@ enum {
     // hit warps: queue entries written with generic shared stores and a
     // release arrive on the slot's full barrier instead of st.async +
     // complete_tx (results stay valid; A/B of the hand-off)
-    FASTED_JOIN_DIAG_GENERICQ = 67108864
+    FASTED_JOIN_DIAG_GENERICQ = 67108864,
+    // epilogue warps wait for the accumulator by test_wait spin (results valid)
+    FASTED_JOIN_DIAG_EPISPIN = 134217728
 };
 constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA | FASTED_JOIN_DIAG_LOADONLY |
@@ -62,7 +64,8 @@ constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_AEVL | FASTED_JOIN_DIAG_TRACE | FASTED_JOIN_DIAG_RARE_LM |
     FASTED_JOIN_DIAG_RARE_ROWS | FASTED_JOIN_DIAG_NOAUG | FASTED_JOIN_DIAG_AUGF16 |
     FASTED_JOIN_DIAG_HITMETA | FASTED_JOIN_DIAG_HITSKIP | FASTED_JOIN_DIAG_NOTMA |
-    FASTED_JOIN_DIAG_NOREMOTE | FASTED_JOIN_DIAG_HITPACK | FASTED_JOIN_DIAG_GENERICQ;
+    FASTED_JOIN_DIAG_NOREMOTE | FASTED_JOIN_DIAG_HITPACK | FASTED_JOIN_DIAG_GENERICQ |
+    FASTED_JOIN_DIAG_EPISPIN;
 
 inline int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -98,7 +101,8 @@ enum {
     FASTED_JOIN_DIAG_NOTMA = 0,
     FASTED_JOIN_DIAG_NOREMOTE = 0,
     FASTED_JOIN_DIAG_HITPACK = 0,
-    FASTED_JOIN_DIAG_GENERICQ = 0
+    FASTED_JOIN_DIAG_GENERICQ = 0,
+    FASTED_JOIN_DIAG_EPISPIN = 0
 };
 
 #endif

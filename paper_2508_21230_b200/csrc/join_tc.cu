@@ -206,6 +206,21 @@ __device__ __forceinline__ bool mbar_test_only(uint32_t bar, uint32_t parity) {
     return ok != 0;
 }
 
+// Pure spin on mbarrier.test_wait (never suspends): the MMA and TMA-producer
+// warps' waits (MMA_SPIN_DEFAULT) -- a suspended try_wait may resume well
+// after the phase completes.
+__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+    if (mbar_test_only(bar, parity)) return;
+    const uint64_t t0 = global_timer();
+    uint32_t polls = 0;
+    while (!mbar_test_only(bar, parity)) {
+        if (++polls == 1024u) {
+            polls = 0;
+            if (global_timer() - t0 > 20000000000ull) __trap();
+        }
+    }
+}
+
 // The epilogue's accumulator wait.  sleep_ns == 0: mbar_wait2 (try_wait
 // with a suspend hint).  Otherwise a failed test sleeps sleep_ns in
 // __nanosleep: a try_wait-suspended warp is woken by other barrier traffic
@@ -218,27 +233,16 @@ __device__ __forceinline__ void epi_wait(uint32_t bar, uint32_t parity, bool spi
         mbar_wait2(bar, parity, spin);
         return;
     }
+    if (sleep_ns == 1u) {   // FASTED_EPI_SLEEP_NS=1: pure test_wait spin
+        mbar_spin(bar, parity);
+        return;
+    }
     if (mbar_test_only(bar, parity)) return;
     const uint64_t t0 = global_timer();
     uint32_t polls = 0;
     while (!mbar_test_only(bar, parity)) {
         __nanosleep(sleep_ns);
         if (++polls == 64u) {
-            polls = 0;
-            if (global_timer() - t0 > 20000000000ull) __trap();
-        }
-    }
-}
-
-// Pure spin on mbarrier.test_wait (never suspends): the MMA and TMA-producer
-// warps' waits (MMA_SPIN_DEFAULT) -- a suspended try_wait may resume well
-// after the phase completes.
-__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
-    if (mbar_test_only(bar, parity)) return;
-    const uint64_t t0 = global_timer();
-    uint32_t polls = 0;
-    while (!mbar_test_only(bar, parity)) {
-        if (++polls == 1024u) {
             polls = 0;
             if (global_timer() - t0 > 20000000000ull) __trap();
         }
@@ -705,7 +709,8 @@ __device__ __forceinline__ void epilogue_tile(const JoinArgs& a, W& wr,
     int nchunks = left <= 0 ? 0 : (left >= HALF ? NCH : (int)(left / 32));
     if (row0 >= a.row_end || (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
     const uint32_t tcol = tmem_base + lane_base + (uint32_t)(buf * TBN + h * HALF);
-    mbar_wait2(tfull, aph, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
+    if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_EPISPIN) mbar_spin(tfull, aph);
+    else mbar_wait2(tfull, aph, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
     tc_fence_after();
     uint32_t r0[32], r1[32], r2[32], r3[32];
     if (NCH > 1 && (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_LDX64) && nchunks == NCH) {
@@ -769,7 +774,8 @@ __device__ __forceinline__ void res_epi_tile(const JoinArgs& a, W& wr, uint32_t 
     constexpr int HALF = TBN / NSPLIT;
     constexpr int NCH = HALF / 32;
     static_assert(NCH == 1 || NCH == 2 || NCH == 4, "a warp covers 32, 64 or 128 columns");
-    epi_wait(tfull, aph, spin, sleep_ns);
+    if (dflags & FASTED_JOIN_DIAG_EPISPIN) mbar_spin(tfull, aph);
+    else epi_wait(tfull, aph, spin, sleep_ns);
     tc_fence_after();
     if (TRACE && tr && lane == 0) tr[0] = clock64();
     uint32_t r0[32], r1[32], r2[32], r3[32];
@@ -1034,7 +1040,8 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
     constexpr int HALF = TBN / NSPLIT;
     constexpr int NCH = HALF / 32;
     static_assert(NCH == 2, "hit-warp epilogue: 64 columns per warp");
-    epi_wait(tfull, aph, spin, sleep_ns);
+    if (dflags & FASTED_JOIN_DIAG_EPISPIN) mbar_spin(tfull, aph);
+    else epi_wait(tfull, aph, spin, sleep_ns);
     tc_fence_after();
     if (TRACE && tr && lane == 0) tr[0] = clock64();
     uint32_t r0[32], r1[32];
@@ -1170,7 +1177,8 @@ __device__ __forceinline__ void epilogue_tile_hit(const JoinArgs& a, uint32_t re
     int nchunks = left <= 0 ? 0 : (left >= HALF ? NCH : (int)(left / 32));
     if (row0 >= a.row_end || (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOEPI)) nchunks = 0;
     const uint32_t tcol = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * TBN + h * HALF);
-    mbar_wait2(tfull, aph, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
+    if (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_EPISPIN) mbar_spin(tfull, aph);
+    else mbar_wait2(tfull, aph, (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0);
     tc_fence_after();
     uint32_t r0[32], r1[32];
     if (nchunks > 0) tmem_ld32(tcol, r0);
