@@ -185,6 +185,7 @@ extern "C" int fasted_join(const uint16_t* values16, const float* norms, int64_t
     a.count = count;
     a.gram_diag = nullptr;
     a.trace = nullptr;
+    a.pace = nullptr;
 #ifdef FASTED_EXPERIMENTS
     if (flags & FASTED_JOIN_DIAG_TRACE) {
         const unsigned long long trace_recs = TRACE_WORDS / 2;

@@ -21,6 +21,7 @@ struct JoinArgs {
     unsigned long long* count;         // [0] exact pair total, [1] chunks taken
     float* gram_diag;                  // diagonal pre-pass output (tcgen05 kernel), else null
     unsigned long long* trace;         // FASTED_JOIN_DIAG_TRACE timeline (CTA 0), else null
+    unsigned long long* pace;          // resident kernel: units issued by all CTAs (zeroed per launch)
 };
 
 // FASTED_JOIN_DIAG_TRACE layout (resident kernel, CTA 0, first TRACE_TILES

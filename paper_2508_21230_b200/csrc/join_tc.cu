@@ -1026,11 +1026,198 @@ __device__ __forceinline__ void hit_push(uint32_t reg, uint32_t creg, uint8_t* s
     __syncwarp();
 }
 
+// ---------------------------------------------------------------------------
+// Ring hand-off (resident kernel, NHIT == RING_NHIT; experiment form).  The
+// shared-queue hand-off above costs an epilogue warp ~1400 cycles per
+// candidate slice at 1M x 128: a returned tail atomic, a returned head read
+// and the slot stores, each a shared-memory round trip behind the tensor
+// core's operand traffic.  Here every epilogue warp owns a private ring of
+// RING_R slots (no tail atomic), fills a slot with st.async + expect_tx on the
+// slot's own full mbarrier (nothing returns: fire and forget), and reads the
+// consumer's counter only when its cached copy says the ring is full.  The
+// hit warps poll their producers' next slots with mbarrier.test_wait, round
+// robin, and publish each producer's consumed count with a release atomic.
+// NHIT template value of the ring form: bit 4 set, the low bits count the
+// hit warps (2: three would cap the kernel at 80 registers).
+constexpr int RING_NHIT = 16 + 2;
+constexpr int RING_HW = RING_NHIT & 15;
+__host__ __device__ constexpr int hit_warps(int nhit) { return nhit > 0 ? (nhit & 15) : 0; }
+struct Ring {
+    static constexpr int R = 4;                       // slots per producer warp
+    static constexpr int NPROD = 16;                  // producers (the 16 epilogue warps)
+    static constexpr int SLOT = 144;                  // 128 B row + 16 B meta
+    static constexpr int HWS = 32;                    // records per staging buffer (hit warp)
+    static constexpr int WRITER_BYTES = RING_HW * 2 * HWS * 16;
+    static constexpr int SLOT_BYTES = NPROD * R * SLOT;
+    static constexpr int BAR_BYTES = NPROD * R * 8;
+    static constexpr int BYTES = WRITER_BYTES + SLOT_BYTES + BAR_BYTES + NPROD * 4 + 16;
+    static __device__ __forceinline__ uint32_t data(uint32_t r, int p, uint32_t s) {
+        return r + WRITER_BYTES + ((uint32_t)p * R + s) * SLOT;
+    }
+    static __device__ __forceinline__ uint32_t full(uint32_t r, int p, uint32_t s) {
+        return r + WRITER_BYTES + SLOT_BYTES + ((uint32_t)p * R + s) * 8u;
+    }
+    static __device__ __forceinline__ uint32_t cons(uint32_t r, int p) {
+        return r + WRITER_BYTES + SLOT_BYTES + BAR_BYTES + 4u * (uint32_t)p;
+    }
+};
+
+__device__ __forceinline__ void ring_init(uint32_t reg, uint8_t* smem_raw, uint32_t raw) {
+    for (int p = 0; p < Ring::NPROD; p++) {
+        for (uint32_t sl = 0; sl < (uint32_t)Ring::R; sl++) mbar_init(Ring::full(reg, p, sl), 1);
+        *reinterpret_cast<volatile uint32_t*>(smem_raw + (Ring::cons(reg, p) - raw)) = 0u;
+    }
+}
+
+// One entry (one thread): its slot's previous lap was consumed (checked by
+// the caller); the bytes travel with st.async and complete the slot's phase.
+__device__ __forceinline__ void ring_put(uint32_t reg, uint32_t creg, int p, uint32_t idx,
+                                         uint32_t kind, uint32_t i, uint32_t jb, uint32_t mask,
+                                         const uint32_t (&r)[32], bool with_data) {
+    const uint32_t sl = idx % Ring::R;
+    const uint32_t full = creg + (Ring::full(reg, p, sl) - reg);
+    mbar_arrive_expect_tx(Ring::full(reg, p, sl), with_data ? 144u : 16u);
+    const uint32_t d = creg + (Ring::data(reg, p, sl) - reg);
+    if (with_data) {
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+            st_async_v4(d + 16u * k, make_uint4(r[4 * k], r[4 * k + 1], r[4 * k + 2], r[4 * k + 3]),
+                        full);
+    }
+    st_async_v4(d + 128u, make_uint4(kind, i, jb, mask), full);
+}
+
+// Warp-uniform: make room for `need` more entries (pw pushed, cw cached).
+__device__ __forceinline__ void ring_room(uint32_t reg, int p, uint32_t pw, uint32_t& cw,
+                                          uint32_t need) {
+    if (pw + need - cw <= (uint32_t)Ring::R) return;
+    const uint64_t t0 = global_timer();
+    while (true) {
+        uint32_t c = 0;
+        if ((threadIdx.x & 31) == 0) c = ld_acquire_shared(Ring::cons(reg, p));
+        cw = __shfl_sync(0xffffffffu, c, 0);
+        if (pw + need - cw <= (uint32_t)Ring::R) return;
+        __nanosleep(64);
+        if (global_timer() - t0 > 20000000000ull) __trap();
+    }
+}
+
+// Hand one 32-column chunk's candidate rows (and the diagonal's self pairs)
+// to this warp's ring.  Warp-collective.
+__device__ __forceinline__ void ring_push(uint32_t reg, uint32_t creg, int p, const uint32_t (&r)[32],
+                                          uint32_t and_r, int jb, int i, int iw, bool row_ok,
+                                          uint32_t lane, uint32_t& pw, uint32_t& cw) {
+    const bool diag = (jb < iw + 32) && (iw < jb + 32);
+    uint32_t rows, selfmask = 0u;
+    if (!diag) {
+        rows = __ballot_sync(0xffffffffu, (int)and_r >= 0 && row_ok);
+    } else {
+        uint32_t lm = hit_mask32(r);
+        const bool self = i >= jb && i < jb + 32 && row_ok;
+        if (self) lm &= ~(1u << (uint32_t)(i - jb));
+        rows = __ballot_sync(0xffffffffu, lm != 0u && row_ok);
+        selfmask = __ballot_sync(0xffffffffu, self);
+    }
+    const uint32_t nrows = (uint32_t)__popc(rows);
+    const uint32_t k = nrows + (selfmask ? 1u : 0u);
+    if (k == 0u) return;
+    const uint32_t rank = (uint32_t)__popc(rows & lanemask_lt());
+    uint32_t done = 0;
+    while (done < k) {   // warp-uniform; one pass unless the ring is short of room
+        ring_room(reg, p, pw, cw, 1u);
+        uint32_t n = (uint32_t)Ring::R - (pw - cw);
+        if (n > k - done) n = k - done;
+        if (((rows >> lane) & 1u) && rank >= done && rank < done + n)
+            ring_put(reg, creg, p, pw + (rank - done), HIT_ROW, (uint32_t)i, (uint32_t)jb, 0u, r,
+                     true);
+        if (selfmask && lane == 0 && nrows >= done && nrows < done + n)
+            ring_put(reg, creg, p, pw + (nrows - done), HIT_SELF, (uint32_t)iw, (uint32_t)jb,
+                     selfmask, r, false);
+        pw += n;
+        done += n;
+    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void ring_end(uint32_t reg, int p, uint32_t lane, uint32_t& pw,
+                                         uint32_t& cw) {
+    ring_room(reg, p, pw, cw, 1u);
+    if (lane == 0) {
+        uint32_t none[32];
+        ring_put(reg, cluster_addr(reg), p, pw, HIT_END, 0u, 0u, 0u, none, false);
+    }
+    pw++;
+    __syncwarp();
+}
+
+// A ring hit warp: poll producers hq, hq + RING_NHIT, ... in turn; each
+// ready entry is tested transposed (lane e = column e) and its records written.
+__device__ __forceinline__ void ring_warp_loop(const JoinArgs& a, uint32_t reg, int hq, int lane) {
+    constexpr int NPQ = (Ring::NPROD + RING_HW - 1) / RING_HW;
+    StagedWriter<Ring::HWS> wr;
+    writer_init(wr, reg + (uint32_t)hq * 2u * Ring::HWS * 16u);
+    uint32_t c[NPQ];
+    int nprod = 0;
+#pragma unroll
+    for (int q = 0; q < NPQ; q++) {
+        c[q] = 0u;
+        if (hq + q * RING_HW < Ring::NPROD) nprod++;
+    }
+    uint32_t ended = 0u;   // bit q: producer q sent END
+    const uint32_t all = (1u << nprod) - 1u;
+    const uint64_t t0 = global_timer();
+    uint32_t idle = 0;
+    while (ended != all) {
+        bool any = false;
+#pragma unroll
+        for (int q = 0; q < NPQ; q++) {
+            const int p = hq + q * RING_HW;
+            if (p >= Ring::NPROD || ((ended >> q) & 1u)) continue;
+            const uint32_t sl = c[q] % Ring::R;
+            if (!mbar_test_only(Ring::full(reg, p, sl), (c[q] / Ring::R) & 1u)) continue;
+            any = true;
+            const uint32_t d = Ring::data(reg, p, sl);
+            const uint4 m = ld_shared_v4(d + 128u);
+            if (m.x == HIT_ROW) {
+                const uint32_t v = ld_shared_u32(d + 4u * (uint32_t)lane);
+                const int64_t is = (int64_t)m.y, j = (int64_t)m.z + lane;
+                const bool hit =
+                    (int)v >= 0 && j < a.n_logical && j != is && (!a.symmetric || j > is);
+                const uint32_t b = __ballot_sync(0xffffffffu, hit);
+                if (b) {
+                    const float d2 = fmaxf(__fmaf_rn(-2.0f, __uint_as_float(v), a.eps_sq), 0.0f);
+                    writer_append(wr, a, b, hit, (uint32_t)(is + 1), (uint32_t)(j + 1), d2);
+                    if (a.symmetric)
+                        writer_append(wr, a, b, hit, (uint32_t)(j + 1), (uint32_t)(is + 1), d2);
+                }
+            } else if (m.x == HIT_SELF) {
+                const bool mine = (m.w >> lane) & 1u;
+                writer_append(wr, a, m.w, mine, m.y + (uint32_t)lane + 1u,
+                              m.y + (uint32_t)lane + 1u, 0.0f);
+            } else {
+                ended |= 1u << q;
+            }
+            c[q]++;
+            __syncwarp();   // every lane's reads of the slot are done
+            if (lane == 0) st_release_shared(Ring::cons(reg, p), c[q]);
+        }
+        if (!any) {
+            if (++idle == 4096u) {
+                idle = 0;
+                if (global_timer() - t0 > 20000000000ull) __trap();
+            }
+            __nanosleep(32);
+        }
+    }
+    writer_finish(wr, a);
+}
+
 // The resident epilogue tile with hit warps: drain, release, slice test, and
 // on a candidate only the hand-off.
 template <int CG, int TBN, int NSPLIT, int NHIT, bool TRACE = false>
 __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg, uint32_t creg,
-                                                 uint32_t& head_seen, uint8_t* smem_raw,
+                                                 uint32_t& head_seen, uint32_t& ring_pw,
+                                                 uint8_t* smem_raw,
                                                  uint32_t raw, int hq, uint32_t tcol,
                                                  uint32_t tfull, uint32_t aph, uint32_t tempty,
                                                  bool local_release, bool spin,
@@ -1071,12 +1258,18 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
     }
     if (dflags & FASTED_JOIN_DIAG_NOSLOW) return;
     if (TRACE && tr && lane == 0) tr[5] = clock64();
+    if constexpr (NHIT == RING_NHIT) {   // hq: this warp's ring; head_seen: its cached consumed count
+        if (nchunks > 0) ring_push(reg, creg, hq, r0, and0, jb, i, iw, row_ok, lane, ring_pw, head_seen);
+        if (nchunks > 1)
+            ring_push(reg, creg, hq, r1, and1, jb + 32, i, iw, row_ok, lane, ring_pw, head_seen);
+    } else {
     if (nchunks > 0)
         hit_push<NHIT>(reg, creg, smem_raw, raw, hq, r0, and0, jb, i, iw, row_ok, lane, head_seen,
                        dflags, (TRACE && tr) ? tr + 4 : nullptr);
     if (nchunks > 1)
         hit_push<NHIT>(reg, creg, smem_raw, raw, hq, r1, and1, jb + 32, i, iw, row_ok, lane,
                        head_seen, dflags);
+    }
 #ifndef FASTED_TRACE_SLOT
     if (TRACE && tr && lane == 0) tr[6] = clock64();
 #endif
@@ -1754,6 +1947,7 @@ struct ResSched {
     int lanes;                // units in flight: CTA pairs (CTAs) launched
     uint32_t epi_sleep_ns;    // epilogue accumulator wait backoff (0: suspend hint)
     int mma_spin = MMA_SPIN_DEFAULT;   // MMA_SPIN_DEFAULT bits (FASTED_MMA_SPIN in experiments)
+    int pace_w = 0;           // unit layers a CTA may run ahead of the slowest (0: unpaced)
 };
 
 // Records per staging buffer in the resident kernel (tight shared memory):
@@ -1778,6 +1972,26 @@ struct ResCfg {
     static constexpr uint32_t IDESC_TF32 = IDESC_F16 | (2u << 7) | (2u << 10);
     static_assert(STAGE_BYTES % 1024 == 0, "stages must stay 1024-aligned");
 };
+
+// Pacing (bounded drift).  Every lane walks the same sequence of unit layers
+// (its ua-th unit is in layer ua), so co-running pairs share each B segment
+// in L2 only while they stay within a few layers of each other.  Uneven
+// epilogue work lets them drift apart (C3: 671 GB of HBM reads per launch,
+// L2 hit rate 45%, against 188 GB with no epilogue).  With pace_w > 0 a
+// producer starts layer ua only after all CTAs issued layer ua - pace_w: a
+// global count of issued units (one relaxed-release add per unit per CTA).
+// Total CTA-units in layers 0..j:
+__device__ __forceinline__ unsigned long long pace_need(const ResSched& s, int64_t j, int cg) {
+    const int64_t full = s.units / s.lanes, rem = s.units % s.lanes;
+    const int64_t t = j + 1 < full ? j + 1 : full;
+    return (unsigned long long)cg * (unsigned long long)(t * s.lanes + (j >= full ? rem : 0));
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
 
 // Unit order: rounds of `lanes` row tiles.  Inside a round, lane (pair) p
 // keeps row tile round * lanes + p and sweeps the column segments in order,
@@ -1820,7 +2034,7 @@ __device__ __forceinline__ void res_unit_sym(const ResSched& s, const JoinArgs& 
 // epilogue warps; NHIT == -1: DirectWriter (registers -> global) in the
 // epilogue warps, the per-lane hit-mask search, no shared memory on the hit path.
 template <int CG, int TBN, int NEPI, bool TRACE = false, int NHIT = 0>
-__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI + (NHIT > 0 ? NHIT : 0)) * 32, 1)
+__global__ void __launch_bounds__((FIRST_EPI_WARP + NEPI + hit_warps(NHIT)) * 32, 1)
 join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                    const __grid_constant__ CUtensorMap tmap_xb,
                    const __grid_constant__ CUtensorMap tmap_aug_a,
@@ -1866,7 +2080,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
             mbar_init(afull_bar(b), 1);
             mbar_init(aempty_bar(b), 1);
         }
-        if constexpr (NHIT > 0) hit_init<NHIT>(bars + C::BAR_REGION, smem_raw, raw);
+        if constexpr (NHIT == RING_NHIT) ring_init(bars + C::BAR_REGION, smem_raw, raw);
+        else if constexpr (NHIT > 0) hit_init<NHIT>(bars + C::BAR_REGION, smem_raw, raw);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmap_xa))
                      : "memory");
@@ -1905,6 +2120,17 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
             uint32_t ph = 0;
             int ua = 0;
             for (int64_t u = unit0; u < sch.units; u += ustep, ++ua) {
+                if (sch.pace_w > 0 && ua >= sch.pace_w) {
+                    if (lane == 0) {
+                        const unsigned long long need = pace_need(sch, ua - sch.pace_w, CG);
+                        const uint64_t t0 = global_timer();
+                        while (ld_acquire_gpu_u64(a.pace) < need) {
+                            __nanosleep(64);
+                            if (global_timer() - t0 > 20000000000ull) __trap();
+                        }
+                    }
+                    __syncwarp();
+                }
                 int rt, ct0, ct1;
                 res_unit_sym<C::TILE_M, TBN>(sch, a, u, rt, ct0, ct1);
                 const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M;
@@ -1968,6 +2194,9 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                         }
                     }
                 }
+                if (sch.pace_w > 0 && lane == 0)   // this unit issued
+                    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.pace)
+                                 : "memory");
             }
         }
         __syncwarp();
@@ -2042,7 +2271,9 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         __syncwarp();
     } else if (NHIT > 0 && warp >= FIRST_EPI_WARP + NEPI) {
         // ---------------- hit warp
-        if constexpr (NHIT > 0)
+        if constexpr (NHIT == RING_NHIT)
+            ring_warp_loop(a, bars + C::BAR_REGION, warp - FIRST_EPI_WARP - NEPI, lane);
+        else if constexpr (NHIT > 0)
             hit_warp_loop<NHIT, TRACE>(a, bars + C::BAR_REGION, warp - FIRST_EPI_WARP - NEPI,
                                        NEPI / NHIT, lane,
                                        (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_SPIN) != 0 ||
@@ -2079,7 +2310,8 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
         const int jbase = (int)a.col_begin + h * HALF;
         const int col_end = (int)a.col_end;
         const uint32_t hit_creg = NHIT > 0 ? cluster_addr(bars + C::BAR_REGION) : 0u;
-        uint32_t head_seen = 0u;
+        uint32_t head_seen = 0u;   // queue: last head read; ring: cached consumed count
+        uint32_t ring_pw = 0u;     // ring: entries pushed
         int lt = 0;
         uint32_t buf = 0, aph = 0;
         for (int u = (int)unit0; u < (int)sch.units; u += (int)ustep) {
@@ -2112,7 +2344,9 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                          8 * (lt * TRACE_EPI_WARPS + (warp - FIRST_EPI_WARP));
                 if constexpr (NHIT > 0)
                     res_epi_tile_hit<CG, TBN, NSPLIT, NHIT, TRACE>(
-                        a, bars + C::BAR_REGION, hit_creg, head_seen, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT,
+                        a, bars + C::BAR_REGION, hit_creg, head_seen, ring_pw, smem_raw, raw,
+                        NHIT == RING_NHIT ? warp - FIRST_EPI_WARP
+                                          : (warp - FIRST_EPI_WARP) % hit_warps(NHIT),
                         tcol0 + buf * TBN, tfull0 + 8u * buf, aph, release0 + 8u * buf,
                         local_release, spin, sch.epi_sleep_ns, dflags, nchunks, fast, jb, i, iw,
                         row_ok, (uint32_t)lane, tr);
@@ -2126,7 +2360,9 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                 aph ^= buf ^ 1u;   // phase flips after buffer 1
             }
         }
-        if constexpr (NHIT > 0)   // end of this warp's stream in its hit warp's queue
+        if constexpr (NHIT == RING_NHIT)   // end of this warp's stream in its ring
+            ring_end(bars + C::BAR_REGION, warp - FIRST_EPI_WARP, (uint32_t)lane, ring_pw, head_seen);
+        else if constexpr (NHIT > 0)   // end of this warp's stream in its hit warp's queue
             hit_end<NHIT>(bars + C::BAR_REGION, smem_raw, raw, (warp - FIRST_EPI_WARP) % NHIT, lane);
         else
             writer_finish(wr, a);
@@ -2591,7 +2827,8 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     ResSched sch;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.a_buf_bytes = (uint32_t)((sch.nkb * A_BYTES + BM * AUG_ROW_BYTES + 1023) & ~1023);
-    const int wstage = NHIT > 0    ? HitQ<(NHIT > 0 ? NHIT : 1)>::BYTES
+    const int wstage = NHIT == RING_NHIT ? Ring::BYTES
+                       : NHIT > 0    ? HitQ<(NHIT > 0 ? NHIT : 1)>::BYTES
                        : NHIT == 0 ? NEPI * (2 * (RES_WSTAGE_TOTAL / (2 * NEPI) * 2) * 16 +
                                              EPI_STASH_BYTES)
                                    : 0;
@@ -2605,6 +2842,9 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     // a segment of ~16K columns per unit: the A panel load is amortised over
     // many tiles and the units stay small enough to balance
     sch.epi_sleep_ns = (uint32_t)FASTED_KNOB("FASTED_EPI_SLEEP_NS", 0);
+    // bounded drift of 2 unit layers (C3 243-247 vs 291 ms, HBM reads 47 vs 712 GB per
+    // launch; C5 shard S~4096 1998 vs 2621 ms; S~256 unchanged -- pace_ab.txt)
+    sch.pace_w = a.pace ? FASTED_KNOB("FASTED_PACE_W", 2) : 0;
     sch.mma_spin = FASTED_KNOB("FASTED_MMA_SPIN", MMA_SPIN_DEFAULT);
     int seg = FASTED_KNOB("FASTED_SEG_TILES", 16384 / TBN);
     if (seg < 1) seg = 1;
@@ -2618,7 +2858,7 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     sch.lanes = (int)work;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(work * CG));
-    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI + (NHIT > 0 ? NHIT : 0)) * 32);
+    cfg.blockDim = dim3((FIRST_EPI_WARP + NEPI + hit_warps(NHIT)) * 32);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -2767,7 +3007,8 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     // per-call scratch (stream ordered): augment rows (two [n_pad][8] FP32,
     // eps-dependent) and the tensor-core Gram diagonal
     float4* aug = nullptr;
-    const size_t aug_bytes = (size_t)a.n_pad * 64 + (size_t)a.n_pad * 4;
+    // (+ 256 bytes: the resident kernel's pacing counter)
+    const size_t aug_bytes = (size_t)a.n_pad * 64 + (size_t)a.n_pad * 4 + 256;
     cudaError_t e = cudaMallocAsync(&aug, aug_bytes, s);
     if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(augment rows)");
     float4* aug_a = aug;
@@ -2850,6 +3091,11 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     // (372 vs 283 ms: the N=128 MMAs re-read A every 64 cycles); A in TMEM
     // (286-296 vs 256 ms).
     if (variant == TC_RESIDENT) {
+        unsigned long long* pace = reinterpret_cast<unsigned long long*>(
+            reinterpret_cast<char*>(aug) + aug_bytes - 256);
+        cudaMemsetAsync(pace, 0, 8, s);
+        JoinArgs ar = a;
+        ar.pace = pace;
 #ifdef FASTED_EXPERIMENTS
         const bool ts = cg == 2 && a.d_pad <= 128 && FASTED_KNOB("FASTED_TS", 0) != 0;
 #else
@@ -2875,11 +3121,13 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         else if (FASTED_KNOB("FASTED_RES_EPI", 16) != 16)
             e = launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
         else if (FASTED_KNOB("FASTED_RES_DIRECT", 0) != 0)
-            e = launch_res<2, 256, 16, -1>(mx, mxb, ma, mbb, a, s);
+            e = launch_res<2, 256, 16, -1>(mx, mxb, ma, mbb, ar, s);
+        else if (FASTED_KNOB("FASTED_RES_HIT", 0) == RING_NHIT)
+            e = launch_res<2, 256, 16, RING_NHIT>(mx, mxb, ma, mbb, ar, s);
         else
 #endif
-            e = res_hit(a.sparse != 0) ? launch_res<2, 256, 16, 2>(mx, mxb, ma, mbb, a, s)
-                                       : launch_res<2, 256, 16>(mx, mxb, ma, mbb, a, s);
+            e = res_hit(a.sparse != 0) ? launch_res<2, 256, 16, 2>(mx, mxb, ma, mbb, ar, s)
+                                       : launch_res<2, 256, 16>(mx, mxb, ma, mbb, ar, s);
         if (e == cudaSuccess) e = cudaGetLastError();
         cudaFreeAsync(aug, s);
         if (e != cudaSuccess) return cuda_status(e, "join_tc_res_kernel");

@@ -12,7 +12,10 @@ import torch  # noqa: E402
 
 import paper_2508_21230_b200 as F  # noqa: E402
 from bench import SEED, WORKLOADS  # noqa: E402
-from paper_2508_21230_b200 import engine  # noqa: E402
+from paper_2508_21230_b200 import _lib, engine  # noqa: E402
+
+if os.environ.get("FASTED_LIB"):   # e.g. the experiment build (env knobs, diagnostic flags)
+    _lib.LIB_PATH = os.path.abspath(os.environ["FASTED_LIB"])
 
 wl = sys.argv[1]
 rows = int(sys.argv[2]) if len(sys.argv) > 2 else 148 * 256 * 2
