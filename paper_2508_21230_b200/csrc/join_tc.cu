@@ -109,7 +109,20 @@ struct Sched {
     int64_t total;
     int diag;   // 1: Gram-diagonal pre-pass (tiles (r, r), no augment step)
     int mma_spin = MMA_SPIN_DEFAULT;   // MMA_SPIN_DEFAULT bits (FASTED_MMA_SPIN in experiments)
+    int pace_w = 0;     // streaming pacing: blocks of PACE_TILES layers a CTA may run ahead
 };
+
+// Streaming-kernel pacing (the resident kernel's, per block of PACE_TILES tile
+// layers: layer k = every pair's k-th tile, a contiguous run of the raster).
+constexpr int PACE_TILES = 64;
+__device__ __forceinline__ unsigned long long pace_need_stream(int64_t total, int64_t step,
+                                                               int64_t b, int cg) {
+    const int64_t L = total / step, rem = total % step;   // pairs p < rem have L + 1 tiles
+    const int64_t jfull = L / PACE_TILES;
+    const int64_t full = b + 1 < jfull ? b + 1 : jfull;
+    const bool last = b >= jfull && (jfull + 1) * PACE_TILES == L + 1;
+    return (unsigned long long)cg * (unsigned long long)(full * step + (last ? rem : 0));
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -148,6 +161,12 @@ __device__ __forceinline__ uint64_t global_timer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
+}
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
 }
 
 // Spin on an mbarrier phase; traps after 20 s so a protocol bug aborts the
@@ -1480,7 +1499,25 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_evl));
             int s = 0;
             uint32_t ph = 0;
-            for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
+            int64_t k = 0;   // this CTA's tile layer
+            for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++k) {
+                if (sch.pace_w > 0 && k % PACE_TILES == 0 && k > 0) {
+                    const int64_t b = k / PACE_TILES;   // block b - 1 issued; gate block b
+                    if (lane == 0) {
+                        asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.pace)
+                                     : "memory");
+                        if (b >= sch.pace_w) {
+                            const unsigned long long need =
+                                pace_need_stream(sch.total, tile_step, b - sch.pace_w, CG);
+                            const uint64_t t0 = global_timer();
+                            while (ld_acquire_gpu_u64(a.pace) < need) {
+                                __nanosleep(64);
+                                if (global_timer() - t0 > 20000000000ull) __trap();
+                            }
+                        }
+                    }
+                    __syncwarp();
+                }
                 int rt, ct;
                 tile_coords(sch, t, rt, ct);
                 const int64_t row0 = a.row_begin + (int64_t)rt * C::TILE_M;
@@ -1985,12 +2022,6 @@ __device__ __forceinline__ unsigned long long pace_need(const ResSched& s, int64
     const int64_t full = s.units / s.lanes, rem = s.units % s.lanes;
     const int64_t t = j + 1 < full ? j + 1 : full;
     return (unsigned long long)cg * (unsigned long long)(t * s.lanes + (j >= full ? rem : 0));
-}
-
-__device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
 }
 
 // Unit order: rounds of `lanes` row tiles.  Inside a round, lane (pair) p
@@ -3090,12 +3121,13 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     // tune_c3_epi_ab_session2.txt); 128-column tiles with four accumulators
     // (372 vs 283 ms: the N=128 MMAs re-read A every 64 cycles); A in TMEM
     // (286-296 vs 256 ms).
+    // the pacing counter (resident kernel; streaming kernel on FASTED_STREAM_PACE_W)
+    unsigned long long* pace = reinterpret_cast<unsigned long long*>(
+        reinterpret_cast<char*>(aug) + aug_bytes - 256);
+    cudaMemsetAsync(pace, 0, 8, s);
+    JoinArgs ar = a;
+    ar.pace = pace;
     if (variant == TC_RESIDENT) {
-        unsigned long long* pace = reinterpret_cast<unsigned long long*>(
-            reinterpret_cast<char*>(aug) + aug_bytes - 256);
-        cudaMemsetAsync(pace, 0, 8, s);
-        JoinArgs ar = a;
-        ar.pace = pace;
 #ifdef FASTED_EXPERIMENTS
         const bool ts = cg == 2 && a.d_pad <= 128 && FASTED_KNOB("FASTED_TS", 0) != 0;
 #else
@@ -3164,6 +3196,10 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     if (sch.group < 1) sch.group = 1;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.total = (int64_t)sch.row_tiles * sch.col_tiles;
+    // pacing, one block of 64 tile layers (C4 on a box whose pairs drifted: HBM reads
+    // 5.45 TB -> 121 GB per launch, L2 hit 59 -> 98%, 1738 -> 1327 ms; profiles/round2/
+    // stream_pacing_ab.txt)
+    sch.pace_w = cg == 2 ? FASTED_KNOB("FASTED_STREAM_PACE_W", 1) : 0;
     // CTA pair: 16 epilogue warps of 64 columns (8 of 128: 1M x 960
     // 1466-1472 vs 1450-1491 TFLOPS, even; 5M x 384 shard at S <= 64:
     // 1917-1946 vs 2060-2253 ms, profiles/round1/tune_sepi_session2.txt)
@@ -3174,8 +3210,8 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         e = launch_variant<2>(mx, ma, mb, a, sch, s);
     else
 #endif
-        e = stream_hit(a.sparse != 0) ? launch_variant<2, false, 16, 2>(mx, ma, mb, a, sch, s)
-                                      : launch_variant<2, false, 16>(mx, ma, mb, a, sch, s);
+        e = stream_hit(a.sparse != 0) ? launch_variant<2, false, 16, 2>(mx, ma, mb, ar, sch, s)
+                                      : launch_variant<2, false, 16>(mx, ma, mb, ar, sch, s);
     if (e == cudaSuccess) e = cudaGetLastError();
     cudaFreeAsync(aug, s);
     if (e != cudaSuccess) return cuda_status(e, "join_tc_kernel");
