@@ -1587,6 +1587,10 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                     }
                 }
             }
+            // a final block of exactly PACE_TILES layers is counted here (the
+            // loop above counts a block when the next one starts)
+            if (sch.pace_w > 0 && k > 0 && k % PACE_TILES == 0 && lane == 0)
+                asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.pace) : "memory");
         }
         __syncwarp();
     } else if (warp == 1) {

@@ -788,6 +788,29 @@ def test_cta_pair_low_output_form_matches_single_cta():
             assert np.array_equal(x.view(np.uint32), y.view(np.uint32)), (sepi, hit)
 
 
+@pytest.mark.parametrize("symmetric", [False, True])
+def test_pacing_layer_counts_complete(symmetric):
+    """Both CTA-pair forms pace their producers on a global count of issued
+    tile layers.  The layer count must close on every schedule shape, or a
+    producer waits forever (the launch traps after 20 s):
+      * streaming pair, 69 x 69 tiles of 256 on 74 pairs (148 SMs): every pair
+        has 64 tiles and 25 have 65 -- a last block of exactly 64 layers;
+      * resident pair, 79 row tiles x 2 column segments = 158 units on 74
+        pairs: a partial last unit layer.
+    Records equal the unpaced single-CTA streaming form bit for bit
+    (symmetric: tiles skipped below the diagonal still count as layers)."""
+    flags = _lib.JOIN_SYMMETRIC if symmetric else 0
+    hd = F.to_half(F.generate_synthetic(69 * 256, 520, seed=69))
+    one = _tc_variant(hd, 8.6, flags=flags, FASTED_CTA_GROUP=1, FASTED_RESIDENT=0)
+    pair = _tc_variant(hd, 8.6, flags=flags, FASTED_CTA_GROUP=2, FASTED_STREAM_PACE_W=1)
+    assert len(one[0]) > 69 * 256 and _same(one, pair)
+    hd = F.to_half(F.generate_synthetic(20000, 128, seed=79))
+    one = _tc_variant(hd, 3.7, flags=flags, FASTED_CTA_GROUP=1, FASTED_RESIDENT=0)
+    for w in (1, 2):
+        res = _tc_variant(hd, 3.7, flags=flags, FASTED_PACE_W=w, FASTED_SEG_TILES=40)
+        assert len(one[0]) > 20000 and _same(one, res), w
+
+
 def test_sort_long_rows_bucket_and_fallback_paths():
     """Rows above 16384 records: spread j -> column buckets + shared-memory
     bitonic per bucket; j clustered in one bucket -> the bitmap fallback.
