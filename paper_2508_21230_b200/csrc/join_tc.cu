@@ -1822,7 +1822,25 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         // ---------------- TMA producer (whole warp; one elected lane issues)
         int s = 0;
         uint32_t ph = 0;
-        for (int64_t t = tile_id0; t < sch.total; t += tile_step) {
+        int64_t k = 0;   // this cluster's tile layer (pacing, as the streaming kernel)
+        for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++k) {
+            if (sch.pace_w > 0 && k % PACE_TILES == 0 && k > 0) {
+                const int64_t b = k / PACE_TILES;
+                if (lane == 0) {
+                    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.pace)
+                                 : "memory");
+                    if (b >= sch.pace_w) {
+                        const unsigned long long need =
+                            pace_need_stream(sch.total, tile_step, b - sch.pace_w, 2);
+                        const uint64_t t0 = global_timer();
+                        while (ld_acquire_gpu_u64(a.pace) < need) {
+                            __nanosleep(64);
+                            if (global_timer() - t0 > 20000000000ull) __trap();
+                        }
+                    }
+                }
+                __syncwarp();
+            }
             int rt, ct;
             tile_coords(sch, t, rt, ct);
             if (sym_skip(a, a.row_begin + (int64_t)rt * 2 * BM, a.col_begin + (int64_t)ct * BN,
@@ -1854,6 +1872,8 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
                 }
             }
         }
+        if (sch.pace_w > 0 && k > 0 && k % PACE_TILES == 0 && lane == 0)   // a final full block
+            asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.pace) : "memory");
     } else if (warp == 1) {
         // ---------------- MMA issuer (every CTA; M = 128; whole warp, one lane issues)
         const bool no_mma = (FASTED_DFLAGS(a) & FASTED_JOIN_DIAG_NOMMA) != 0;
@@ -2811,6 +2831,7 @@ static cudaError_t launch_mc(const CUtensorMap& mx, const CUtensorMap& ma, const
     if (sch.group < 1) sch.group = 1;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.total = (int64_t)sch.row_tiles * sch.col_tiles;
+    sch.pace_w = a.pace ? FASTED_KNOB("FASTED_MC_PACE_W", 0) : 0;
     const int64_t slots = sm_count_current() / 2;
     const int64_t work = sch.total < slots ? sch.total : slots;
     if (work <= 0) return cudaSuccess;
@@ -3179,8 +3200,8 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
             e = launch_mc<8>(mx, ma, mb, a, s);
         else
 #endif
-            e = mc_hit(a.sparse != 0) ? launch_mc<16, 2>(mx, ma, mb, a, s)
-                                      : launch_mc<16>(mx, ma, mb, a, s);
+            e = mc_hit(a.sparse != 0) ? launch_mc<16, 2>(mx, ma, mb, ar, s)
+                                      : launch_mc<16>(mx, ma, mb, ar, s);
         if (e == cudaSuccess) e = cudaGetLastError();
         cudaFreeAsync(aug, s);
         if (e != cudaSuccess) return cuda_status(e, "join_tc_mc_kernel");

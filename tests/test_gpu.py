@@ -804,6 +804,9 @@ def test_pacing_layer_counts_complete(symmetric):
     one = _tc_variant(hd, 8.6, flags=flags, FASTED_CTA_GROUP=1, FASTED_RESIDENT=0)
     pair = _tc_variant(hd, 8.6, flags=flags, FASTED_CTA_GROUP=2, FASTED_STREAM_PACE_W=1)
     assert len(one[0]) > 69 * 256 and _same(one, pair)
+    # multicast clusters: 35 super-rows x 69 column tiles = 2415 tiles on 74 clusters
+    mc = _tc_variant(hd, 8.6, flags=flags, FASTED_MC=1, FASTED_CTA_GROUP=0, FASTED_MC_PACE_W=1)
+    assert _same(one, mc)
     hd = F.to_half(F.generate_synthetic(20000, 128, seed=79))
     one = _tc_variant(hd, 3.7, flags=flags, FASTED_CTA_GROUP=1, FASTED_RESIDENT=0)
     for w in (1, 2):
