@@ -2953,7 +2953,8 @@ static int tc_variant(int64_t d_pad, int64_t rows, int64_t cols, bool low_output
     *cg = cg_env == 1 ? 1 : cg_env == 2 ? 2 : (d_pad <= res_max ? 2 : 1);
     if (d_pad <= res_max) return FASTED_KNOB("FASTED_RESIDENT", 1) != 0 ? TC_RESIDENT : TC_STREAMING;
     if (cg_env != 0 || FASTED_KNOB("FASTED_MC", 1) == 0) return TC_STREAMING;
-    if (low_output && (double)rows * (double)cols >= 68.7e9) {   // >= 2^36 pairs examined
+    if (low_output && (double)rows * (double)cols >= 68.7e9 &&   // >= 2^36 pairs examined
+        FASTED_KNOB("FASTED_PAIR_LOWOUT", 1) != 0) {
         *cg = 2;
         return TC_STREAMING;
     }
