@@ -2009,6 +2009,7 @@ struct ResSched {
     uint32_t epi_sleep_ns;    // epilogue accumulator wait backoff (0: suspend hint)
     int mma_spin = MMA_SPIN_DEFAULT;   // MMA_SPIN_DEFAULT bits (FASTED_MMA_SPIN in experiments)
     int pace_w = 0;           // unit layers a CTA may run ahead of the slowest (0: unpaced)
+    int order = 0;            // unit order: 0 row-tile rounds, 1 segment-major
 };
 
 // Records per staging buffer in the resident kernel (tight shared memory):
@@ -2048,7 +2049,10 @@ __device__ __forceinline__ unsigned long long pace_need(const ResSched& s, int64
     return (unsigned long long)cg * (unsigned long long)(t * s.lanes + (j >= full ? rem : 0));
 }
 
-// Unit order: rounds of `lanes` row tiles.  Inside a round, lane (pair) p
+// Unit order (ResSched::order).  1, the default: segment-major -- unit u is
+// row tile u % row_tiles of column segment u / row_tiles, so the co-running
+// pairs sweep neighbouring row tiles of the same B segment and a pair that
+// runs a few units ahead is still on it.  0: rounds of `lanes` row tiles.  Inside a round, lane (pair) p
 // keeps row tile round * lanes + p and sweeps the column segments in order,
 // all lanes on the same segment at the same time -- so co-running pairs share
 // each B panel in L2 (as a segment-major order would), each pair's A panel
@@ -2059,6 +2063,13 @@ __device__ __forceinline__ unsigned long long pace_need(const ResSched& s, int64
 // lanes (unit v -> row tile v % m, segment v / m).
 __device__ __forceinline__ void res_unit(const ResSched& s, int64_t u, int& rt, int& ct0,
                                          int& ct1) {
+    if (s.order == 1) {   // segment-major: all row tiles on segment 0, then segment 1, ...
+        const int64_t g = u / s.row_tiles;
+        rt = (int)(u - g * s.row_tiles);
+        ct0 = (int)((int64_t)s.col_tiles * g / s.nsegs);
+        ct1 = (int)((int64_t)s.col_tiles * (g + 1) / s.nsegs);
+        return;
+    }
     const int64_t per_round = (int64_t)s.lanes * s.nsegs;
     const int64_t R = u / per_round;
     const int64_t v = u - R * per_round;
@@ -2901,6 +2912,10 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     // bounded drift of 2 unit layers (C3 243-247 vs 291 ms, HBM reads 47 vs 712 GB per
     // launch; C5 shard S~4096 1998 vs 2621 ms; S~256 unchanged -- pace_ab.txt)
     sch.pace_w = a.pace ? FASTED_KNOB("FASTED_PACE_W", 2) : 0;
+    // segment-major unit order (with pacing: C3 234 vs 244 ms, C5 shard S~4096 1970 vs
+    // 2090 ms, S~1024 1677 vs 1721, C2 2.67 vs 2.80 ms; the S~4096 sort is 115 vs 82 ms
+    // because a row's records spread over the launch -- profiles/round2/unit_order_ab.txt)
+    sch.order = FASTED_KNOB("FASTED_RES_ORDER", 1);
     sch.mma_spin = FASTED_KNOB("FASTED_MMA_SPIN", MMA_SPIN_DEFAULT);
     int seg = FASTED_KNOB("FASTED_SEG_TILES", 16384 / TBN);
     if (seg < 1) seg = 1;
@@ -3004,6 +3019,7 @@ static cudaError_t launch_ts(const __half* X, const CUtensorMap& mxb, const CUte
     ResSched sch;
     sch.epi_sleep_ns = 0u;
     sch.mma_spin = 0;
+    sch.order = 0;
     sch.nkb = (int)((a.d_pad + BK - 1) / BK);
     sch.na = 2;
     sch.a_buf_bytes = 0;
