@@ -298,8 +298,7 @@ def measure_workload(dd, n, d, eps, rows, peaks, device, reps, warmup, host_copy
     sout = (torch.empty(max(pairs, 1), dtype=torch.int32, device=dev),
             torch.empty(max(pairs, 1), dtype=torch.int32, device=dev),
             torch.empty(max(pairs, 1), dtype=torch.float32, device=dev))
-    stmp = (torch.empty(max(pairs, 1), dtype=torch.int32, device=dev),
-            torch.empty(max(pairs, 1), dtype=torch.float32, device=dev))
+    stmp = torch.empty(max(pairs, 1), dtype=torch.int64, device=dev)   # 8-byte (j, d) scratch
     sws = torch.empty(max(L.fasted_sort_workspace_bytes(rows[1] - rows[0], dd.n_dev), 1),
                       dtype=torch.uint8, device=dev)
 

@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define FASTED_ABI_VERSION 1
+#define FASTED_ABI_VERSION 2
 
 enum {
     FASTED_OK = 0,
@@ -155,14 +155,15 @@ int fasted_join(const uint16_t* values16, const float* norms, int64_t n_logical,
  * (16-byte records from fasted_join; slots with i == 0 are unused and
  * dropped) whose i lie in [row_begin+1, row_end] and j in [1, n_cols].
  * Writes the valid records, sorted, to out_i/out_j/out_d (SoA, length >=
- * number of valid records); tmp_j/tmp_d are scratch of the same length.
+ * number of valid records).  tmp is 8-byte aligned scratch of tmp_bytes >=
+ * 8 bytes per valid record (the row-bucketed (j, dist_sq) pairs).
  * workspace must hold fasted_sort_workspace_bytes(row_end - row_begin,
- * n_cols) bytes.
+ * n_cols) bytes.  (ABI version 2: version 1 took two 4-byte scratch arrays.)
  */
 size_t fasted_sort_workspace_bytes(int64_t n_rows, int64_t n_cols);
 int fasted_sort_pairs(const void* records, uint64_t slots, int64_t row_begin, int64_t row_end,
                       int64_t n_cols, uint32_t* out_i, uint32_t* out_j, float* out_d,
-                      uint32_t* tmp_j, float* tmp_d, void* workspace, size_t workspace_bytes,
+                      void* tmp, size_t tmp_bytes, void* workspace, size_t workspace_bytes,
                       void* stream);
 
 /*

@@ -83,11 +83,11 @@ def _load(path):
         L.fasted_sort_workspace_bytes.restype = ctypes.c_size_t
         L.fasted_sort_workspace_bytes.argtypes = [i64, i64]
         L.fasted_sort_pairs.restype = ci
-        L.fasted_sort_pairs.argtypes = [p, u64, i64, i64, i64, p, p, p, p, p, p,
-                                        ctypes.c_size_t, p]
+        L.fasted_sort_pairs.argtypes = [p, u64, i64, i64, i64, p, p, p, p, ctypes.c_size_t,
+                                        p, ctypes.c_size_t, p]
         L.fasted_fp64_rows.restype = ci
         L.fasted_fp64_rows.argtypes = [p, i64, i64, p, i64, ctypes.c_double, p, u64, p, p]
-        if L.fasted_abi_version() != 1:
+        if L.fasted_abi_version() != 2:
             raise DeviceError("libfasted ABI version mismatch")
         _libs[path] = L
         return L

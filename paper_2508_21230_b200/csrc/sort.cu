@@ -134,6 +134,31 @@ __device__ __forceinline__ uint32_t sort_lanemask_lt() {
     return m;
 }
 
+// Row-segment readers: the scatter's scratch is AoS (j, dist_sq bits) in 8
+// bytes (one store per record instead of two scattered 4-byte stores, each
+// an L2 request and a partial 32-byte sector); the super-bucket path sorts
+// the final SoA arrays in place.
+struct JdAoS {
+    const uint2* p;
+    __device__ __forceinline__ uint32_t j(uint64_t e) const { return p[e].x; }
+    __device__ __forceinline__ void jd(uint64_t e, uint32_t& j, float& d) const {
+        const uint2 v = p[e];
+        j = v.x;
+        d = __uint_as_float(v.y);
+    }
+    __device__ __forceinline__ JdAoS at(uint64_t o) const { return JdAoS{p + o}; }
+};
+struct JdSoA {
+    const uint32_t* pj;
+    const float* pd;
+    __device__ __forceinline__ uint32_t j(uint64_t e) const { return pj[e]; }
+    __device__ __forceinline__ void jd(uint64_t e, uint32_t& j, float& d) const {
+        j = pj[e];
+        d = pd[e];
+    }
+    __device__ __forceinline__ JdSoA at(uint64_t o) const { return JdSoA{pj + o, pd + o}; }
+};
+
 __global__ void __launch_bounds__(256)
 hist_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
             uint32_t* __restrict__ counts) {
@@ -250,7 +275,7 @@ __global__ void scan_add_kernel(unsigned long long* __restrict__ offsets, int64_
 __global__ void __launch_bounds__(256)
 scatter_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
                const unsigned long long* __restrict__ offsets, uint32_t* __restrict__ cursor,
-               uint32_t* __restrict__ tj, float* __restrict__ td) {
+               uint2* __restrict__ tjd, unsigned long long tjd_cap) {
     const uint64_t pol = stream_policy();
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
@@ -280,15 +305,14 @@ scatter_kernel(const uint4* __restrict__ rec, uint64_t count, int64_t row_begin,
         for (int k = 0; k < SORT_ILP; k++) {
             if (v[k].x == 0) continue;
             const unsigned long long pos = offsets[(int64_t)v[k].x - 1 - row_begin] + c[k];
-            tj[pos] = v[k].y;
-            td[pos] = __uint_as_float(v[k].z);
+            if (pos < tjd_cap) tjd[pos] = make_uint2(v[k].y, v[k].z);
         }
     }
 }
 
 // One warp per row: rank-by-comparison inside shared memory.
 __global__ void __launch_bounds__(SHORT_WARPS * 32)
-short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
+short_rows_kernel(const uint2* __restrict__ tjd,
                   const unsigned long long* __restrict__ offsets, int64_t n_rows,
                   int64_t row_begin, uint32_t* __restrict__ oi, uint32_t* __restrict__ oj,
                   float* __restrict__ od, uint32_t* __restrict__ long_rows,
@@ -310,7 +334,7 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
             }
             continue;
         }
-        for (uint32_t e = lane; e < len; e += 32) keys[w][e] = tj[s0 + e];
+        for (uint32_t e = lane; e < len; e += 32) keys[w][e] = tjd[s0 + e].x;
         __syncwarp();
         for (uint32_t e = lane; e < len; e += 32) {
             const uint32_t k = keys[w][e];
@@ -318,7 +342,7 @@ short_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
             for (uint32_t q = 0; q < len; q++) rank += keys[w][q] < k;
             oi[s0 + rank] = (uint32_t)(row_begin + r + 1);
             oj[s0 + rank] = k;
-            od[s0 + rank] = td[s0 + e];
+            od[s0 + rank] = __uint_as_float(tjd[s0 + e].y);
         }
         __syncwarp();
     }
@@ -415,8 +439,8 @@ __device__ uint32_t block_scan_excl(uint32_t* a, uint32_t n, uint32_t* red) {
 // scatter into shared memory, then each record's rank inside its bucket by
 // comparison.  Returns false (nothing written) if some bucket holds more
 // than RANK_BUCKET_MAX records (clustered j): the caller sorts otherwise.
-template <int CAP>
-__device__ bool rank_sort_segment(const uint32_t* sj, const float* sd, uint32_t L, uint32_t* dj,
+template <int CAP, typename Src>
+__device__ bool rank_sort_segment(const Src src, uint32_t L, uint32_t* dj,
                                   float* dd, uint32_t* di, uint32_t row1, RankSmem<CAP>& S) {
     // the row is read from global memory ONCE, into registers (element
     // threadIdx.x + k * blockDim.x in slot k; every launch of a CAP tier
@@ -428,8 +452,9 @@ __device__ bool rank_sort_segment(const uint32_t* sj, const float* sd, uint32_t 
 #pragma unroll
     for (int k = 0; k < RANK_PER; k++) {
         const uint32_t e = threadIdx.x + (uint32_t)k * blockDim.x;
-        vj[k] = e < L ? sj[e] : 0u;
-        vd[k] = e < L ? sd[e] : 0.0f;
+        vj[k] = 0u;
+        vd[k] = 0.0f;
+        if (e < L) src.jd(e, vj[k], vd[k]);
         if (e < L) {
             mn = min(mn, vj[k]);
             mx = max(mx, vj[k]);
@@ -499,15 +524,19 @@ __device__ bool rank_sort_segment(const uint32_t* sj, const float* sd, uint32_t 
 
 // Bitonic fallback for a segment of L <= CAP records (dst may alias src):
 // (j << 32 | d bits) keys in the rank sort's shared memory.
-template <int CAP>
-__device__ void bitonic_segment(const uint32_t* sj, const float* sd, uint32_t L, uint32_t* dj,
+template <int CAP, typename Src>
+__device__ void bitonic_segment(const Src src, uint32_t L, uint32_t* dj,
                                 float* dd, uint32_t* di, uint32_t row1, RankSmem<CAP>& S) {
     unsigned long long* key = reinterpret_cast<unsigned long long*>(S.bj);
     uint32_t n = 1;
     while (n < L) n <<= 1;
-    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x)
-        key[e] = e < L ? ((unsigned long long)sj[e] << 32) | (unsigned long long)__float_as_uint(sd[e])
+    for (uint32_t e = threadIdx.x; e < n; e += blockDim.x) {
+        uint32_t j = 0u;
+        float d = 0.0f;
+        if (e < L) src.jd(e, j, d);
+        key[e] = e < L ? ((unsigned long long)j << 32) | (unsigned long long)__float_as_uint(d)
                        : ~0ull;
+    }
     __syncthreads();
     block_bitonic(key, n);
     for (uint32_t e = threadIdx.x; e < L; e += blockDim.x) {
@@ -523,7 +552,7 @@ __device__ void bitonic_segment(const uint32_t* sj, const float* sd, uint32_t L,
 // bucket overflows.
 template <int CAP, int THREADS>
 __global__ void __launch_bounds__(THREADS)
-rank_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
+rank_rows_kernel(const uint2* __restrict__ tjd,
                  const unsigned long long* __restrict__ offsets, int64_t row_begin,
                  const uint32_t* __restrict__ rows, const uint32_t* __restrict__ nrows,
                  uint32_t* __restrict__ oi, uint32_t* __restrict__ oj, float* __restrict__ od) {
@@ -535,8 +564,9 @@ rank_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
         const unsigned long long s0 = offsets[r];
         const uint32_t len = (uint32_t)(offsets[r + 1] - s0);
         const uint32_t row1 = (uint32_t)(row_begin + r + 1);
-        if (!rank_sort_segment<CAP>(tj + s0, td + s0, len, oj + s0, od + s0, oi + s0, row1, S))
-            bitonic_segment<CAP>(tj + s0, td + s0, len, oj + s0, od + s0, oi + s0, row1, S);
+        const JdAoS src{tjd + s0};
+        if (!rank_sort_segment<CAP>(src, len, oj + s0, od + s0, oi + s0, row1, S))
+            bitonic_segment<CAP>(src, len, oj + s0, od + s0, oi + s0, row1, S);
     }
 }
 
@@ -547,7 +577,7 @@ constexpr uint32_t SUPER_TARGET = BIG_MAX / 2;   // expected records per column 
 // scatter in place into the row's final slots of out_j/out_d), then a rank
 // sort of each, in place.
 __global__ void __launch_bounds__(BIG_THREADS)
-bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
+bucket_rows_kernel(const uint2* __restrict__ tjd,
                    const unsigned long long* __restrict__ offsets, int64_t row_begin,
                    int64_t n_cols, const uint32_t* __restrict__ long_rows,
                    const uint32_t* __restrict__ long_count, uint32_t* __restrict__ fb_rows,
@@ -569,7 +599,7 @@ bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td
         if (threadIdx.x == 0) overflow = 0;
         __syncthreads();
         for (uint32_t e = threadIdx.x; e < len; e += blockDim.x)
-            atomicAdd(&cnt[(tj[s0 + e] - 1u) / bw], 1u);
+            atomicAdd(&cnt[(tjd[s0 + e].x - 1u) / bw], 1u);
         __syncthreads();
         if (threadIdx.x == 0) {   // nb <= 1024: a serial scan is cheap next to the row
             uint32_t run = 0;
@@ -588,10 +618,10 @@ bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td
             continue;
         }
         for (uint32_t e = threadIdx.x; e < len; e += blockDim.x) {
-            const uint32_t j = tj[s0 + e];
-            const uint32_t pos = atomicAdd(&cur[(j - 1u) / bw], 1u);
-            oj[s0 + pos] = j;
-            od[s0 + pos] = td[s0 + e];
+            const uint2 v = tjd[s0 + e];
+            const uint32_t pos = atomicAdd(&cur[(v.x - 1u) / bw], 1u);
+            oj[s0 + pos] = v.x;
+            od[s0 + pos] = __uint_as_float(v.y);
         }
         __syncthreads();   // the block's own global writes are visible to it after this
         const uint32_t row1 = (uint32_t)(row_begin + r + 1);
@@ -600,15 +630,16 @@ bucket_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td
             if (bl == 0) continue;
             uint32_t* sj = oj + s0 + b0;
             float* sd = od + s0 + b0;
-            if (!rank_sort_segment<BIG_MAX>(sj, sd, bl, sj, sd, oi + s0 + b0, row1, S))
-                bitonic_segment<BIG_MAX>(sj, sd, bl, sj, sd, oi + s0 + b0, row1, S);
+            const JdSoA src{sj, sd};
+            if (!rank_sort_segment<BIG_MAX>(src, bl, sj, sd, oi + s0 + b0, row1, S))
+                bitonic_segment<BIG_MAX>(src, bl, sj, sd, oi + s0 + b0, row1, S);
         }
     }
 }
 
 // One block per long row: bitmap ranks over the column range.
 __global__ void __launch_bounds__(LONG_THREADS)
-long_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
+long_rows_kernel(const uint2* __restrict__ tjd,
                  const unsigned long long* __restrict__ offsets, int64_t row_begin,
                  int64_t n_cols, const uint32_t* __restrict__ long_rows,
                  const uint32_t* __restrict__ long_count, uint32_t* __restrict__ bitmap_all,
@@ -626,7 +657,7 @@ long_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
         for (int64_t w = threadIdx.x; w < words; w += blockDim.x) bits[w] = 0;
         __syncthreads();
         for (unsigned long long e = s0 + threadIdx.x; e < s1; e += blockDim.x) {
-            const uint32_t j0 = tj[e] - 1;
+            const uint32_t j0 = tjd[e].x - 1;
             atomicOr(&bits[j0 >> 5], 1u << (j0 & 31));
         }
         __syncthreads();
@@ -651,13 +682,14 @@ long_rows_kernel(const uint32_t* __restrict__ tj, const float* __restrict__ td,
             __syncthreads();
         }
         for (unsigned long long e = s0 + threadIdx.x; e < s1; e += blockDim.x) {
-            const uint32_t j = tj[e];
+            const uint2 v = tjd[e];
+            const uint32_t j = v.x;
             const uint32_t j0 = j - 1;
             const uint32_t rank =
                 pref[j0 >> 5] + (uint32_t)__popc(bits[j0 >> 5] & ((1u << (j0 & 31)) - 1u));
             oi[s0 + rank] = (uint32_t)(row_begin + r + 1);
             oj[s0 + rank] = j;
-            od[s0 + rank] = td[e];
+            od[s0 + rank] = __uint_as_float(v.y);
         }
         __syncthreads();
     }
@@ -674,12 +706,14 @@ extern "C" size_t fasted_sort_workspace_bytes(int64_t n_rows, int64_t n_cols) {
 
 extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t row_begin,
                                  int64_t row_end, int64_t n_cols, uint32_t* out_i,
-                                 uint32_t* out_j, float* out_d, uint32_t* tmp_j, float* tmp_d,
+                                 uint32_t* out_j, float* out_d, void* tmp, size_t tmp_bytes,
                                  void* workspace, size_t workspace_bytes, void* stream) {
     const int64_t n_rows = row_end - row_begin;
     if (count == 0) return FASTED_OK;
     const uint4* rec = static_cast<const uint4*>(records);
-    if (!rec || !out_i || !out_j || !out_d || !tmp_j || !tmp_d || !workspace || n_rows < 1 ||
+    uint2* tjd = static_cast<uint2*>(tmp);
+    if (!rec || !out_i || !out_j || !out_d || !tmp || (reinterpret_cast<uintptr_t>(tmp) & 7u) ||
+        tmp_bytes < 8 || !workspace || n_rows < 1 ||
         n_cols < 1 || n_cols > 0xffffffffLL) {
         set_error("fasted_sort_pairs: bad arguments");
         return FASTED_ERR_ARGUMENT;
@@ -713,12 +747,12 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
     FASTED_CHECK_LAUNCH("scan_blocks_kernel");
     scan_add_kernel<<<(unsigned)((n_rows + 255) / 256), 256, 0, s>>>(ws.offsets, n_rows, ws.bsum);
     FASTED_CHECK_LAUNCH("scan_add_kernel");
-    scatter_kernel<<<rec_grid, 256, 0, s>>>(rec, count, row_begin, ws.offsets, ws.cursor, tmp_j,
-                                            tmp_d);
+    scatter_kernel<<<rec_grid, 256, 0, s>>>(rec, count, row_begin, ws.offsets, ws.cursor, tjd,
+                                            (unsigned long long)(tmp_bytes / 8));
     FASTED_CHECK_LAUNCH("scatter_kernel");
     const int64_t sgrid = (n_rows + SHORT_WARPS - 1) / SHORT_WARPS;
     short_rows_kernel<<<(unsigned)(sgrid < (int64_t)sms * 64 ? sgrid : (int64_t)sms * 64),
-                        SHORT_WARPS * 32, 0, s>>>(tmp_j, tmp_d, ws.offsets, n_rows, row_begin,
+                        SHORT_WARPS * 32, 0, s>>>(tjd, ws.offsets, n_rows, row_begin,
                                                   out_i, out_j, out_d, ws.long_rows,
                                                   ws.long_count, ws.mid_rows, ws.mid_count,
                                                   ws.big_rows, ws.big_count);
@@ -742,16 +776,16 @@ extern "C" int fasted_sort_pairs(const void* records, uint64_t count, int64_t ro
         if (e != cudaSuccess) return cuda_status(e, "rank sort attributes");
     }
     rank_rows_kernel<MID_MAX, RANK_THREADS><<<(unsigned)(sms * 6), RANK_THREADS, RankSmem<MID_MAX>::BYTES, s>>>(
-        tmp_j, tmp_d, ws.offsets, row_begin, ws.mid_rows, ws.mid_count, out_i, out_j, out_d);
+        tjd, ws.offsets, row_begin, ws.mid_rows, ws.mid_count, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("rank_rows_kernel<4096>");
     rank_rows_kernel<BIG_MAX, BIG_THREADS><<<(unsigned)sms, BIG_THREADS, RankSmem<BIG_MAX>::BYTES, s>>>(
-        tmp_j, tmp_d, ws.offsets, row_begin, ws.big_rows, ws.big_count, out_i, out_j, out_d);
+        tjd, ws.offsets, row_begin, ws.big_rows, ws.big_count, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("rank_rows_kernel<16384>");
     bucket_rows_kernel<<<(unsigned)sms, BIG_THREADS, RankSmem<BIG_MAX>::BYTES, s>>>(
-        tmp_j, tmp_d, ws.offsets, row_begin, n_cols, ws.long_rows, ws.long_count, ws.fb_rows,
+        tjd, ws.offsets, row_begin, n_cols, ws.long_rows, ws.long_count, ws.fb_rows,
         ws.fb_count, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("bucket_rows_kernel");
-    long_rows_kernel<<<LONG_BLOCKS, LONG_THREADS, 0, s>>>(tmp_j, tmp_d, ws.offsets, row_begin,
+    long_rows_kernel<<<LONG_BLOCKS, LONG_THREADS, 0, s>>>(tjd, ws.offsets, row_begin,
                                                           n_cols, ws.fb_rows, ws.fb_count,
                                                           ws.bitmap, out_i, out_j, out_d);
     FASTED_CHECK_LAUNCH("long_rows_kernel");

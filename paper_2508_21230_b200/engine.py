@@ -310,25 +310,25 @@ def _sort_records(dd: DeviceData, rec, slots: int, count: int, rows, stream, out
         ws_bytes = L.fasted_sort_workspace_bytes(rows[1] - rows[0], dd.n_dev)
         if ws is None or ws.numel() < ws_bytes:
             ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
-        if tmp is None or tmp[0].shape[0] < count:
-            tj = torch.empty(count, dtype=torch.int32, device=dev)
-            td = torch.empty(count, dtype=torch.float32, device=dev)
+        # scratch: the row-bucketed (j, dist_sq) pairs, 8 bytes per valid record
+        if tmp is None or tmp.numel() < count:
+            tjd = torch.empty(count, dtype=torch.int64, device=dev)
         else:
-            tj, td = tmp
+            tjd = tmp
         if timed:
             s0 = torch.cuda.Event(enable_timing=True)
             s1 = torch.cuda.Event(enable_timing=True)
             s0.record(stream)
         _lib.check(L.fasted_sort_pairs(rec.data_ptr(), slots, rows[0], rows[1], dd.n_dev,
                                        oi.data_ptr(), oj.data_ptr(), od.data_ptr(),
-                                       tj.data_ptr(), td.data_ptr(), ws.data_ptr(), ws.numel(),
+                                       tjd.data_ptr(), tjd.numel() * 8, ws.data_ptr(), ws.numel(),
                                        stream.cuda_stream),
                    "fasted_sort_pairs")
         if timed:
             s1.record(stream)
             s1.synchronize()
             sort_ms = s0.elapsed_time(s1)
-        del ws, tj, td   # stream-ordered reuse by the caching allocator is safe
+        del ws, tjd   # stream-ordered reuse by the caching allocator is safe
     return oi, oj, od, sort_ms
 
 
@@ -574,8 +574,7 @@ def stream_join(dd: DeviceData, eps_sq: float, rows, exact: bool, host: HostPair
                       for _ in range(nbuf)]
         if nbuf == 1:
             sorted_out.append(sorted_out[0])
-        sort_tmp = (torch.empty(out_cap, dtype=torch.int32, device=dev),
-                    torch.empty(out_cap, dtype=torch.float32, device=dev))
+        sort_tmp = torch.empty(out_cap, dtype=torch.int64, device=dev)
         max_rows = max(ch[1] - ch[0] for ch in chunks)
         sort_ws = torch.empty(max(L.fasted_sort_workspace_bytes(max_rows, dd.n_dev), 1),
                               dtype=torch.uint8, device=dev)

@@ -101,8 +101,7 @@ def main():
         sout = (torch.empty(max(pairs, 1), dtype=torch.int32, device=dev),
                 torch.empty(max(pairs, 1), dtype=torch.int32, device=dev),
                 torch.empty(max(pairs, 1), dtype=torch.float32, device=dev))
-        stmp = (torch.empty(max(pairs, 1), dtype=torch.int32, device=dev),
-                torch.empty(max(pairs, 1), dtype=torch.float32, device=dev))
+        stmp = torch.empty(max(pairs, 1), dtype=torch.int64, device=dev)   # 8-byte (j, d) scratch
         sws = torch.empty(L.fasted_sort_workspace_bytes(rows[1] - rows[0], dd.n_dev),
                           dtype=torch.uint8, device=dev)
         sort = lambda: engine._sort_records(dd, rec, slots, pairs, rows, stream, out=sout,

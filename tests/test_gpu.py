@@ -397,12 +397,12 @@ def test_sort_pairs_random_records(n_rows, maxc):
     L = _lib.load()
     trec = torch.from_numpy(rec).cuda()
     oi, oj = torch.empty(len(i), dtype=torch.int32, device="cuda"), torch.empty(len(i), dtype=torch.int32, device="cuda")
-    od, tj = torch.empty(len(i), dtype=torch.float32, device="cuda"), torch.empty(len(i), dtype=torch.int32, device="cuda")
-    td = torch.empty(len(i), dtype=torch.float32, device="cuda")
+    od = torch.empty(len(i), dtype=torch.float32, device="cuda")
+    tjd = torch.empty(len(i), dtype=torch.int64, device="cuda")   # 8-byte (j, d) scratch
     wsb = L.fasted_sort_workspace_bytes(n_rows, n_cols)
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     _lib.check(L.fasted_sort_pairs(trec.data_ptr(), len(rec), 0, n_rows, n_cols, oi.data_ptr(),
-                                   oj.data_ptr(), od.data_ptr(), tj.data_ptr(), td.data_ptr(),
+                                   oj.data_ptr(), od.data_ptr(), tjd.data_ptr(), tjd.numel() * 8,
                                    ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream),
                "sort")
     order = np.lexsort((j, i))
@@ -833,12 +833,13 @@ def test_sort_long_rows_bucket_and_fallback_paths():
     L = _lib.load()
     trec = torch.from_numpy(rec).cuda()
     n = len(i)
-    oi, oj, tj = (torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3))
-    od, td = (torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(2))
+    oi, oj = (torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(2))
+    od = torch.empty(n, dtype=torch.float32, device="cuda")
+    tjd = torch.empty(n, dtype=torch.int64, device="cuda")   # 8-byte (j, d) scratch
     wsb = L.fasted_sort_workspace_bytes(len(rows), n_cols)
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     _lib.check(L.fasted_sort_pairs(trec.data_ptr(), n, 0, len(rows), n_cols, oi.data_ptr(),
-                                   oj.data_ptr(), od.data_ptr(), tj.data_ptr(), td.data_ptr(),
+                                   oj.data_ptr(), od.data_ptr(), tjd.data_ptr(), tjd.numel() * 8,
                                    ws.data_ptr(), wsb, torch.cuda.current_stream().cuda_stream),
                "sort")
     order = np.lexsort((j, i))
@@ -860,13 +861,14 @@ def _sort_rows_on_device(rows, n_cols, seed=0):
     L = _lib.load()
     trec = torch.from_numpy(rec).cuda()
     n = len(i)
-    oi, oj, tj = (torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(3))
-    od, td = (torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(2))
+    oi, oj = (torch.empty(n, dtype=torch.int32, device="cuda") for _ in range(2))
+    od = torch.empty(n, dtype=torch.float32, device="cuda")
+    tjd = torch.empty(n, dtype=torch.int64, device="cuda")   # 8-byte (j, d) scratch
     wsb = L.fasted_sort_workspace_bytes(len(rows), n_cols)
     ws = torch.empty(wsb, dtype=torch.uint8, device="cuda")
     _lib.check(L.fasted_sort_pairs(trec.data_ptr(), len(rec), 0, len(rows), n_cols,
-                                   oi.data_ptr(), oj.data_ptr(), od.data_ptr(), tj.data_ptr(),
-                                   td.data_ptr(), ws.data_ptr(), wsb,
+                                   oi.data_ptr(), oj.data_ptr(), od.data_ptr(), tjd.data_ptr(),
+                                   tjd.numel() * 8, ws.data_ptr(), wsb,
                                    torch.cuda.current_stream().cuda_stream), "sort")
     order = np.lexsort((j, i))
     return (i[order], j[order], d[order]), (oi.cpu().numpy(), oj.cpu().numpy(), od.cpu().numpy())

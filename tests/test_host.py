@@ -35,7 +35,7 @@ def test_library_exports_every_header_symbol():
 
 def test_library_host_calls_without_gpu():
     L = _lib.load()
-    assert L.fasted_abi_version() == 1
+    assert L.fasted_abi_version() == 2
     assert L.fasted_strerror(3) == b"value out of FP16 range"
     assert L.fasted_sort_workspace_bytes(1000, 1000) > 0
     # argument validation happens before any device work
