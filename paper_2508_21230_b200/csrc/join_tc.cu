@@ -3082,6 +3082,24 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     float4* aug = nullptr;
     // (+ 256 bytes: the resident kernel's pacing counter)
     const size_t aug_bytes = (size_t)a.n_pad * 64 + (size_t)a.n_pad * 4 + 256;
+    // The per-call scratch comes from the device's default stream-ordered pool.
+    // Its release threshold defaults to 0, so every synchronisation handed the
+    // freed scratch back to the driver and the next call's cudaMallocAsync
+    // mapped it again, on the timed path (60K x 512: 2.5-4 ms per 2.5 ms join
+    // from one launch to the next).  Keep up to 1 GiB cached in the pool.
+    static PerDeviceOnce pool_once;
+    pool_once.run([] {
+        int dev = 0;
+        cudaMemPool_t pool;
+        cudaError_t r = cudaGetDevice(&dev);
+        if (r == cudaSuccess) r = cudaDeviceGetDefaultMemPool(&pool, dev);
+        if (r == cudaSuccess && FASTED_KNOB("FASTED_POOL_KEEP", 1) != 0) {
+            uint64_t keep = 1ull << 30;
+            r = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        (void)cudaGetLastError();
+        return cudaSuccess;
+    });
     cudaError_t e = cudaMallocAsync(&aug, aug_bytes, s);
     if (e != cudaSuccess) return cuda_status(e, "cudaMallocAsync(augment rows)");
     float4* aug_a = aug;
