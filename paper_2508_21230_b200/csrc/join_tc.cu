@@ -3209,9 +3209,9 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
         if (ts)
             e = launch_ts(X, mxb, ma, mbb, a, s);
         else if (cg == 1)
-            e = launch_res<1, 256, 8>(mx, mxb, ma, mbb, a, s);
+            e = launch_res<1, 256, 8>(mx, mxb, ma, mbb, ar, s);
         else if (FASTED_KNOB("FASTED_RES_EPI", 16) != 16)
-            e = launch_res<2, 256, 8>(mx, mxb, ma, mbb, a, s);
+            e = launch_res<2, 256, 8>(mx, mxb, ma, mbb, ar, s);
         else if (FASTED_KNOB("FASTED_RES_DIRECT", 0) != 0)
             e = launch_res<2, 256, 16, -1>(mx, mxb, ma, mbb, ar, s);
         else if (FASTED_KNOB("FASTED_RES_HIT", 0) == RING_NHIT)
@@ -3232,7 +3232,7 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     if (variant == TC_MULTICAST) {
 #ifdef FASTED_EXPERIMENTS
         if (FASTED_KNOB("FASTED_MC_EPI", 16) == 8)
-            e = launch_mc<8>(mx, ma, mb, a, s);
+            e = launch_mc<8>(mx, ma, mb, ar, s);
         else
 #endif
             e = mc_hit(a.sparse != 0) ? launch_mc<16, 2>(mx, ma, mb, ar, s)
@@ -3259,15 +3259,15 @@ int launch_join_tc(const __half* X, const JoinArgs& a, cudaStream_t s) {
     // pacing, one block of 64 tile layers (C4 on a box whose pairs drifted: HBM reads
     // 5.45 TB -> 121 GB per launch, L2 hit 59 -> 98%, 1738 -> 1327 ms; profiles/round2/
     // stream_pacing_ab.txt)
-    sch.pace_w = cg == 2 ? FASTED_KNOB("FASTED_STREAM_PACE_W", 1) : 0;
+    sch.pace_w = (cg == 2 && ar.pace) ? FASTED_KNOB("FASTED_STREAM_PACE_W", 1) : 0;
     // CTA pair: 16 epilogue warps of 64 columns (8 of 128: 1M x 960
     // 1466-1472 vs 1450-1491 TFLOPS, even; 5M x 384 shard at S <= 64:
     // 1917-1946 vs 2060-2253 ms, profiles/round1/tune_sepi_session2.txt)
 #ifdef FASTED_EXPERIMENTS
     if (cg == 1)
-        e = launch_variant<1>(mx, ma, mb, a, sch, s);
+        e = launch_variant<1>(mx, ma, mb, ar, sch, s);
     else if (FASTED_KNOB("FASTED_STREAM_EPI", 16) == 8)
-        e = launch_variant<2>(mx, ma, mb, a, sch, s);
+        e = launch_variant<2>(mx, ma, mb, ar, sch, s);
     else
 #endif
         e = stream_hit(a.sparse != 0) ? launch_variant<2, false, 16, 2>(mx, ma, mb, ar, sch, s)
