@@ -2015,7 +2015,10 @@ struct ResSched {
 // Records per staging buffer in the resident kernel (tight shared memory):
 // 8 KB for the epilogue in total, so the B ring keeps its 7 stages at d = 128
 // (16 KB cost a stage: no-epilogue 204 vs 174 ms at 1M x 128).
-constexpr int RES_WSTAGE_TOTAL = 256;   // records, all epilogue warps x 2 buffers
+#ifndef FASTED_RES_WSTAGE
+#define FASTED_RES_WSTAGE 256
+#endif
+constexpr int RES_WSTAGE_TOTAL = FASTED_RES_WSTAGE;   // records, all epilogue warps x 2 buffers
 
 template <int CG, int TBN>
 struct ResCfg {
