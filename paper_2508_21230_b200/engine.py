@@ -489,7 +489,7 @@ def form_hints(expected_pairs: int, rows, cols) -> int:
     if expected_pairs * SPARSE_EXAMINED_PER_PAIR <= nr * nc:
         f |= _lib.JOIN_SPARSE
     return f
-PIPELINE_CHUNKS = 4                 # chunks for mid-size outputs (overlap)
+PIPELINE_CHUNKS = 2                 # chunks for mid-size outputs (overlap; C4 e2e 1.304 vs 1.311 s at 4)
 BYTES_PER_RECORD_IN_FLIGHT = 2 * 16 + 2 * 12 + 8   # raw x2, sorted x2, sort scratch
 
 
