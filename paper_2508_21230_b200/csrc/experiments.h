@@ -56,7 +56,10 @@ enum {
     // complete_tx (results stay valid; A/B of the hand-off)
     FASTED_JOIN_DIAG_GENERICQ = 67108864,
     // epilogue warps wait for the accumulator by test_wait spin (results valid)
-    FASTED_JOIN_DIAG_EPISPIN = 134217728
+    FASTED_JOIN_DIAG_EPISPIN = 134217728,
+    // resident kernel with hit warps: one epilogue warp waits for the
+    // accumulator, the other 15 block on a named barrier (results valid)
+    FASTED_JOIN_DIAG_EPIBAR = 268435456
 };
 constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_NOEPI | FASTED_JOIN_DIAG_NOMMA | FASTED_JOIN_DIAG_LOADONLY |
@@ -65,7 +68,7 @@ constexpr int FASTED_JOIN_DIAG_ALL =
     FASTED_JOIN_DIAG_RARE_ROWS | FASTED_JOIN_DIAG_NOAUG | FASTED_JOIN_DIAG_AUGF16 |
     FASTED_JOIN_DIAG_HITMETA | FASTED_JOIN_DIAG_HITSKIP | FASTED_JOIN_DIAG_NOTMA |
     FASTED_JOIN_DIAG_NOREMOTE | FASTED_JOIN_DIAG_HITPACK | FASTED_JOIN_DIAG_GENERICQ |
-    FASTED_JOIN_DIAG_EPISPIN;
+    FASTED_JOIN_DIAG_EPISPIN | FASTED_JOIN_DIAG_EPIBAR;
 
 inline int env_int(const char* name, int dflt) {
     const char* v = getenv(name);
@@ -102,7 +105,8 @@ enum {
     FASTED_JOIN_DIAG_NOREMOTE = 0,
     FASTED_JOIN_DIAG_HITPACK = 0,
     FASTED_JOIN_DIAG_GENERICQ = 0,
-    FASTED_JOIN_DIAG_EPISPIN = 0
+    FASTED_JOIN_DIAG_EPISPIN = 0,
+    FASTED_JOIN_DIAG_EPIBAR = 0
 };
 
 #endif

@@ -1242,12 +1242,21 @@ __device__ __forceinline__ void res_epi_tile_hit(const JoinArgs& a, uint32_t reg
                                                  bool local_release, bool spin,
                                                  uint32_t sleep_ns, int dflags, int nchunks,
                                                  bool fast, int jb, int i, int iw, bool row_ok,
-                                                 uint32_t lane, unsigned long long* tr = nullptr) {
+                                                 uint32_t lane, unsigned long long* tr = nullptr,
+                                                 bool waiter = false) {
+    constexpr int NEPI_BAR = 16;   // the resident kernel's epilogue warps
     constexpr int HALF = TBN / NSPLIT;
     constexpr int NCH = HALF / 32;
     static_assert(NCH == 2, "hit-warp epilogue: 64 columns per warp");
-    if (dflags & FASTED_JOIN_DIAG_EPISPIN) mbar_spin(tfull, aph);
-    else epi_wait(tfull, aph, spin, sleep_ns);
+    if (dflags & FASTED_JOIN_DIAG_EPIBAR) {
+        // one waiter per CTA; the rest sleep in a hardware barrier (no re-polls)
+        if (waiter) epi_wait(tfull, aph, spin, sleep_ns);
+        asm volatile("bar.sync 1, %0;" ::"r"(NEPI_BAR * 32) : "memory");
+    } else if (dflags & FASTED_JOIN_DIAG_EPISPIN) {
+        mbar_spin(tfull, aph);
+    } else {
+        epi_wait(tfull, aph, spin, sleep_ns);
+    }
     tc_fence_after();
     if (TRACE && tr && lane == 0) tr[0] = clock64();
     uint32_t r0[32], r1[32];
@@ -2418,7 +2427,7 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
                                           : (warp - FIRST_EPI_WARP) % hit_warps(NHIT),
                         tcol0 + buf * TBN, tfull0 + 8u * buf, aph, release0 + 8u * buf,
                         local_release, spin, sch.epi_sleep_ns, dflags, nchunks, fast, jb, i, iw,
-                        row_ok, (uint32_t)lane, tr);
+                        row_ok, (uint32_t)lane, tr, warp == FIRST_EPI_WARP);
                 else
                     res_epi_tile<CG, TBN, NSPLIT, TRACE>(
                         a, wr, tcol0 + buf * TBN, tfull0 + 8u * buf, aph,

@@ -72,7 +72,7 @@ for r in range(rounds + 1):
         e1.synchronize()
         # diagnostic flags (>= 256) invalidate results, except the hit-search /
         # hand-off A/B flags (RARE_LM, RARE_ROWS, HITPACK, GENERICQ)
-        if extra.get("F", 0) & ~(131072 | 262144 | 33554432 | 67108864 | 134217728) < 256:
+        if extra.get("F", 0) & ~(131072 | 262144 | 33554432 | 67108864 | 134217728 | 268435456) < 256:
             assert int(cnt[0]) == ref, (st, int(cnt[0]), ref)
         if r:   # round 0 warms up every setting
             times[st].append(e0.elapsed_time(e1))
