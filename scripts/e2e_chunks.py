@@ -17,10 +17,10 @@ hd = F.to_half(F.generate_synthetic(n, d, seed=SEED), pin_host=True)
 hd_host = F.HalfDataset(hd.n_logical, hd.d_logical, hd.values, hd.norms)
 del hd
 torch.cuda.empty_cache()
-res = {k: [] for k in (1, 2, 4, 8)}
+res = {k: [] for k in ((2, False), (2, True), (4, False), (4, True), (1, False))}
 for r in range(4):
     for k in res:
-        engine.PIPELINE_CHUNKS = k
+        engine.PIPELINE_CHUNKS, engine.TAPER_CHUNKS = k
         st = F.EngineStats()
         t0 = time.perf_counter()
         rs = F.self_join(hd_host, eps, stats_out=st)
@@ -32,5 +32,5 @@ for r in range(4):
             res[k].append((dt, st.kernel_wall_seconds, st.per_device[0]["chunks"]))
         del rs
 for k, v in res.items():
-    print(f"chunks {k}: wall median {statistics.median(x[0] for x in v):.4f} s, kernels "
+    print(f"chunks/taper {k}: wall median {statistics.median(x[0] for x in v):.4f} s, kernels "
           f"{statistics.median(x[1] for x in v):.4f} s, chunks used {v[0][2]}", flush=True)

@@ -291,6 +291,22 @@ def test_plan_row_chunks():
     assert engine.plan_row_chunks((128, 128), 10, 1, 4) == [(128, 128)]
 
 
+def test_taper_chunks():
+    """k >= 2 equal chunks -> k + 1 contiguous 128-aligned chunks, first and
+    last half-size, none larger than the equal split."""
+    eq = engine.plan_row_chunks((0, 1000064), 49e6, 1e9, 2)
+    ch = engine.taper_chunks(eq)
+    assert len(ch) == 3 and ch[0][0] == 0 and ch[-1][1] == 1000064
+    assert all(a[1] == b[0] for a, b in zip(ch, ch[1:]))
+    assert all(c[0] % 128 == 0 and c[1] % 128 == 0 for c in ch)
+    size = [b - a for a, b in ch]
+    assert max(size) <= max(b - a for a, b in eq) and size[0] * 2 <= size[1] + 128
+    assert engine.taper_chunks([(0, 1024)]) == [(0, 1024)]
+    assert engine.taper_chunks([(0, 128), (128, 256)]) == [(0, 128), (128, 256)]
+    four = engine.taper_chunks(engine.plan_row_chunks((256, 256 + 128 * 1000), 1e9, 3e8, 1))
+    assert len(four) == 5 and four[0][0] == 256 and four[-1][1] == 256 + 128 * 1000
+
+
 def test_kernel_selection_rule_is_host_side(monkeypatch):
     """fasted_join_kernel_name applies the launch's selection rule without a
     GPU: resident pair for d_pad <= 512, the CTA pair for large low-output
