@@ -169,6 +169,24 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu_u64(const unsigned 
     return v;
 }
 
+// Pacing wait: until `need` units were issued by all CTAs, at most
+// PACE_GIVE_UP_NS.  Pacing is a locality aid, never a dependency: if the other
+// CTAs are not resident (another kernel holds SMs -- e.g. two joins launched
+// concurrently on one device) the wait would never end, so the CTA stops
+// pacing for the rest of the launch instead (normal waits are microseconds).
+constexpr uint64_t PACE_GIVE_UP_NS = 5000000ull;   // 5 ms
+__device__ __forceinline__ void pace_wait(const unsigned long long* pace,
+                                          unsigned long long need, bool& paced) {
+    const uint64_t t0 = global_timer();
+    while (ld_acquire_gpu_u64(pace) < need) {
+        __nanosleep(64);
+        if (global_timer() - t0 > PACE_GIVE_UP_NS) {
+            paced = false;
+            return;
+        }
+    }
+}
+
 // Spin on an mbarrier phase; traps after 20 s so a protocol bug aborts the
 // launch (cudaErrorLaunchFailure) instead of wedging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
@@ -1509,21 +1527,17 @@ join_tc_kernel(const __grid_constant__ CUtensorMap tmap_x,
             int s = 0;
             uint32_t ph = 0;
             int64_t k = 0;   // this CTA's tile layer
+            bool paced = true;   // lane 0's: cleared if a pacing wait gives up
             for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++k) {
                 if (sch.pace_w > 0 && k % PACE_TILES == 0 && k > 0) {
                     const int64_t b = k / PACE_TILES;   // block b - 1 issued; gate block b
                     if (lane == 0) {
                         asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.pace)
                                      : "memory");
-                        if (b >= sch.pace_w) {
-                            const unsigned long long need =
-                                pace_need_stream(sch.total, tile_step, b - sch.pace_w, CG);
-                            const uint64_t t0 = global_timer();
-                            while (ld_acquire_gpu_u64(a.pace) < need) {
-                                __nanosleep(64);
-                                if (global_timer() - t0 > 20000000000ull) __trap();
-                            }
-                        }
+                        if (paced && b >= sch.pace_w)
+                            pace_wait(a.pace,
+                                      pace_need_stream(sch.total, tile_step, b - sch.pace_w, CG),
+                                      paced);
                     }
                     __syncwarp();
                 }
@@ -1832,21 +1846,16 @@ join_tc_mc_kernel(const __grid_constant__ CUtensorMap tmap_x,
         int s = 0;
         uint32_t ph = 0;
         int64_t k = 0;   // this cluster's tile layer (pacing, as the streaming kernel)
+        bool paced = true;
         for (int64_t t = tile_id0; t < sch.total; t += tile_step, ++k) {
             if (sch.pace_w > 0 && k % PACE_TILES == 0 && k > 0) {
                 const int64_t b = k / PACE_TILES;
                 if (lane == 0) {
                     asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(a.pace)
                                  : "memory");
-                    if (b >= sch.pace_w) {
-                        const unsigned long long need =
-                            pace_need_stream(sch.total, tile_step, b - sch.pace_w, 2);
-                        const uint64_t t0 = global_timer();
-                        while (ld_acquire_gpu_u64(a.pace) < need) {
-                            __nanosleep(64);
-                            if (global_timer() - t0 > 20000000000ull) __trap();
-                        }
-                    }
+                    if (paced && b >= sch.pace_w)
+                        pace_wait(a.pace, pace_need_stream(sch.total, tile_step, b - sch.pace_w, 2),
+                                  paced);
                 }
                 __syncwarp();
             }
@@ -2197,16 +2206,11 @@ join_tc_res_kernel(const __grid_constant__ CUtensorMap tmap_xa,
             int s = 0;
             uint32_t ph = 0;
             int ua = 0;
+            bool paced = true;   // lane 0's: cleared if a pacing wait gives up
             for (int64_t u = unit0; u < sch.units; u += ustep, ++ua) {
                 if (sch.pace_w > 0 && ua >= sch.pace_w) {
-                    if (lane == 0) {
-                        const unsigned long long need = pace_need(sch, ua - sch.pace_w, CG);
-                        const uint64_t t0 = global_timer();
-                        while (ld_acquire_gpu_u64(a.pace) < need) {
-                            __nanosleep(64);
-                            if (global_timer() - t0 > 20000000000ull) __trap();
-                        }
-                    }
+                    if (lane == 0 && paced)
+                        pace_wait(a.pace, pace_need(sch, ua - sch.pace_w, CG), paced);
                     __syncwarp();
                 }
                 int rt, ct0, ct1;

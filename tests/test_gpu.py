@@ -814,6 +814,42 @@ def test_pacing_layer_counts_complete(symmetric):
         assert len(one[0]) > 20000 and _same(one, res), w
 
 
+def test_concurrent_paced_joins_complete():
+    """Two joins launched at once on two streams of one device: each grid
+    holds one CTA per SM, so the block scheduler can leave each kernel only
+    partly resident.  Pacing must not turn that into a deadlock (a producer
+    waiting for CTAs that cannot be scheduled until the other kernel ends): a
+    pacing wait gives up after 5 ms.  Both launches finish and each equals the
+    same join run alone, bit for bit."""
+    import torch
+
+    hd = F.to_half(F.generate_synthetic(60000, 128, seed=61))
+    dd = engine.upload(hd, 0)
+    es = float(np.float32(np.float32(3.7) ** 2))
+    rows, cols = (0, dd.n_dev), (0, dd.n_dev)
+    alone = engine.join_device(dd, es, rows=rows, sort=False)
+    cap = alone.count + engine.hole_slack(0)
+    ref = engine.to_host(engine.join_device(dd, es, rows=rows))
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    recs = [torch.empty((cap, 4), dtype=torch.int32, device="cuda") for _ in range(2)]
+    cnts = [torch.zeros(2, dtype=torch.int64, device="cuda") for _ in range(2)]
+    torch.cuda.synchronize()
+    for _ in range(3):
+        for k in range(2):
+            engine.join_raw(dd, es, _lib.JOIN_TC, rows, cols, recs[k], cap, cnts[k],
+                            streams[k].cuda_stream)
+    torch.cuda.synchronize()
+    for k in range(2):
+        assert int(cnts[k][0].item()) == alone.count
+        slots = int(cnts[k][1].item()) * engine.RECORD_CHUNK
+        raw = recs[k][:slots].cpu().numpy()
+        raw = raw[raw[:, 0] != 0]
+        order = np.lexsort((raw[:, 1].view(np.uint32), raw[:, 0].view(np.uint32)))
+        got = (raw[order, 0].view(np.uint32), raw[order, 1].view(np.uint32),
+               raw[order, 2].view(np.float32))
+        assert _same(ref, got)
+
+
 def test_sort_long_rows_bucket_and_fallback_paths():
     """Rows above 16384 records: spread j -> column buckets + shared-memory
     bitonic per bucket; j clustered in one bucket -> the bitmap fallback.
