@@ -17,10 +17,21 @@ hd = F.to_half(F.generate_synthetic(n, d, seed=SEED), pin_host=True)
 hd_host = F.HalfDataset(hd.n_logical, hd.d_logical, hd.values, hd.norms)
 del hd
 torch.cuda.empty_cache()
-res = {k: [] for k in ((2, False), (2, True), (4, False), (4, True), (1, False))}
+_plan = engine.plan_row_chunks
+
+
+def head_plan(rows, est, budget, min_chunks=1, frac=16):
+    """a first chunk of ~1/frac of the rows (starts after 1/frac of the upload), then the plan"""
+    r0, r1 = rows
+    cut = r0 + max(1, (r1 - r0) // engine.BLOCK // frac) * engine.BLOCK
+    return [(r0, cut)] + _plan((cut, r1), est, budget, min_chunks)
+
+
+res = {k: [] for k in ((2, False, 0), (2, False, 16), (2, False, 8), (1, False, 16))}
 for r in range(4):
     for k in res:
-        engine.PIPELINE_CHUNKS, engine.TAPER_CHUNKS = k
+        engine.PIPELINE_CHUNKS, engine.TAPER_CHUNKS = k[0], k[1]
+        engine.plan_row_chunks = (lambda *a, f=k[2]: head_plan(*a, frac=f)) if k[2] else _plan
         st = F.EngineStats()
         t0 = time.perf_counter()
         rs = F.self_join(hd_host, eps, stats_out=st)
