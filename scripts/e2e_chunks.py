@@ -18,6 +18,7 @@ hd_host = F.HalfDataset(hd.n_logical, hd.d_logical, hd.values, hd.norms)
 del hd
 torch.cuda.empty_cache()
 _plan = engine.plan_row_chunks
+_upload = engine.upload_segmented
 
 
 def head_plan(rows, est, budget, min_chunks=1, frac=16):
@@ -27,10 +28,11 @@ def head_plan(rows, est, budget, min_chunks=1, frac=16):
     return [(r0, cut)] + _plan((cut, r1), est, budget, min_chunks)
 
 
-res = {k: [] for k in ((2, False, 0), (2, False, 16), (2, False, 8), (1, False, 16))}
+res = {k: [] for k in ((2, False, 0, 16), (2, False, 0, 8), (2, False, 0, 4), (2, False, 0, 32))}
 for r in range(4):
     for k in res:
         engine.PIPELINE_CHUNKS, engine.TAPER_CHUNKS = k[0], k[1]
+        engine.upload_segmented = (lambda hd, dev, _s=k[3], _f=_upload: _f(hd, dev, segments=_s))
         engine.plan_row_chunks = (lambda *a, f=k[2]: head_plan(*a, frac=f)) if k[2] else _plan
         st = F.EngineStats()
         t0 = time.perf_counter()
