@@ -2933,7 +2933,13 @@ static cudaError_t launch_res(const CUtensorMap& mxa, const CUtensorMap& mxb,
     // because a row's records spread over the launch -- profiles/round2/unit_order_ab.txt)
     sch.order = FASTED_KNOB("FASTED_RES_ORDER", 1);
     sch.mma_spin = FASTED_KNOB("FASTED_MMA_SPIN", MMA_SPIN_DEFAULT);
-    int seg = FASTED_KNOB("FASTED_SEG_TILES", 16384 / TBN);
+    // ~16K columns per unit; 64K with hit warps (sparse output) and a
+    // single-buffered A panel (d_pad > 256), whose reload every unit then
+    // shows: C5 shard S~16 / eps 0 1532 / 1534 vs 1554 / 1553 ms; dense output
+    // and C2 prefer 16K (S~1024 1630 vs 1647, C2 2.60 vs 3.05 ms;
+    // profiles/round2/segment_length_single_a_ab.txt)
+    int seg = FASTED_KNOB("FASTED_SEG_TILES",
+                          (NHIT > 0 && sch.na == 1 ? 65536 : 16384) / TBN);
     if (seg < 1) seg = 1;
     sch.nsegs = (sch.col_tiles + seg - 1) / seg;
     sch.units = (int64_t)sch.row_tiles * sch.nsegs;
