@@ -462,7 +462,8 @@ def main():
     ap.add_argument("--workload", default="C4", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="fasted", choices=["fasted", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--ref-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", type=float, default=5.0,
+                    help="CPU seconds per reference-arm step (a bounded sample of the workload)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-accuracy", action="store_true")
     ap.add_argument("--no-symmetric", action="store_true")
